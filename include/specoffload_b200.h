@@ -1,0 +1,150 @@
+/*
+ * specoffload_b200.h — C ABI of the B200-native offloaded speculative-decoding
+ * hot path (SpecOffload, arXiv 2505.10259).
+ *
+ * The reference (`specpipe`, /root/reference/pkg) is a Python performance model
+ * with no FFI; the path it models is entered through
+ *   simulate_decoding(policy, workload, hw, target, draft, plan, seed)
+ *       pkg/src/specpipe/simulator.py:108-116
+ * whose per-round, per-layer body (simulator.py:155-215) is
+ *   attention ‖ FFN C2G load  →  FFN compute  →  barrier → sample_accepted
+ * Each entry point below is one of the physical operations that loop models;
+ * the comment on each names the reference line it replaces.  The Python host
+ * layer (paper_2505_10259_b200/native.py) binds these with ctypes.
+ *
+ * Conventions:
+ *  - every call is asynchronous on the caller's cudaStream_t (passed as void*);
+ *  - all pointers are device pointers unless named *_host / pinned;
+ *  - the caller owns every buffer; the library never allocates or frees
+ *    caller-visible memory and keeps no per-call state;
+ *  - return 0 on success, a negative SO_E_* code for argument errors, or a
+ *    positive cudaError_t for launch failures.  Nothing throws or aborts.
+ *  - bf16 tensors are passed as `const void*` (uint16 bit patterns).
+ */
+#ifndef SPECOFFLOAD_B200_H
+#define SPECOFFLOAD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SO_OK 0
+#define SO_E_NULLPTR (-1)
+#define SO_E_SHAPE (-2)
+#define SO_E_ALIGN (-3)
+#define SO_E_UNSUPPORTED (-4)
+#define SO_E_DRIVER (-5)
+
+/* GEMM epilogues (so_gemm_bf16 / grouped GEMMs). */
+#define SO_EPI_BF16 0          /* C = A·Bᵀ                         (bf16 out) */
+#define SO_EPI_F32 1           /* C = A·Bᵀ                         (fp32 out) */
+#define SO_EPI_BF16_RESID 2    /* C = A·Bᵀ + R                     (bf16 out) */
+#define SO_EPI_SWIGLU 3        /* C = silu(A·Bgᵀ) ⊙ (A·Buᵀ), B rows interleaved in 64-row gate/up blocks */
+#define SO_EPI_BF16_ROWSCALE 4 /* C[r,:] = w[r] · (A·Bᵀ)[r,:]      (bf16 out) */
+
+int so_abi_version(void);
+const char* so_status_string(int status);
+int so_device_sm_count(void);
+
+/* ---- K7: speculative accept / reject ------------------------------------
+ * Replaces the statistical draw `sample_accepted` (acceptance.py:55-72,
+ * called at simulator.py:213) and the clamp `remaining - accepted`
+ * (simulator.py:214) with the real decision on target logits.
+ * Greedy: n = leading count of draft[i] == argmax(logits[i]) (lowest index on
+ * ties); emit draft[0:n] ++ [argmax(logits[n])]; count = min(n+1, remaining).
+ * forced_accept (optional, may be NULL) replaces n by min(forced-1, n_cand)
+ * (forced-acceptance benchmark mode).
+ * out_tokens [bs, n_cand+1] (entries past count are -1), out_counts [bs]. */
+int so_accept_greedy(const int32_t* draft_tokens, const float* target_logits,
+                     const int32_t* remaining, const int32_t* forced_accept,
+                     int bs, int n_cand, int vocab,
+                     int32_t* out_tokens, int32_t* out_counts, void* stream);
+
+/* Sampling verification (Leviathan et al. Alg. 1): accept draft token i iff
+ * u_accept[i]·q_i(d_i) ≤ p_i(d_i), p = softmax(inv_temp·logits) in the
+ * canonical deterministic order; on the first rejection
+ * sample norm(max(p_i−q_i,0)) with u_resample, else the bonus from p_n. */
+int so_accept_sample(const int32_t* draft_tokens, const float* target_logits,
+                     const float* draft_probs, const float* u_accept,
+                     const float* u_resample, const int32_t* remaining,
+                     float inv_temperature, int bs, int n_cand, int vocab,
+                     int32_t* out_tokens, int32_t* out_counts, void* stream);
+
+/* Draft-side token choice: greedy argmax (uniforms == NULL) or inverse-CDF
+ * sampling from softmax(inv_temp·logits); optionally writes the normalised
+ * probabilities (needed by so_accept_sample).  logits may be strided rows. */
+int so_sample_tokens(const float* logits, int64_t row_stride, const float* uniforms,
+                     float inv_temperature, int rows, int vocab,
+                     int32_t* out_tokens, int64_t token_stride,
+                     float* out_probs, int64_t probs_row_stride, void* stream);
+
+/* ---- K2: fused top-2 router + token permutation --------------------------
+ * Mixtral routing: logits = x·Wgᵀ (fp32 accumulate), fp32 softmax, top-2
+ * (ties → lower expert), renormalise by the pair sum.  Produces a stable
+ * (token-ordered) expert-major permutation so the grouped GEMMs see one
+ * contiguous row block per expert.
+ * outputs: expert_offsets [E+1]; perm_token [2T] (row → token);
+ * row_weight [2T] (routing weight of the row); token_rows [T,2] (token →
+ * its two rows); x_perm [2T,H] (gathered activations);
+ * topk_idx [T,2] / topk_w [T,2] (for inspection, may be NULL).
+ * workspace: so_router_workspace_bytes(T, E) bytes of device scratch. */
+size_t so_router_workspace_bytes(int T, int E);
+int so_router_top2(const void* x, const void* w_gate, int T, int H, int E,
+                   int32_t* topk_idx, float* topk_w, int32_t* expert_offsets,
+                   int32_t* perm_token, float* row_weight, int32_t* token_rows,
+                   void* x_perm, void* workspace, void* stream);
+
+/* out[t] = resid[t] + y[token_rows[t,0]] + y[token_rows[t,1]] (fixed order) */
+int so_moe_combine(const void* y_perm, const int32_t* token_rows, const void* resid,
+                   int T, int H, void* out, void* stream);
+
+/* ---- K3/K4/K5: tcgen05 GEMMs (bf16 in, fp32 accumulate in TMEM) ---------
+ * C[M,N] = A[M,K] · B[N,K]ᵀ, both K-major, K % 64 == 0, 16-B aligned rows.
+ * epilogue SO_EPI_*; aux = residual (bf16 [M,ldc]) or row scale (fp32 [M]).
+ * For SO_EPI_SWIGLU, N counts the interleaved gate+up rows and C has N/2
+ * columns. */
+int so_gemm_bf16(const void* A, const void* B, int M, int N, int K,
+                 void* C, int ldc, int epilogue, const void* aux, void* stream);
+
+/* Grouped (MoE) GEMM: rows [offs[e], offs[e+1]) of A use expert e's weight
+ * B + e·N·K.  max_rows bounds offs[E] (no host sync: the tile schedule is
+ * derived on device from offs). */
+int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_offsets,
+                         int E, int max_rows, int N, int K, void* C, int ldc,
+                         int epilogue, const void* aux, void* stream);
+
+/* ---- K8: auxiliary ------------------------------------------------------- */
+int so_embed(const int32_t* tokens, const void* table, int T, int H, void* out, void* stream);
+int so_rmsnorm(const void* x, const void* w, int T, int H, float eps, void* out, void* stream);
+/* qkv [T, (hq+2hkv)·dh] → RoPE(q) into q_out [T,hq,dh]; RoPE(k), v appended
+ * to the paged caches at slot_mapping[t] (page·page_size + offset).
+ * cache layout: [num_pages, hkv, page_size, dh]. */
+int so_rope_kv_append(const void* qkv, const int32_t* positions, const int32_t* slot_mapping,
+                      int T, int hq, int hkv, int dh, float rope_theta, int page_size,
+                      void* q_out, void* k_cache, void* v_cache, void* stream);
+
+/* ---- K6: multi-token verification attention over the paged KV cache ------
+ * Sequence s owns query rows [q_start[s], q_start[s+1]); query row j of s
+ * sits at position kv_before[s] + j and attends keys [0, kv_before[s]+j]
+ * (causal inside the new tokens).  GQA: q head h reads kv head h/(hq/hkv).
+ * out [rows, hq·dh] bf16. */
+int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
+                  const int32_t* block_table, int max_pages,
+                  const int32_t* q_start, const int32_t* kv_before,
+                  int bs, int max_q, int hq, int hkv, int dh, int page_size,
+                  float scale, void* out, void* stream);
+
+/* ---- K1: layer streamer -------------------------------------------------
+ * Pinned host → HBM window slot, `chunk`-byte cudaMemcpyAsync pieces on the
+ * caller's copy stream, then records `done_event` (may be NULL).
+ * Replaces the modeled `ffn_load` event (simulator.py:172-176). */
+int so_stream_layer(void* slot, const void* pinned_src, size_t bytes, size_t chunk,
+                    void* stream, void* done_event);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECOFFLOAD_B200_H */

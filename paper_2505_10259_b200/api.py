@@ -1,0 +1,47 @@
+"""User-facing construction of the offloaded target/draft pair.
+
+``build_engine`` is what a caller of the reference would reach for after
+``assign_tiers`` (placement.py:167): it takes the target FFN layers the plan
+streams (the rest stay pinned in HBM), places the streamed ones in pinned host
+memory, creates the two-or-more-slot HBM window and returns an ``Engine``.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import weights as W
+from .config import ModelArch
+from .engine import Engine
+from .models import DraftModel, TargetModel
+from .streamer import HostStore, LayerStreamer
+
+
+def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: dict | None = None,
+                 draft_weights: dict | None = None, device="cuda:0", stream_layers=None, n_slots: int = 2,
+                 seed: int = 0, trace: bool = True, page_size: int = 64, host_store: HostStore | None = None,
+                 chunk_bytes: int = 256 << 20) -> Engine:
+    """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
+    synthetic random init of the architecture.  ``stream_layers`` = target
+    FFN layers kept in pinned host DRAM and streamed each pass (default:
+    all of them — the fully offloaded configuration)."""
+    dev = torch.device(device)
+    if stream_layers is None:
+        stream_layers = set(range(target_arch.n_layer))
+    stream_layers = set(stream_layers)
+    if target_weights is not None:
+        tw = W.from_logical(target_arch, target_weights, dev, stream_layers)
+    else:
+        store = host_store or HostStore()
+        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc)
+    if draft_weights is not None:
+        dw = W.from_logical(draft_arch, draft_weights, dev)
+    else:
+        dw = W.synthetic(draft_arch, dev, seed=seed + 1)
+    _, _, ffn_bytes = W.ffn_offsets(target_arch)
+    resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
+    host = {li: t.view(torch.uint8) for li, t in tw.host_ffn.items()}
+    streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
+                             chunk_bytes=chunk_bytes) if host else None
+    target = TargetModel(tw, dev, streamer)
+    draft = DraftModel(dw, dev)
+    return Engine(target, draft, device=dev, page_size=page_size, trace=trace)

@@ -1,0 +1,286 @@
+// K6 — multi-token verification attention over the paged KV cache.
+//
+// In the paper this is the CPU attention the reference charges as
+// `n_cand · bs · t_attn_cpu` per layer (costmodel.py:73, simulator.py:169-171,
+// PAPER.md:157).  On B200 the target KV lives in HBM and the
+// verify pass attends n_cand+1 new query positions per sequence over
+// ctx + n_cand + 1 keys, causally inside the new block.  The same kernel serves
+// prefill (q_len = prompt length).
+//
+// Work unit: one CTA (4 warps) per (sequence, kv-head, 64-row query tile).  The
+// rows of a (sequence, kv-head) pair are all q_len positions × the G = hq/hkv
+// query heads sharing that KV head (GQA), so each K/V tile read from HBM feeds
+// every query head of the group.  K/V tiles of 64 keys are staged with 16-B
+// cp.async into an XOR-swizzled, double-buffered smem ring (one page = one
+// contiguous [page_size, dh] block per kv-head, so a tile is one coalesced
+// 8–16 KB run); S = QKᵀ and O += PV run on bf16 mma.sync with fp32 accumulate;
+// the softmax is the online (flash) form with quad-shuffle row reductions.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kRows = 64;   // query rows per CTA (4 warps × 16)
+constexpr int kKeys = 64;   // keys per smem tile
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int DH>
+struct Tile {
+  static constexpr int kChunks = DH / 8;                 // 16-B chunks per key row
+  static constexpr int kBytes = kKeys * DH * 2;          // one K or V tile
+  // swizzled byte offset of (key row, chunk)
+  __device__ __forceinline__ static uint32_t off(int row, int chunk) {
+    return (uint32_t)(row * DH * 2 + ((chunk ^ (row & 7)) << 4));
+  }
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads) attn_paged_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
+    const int32_t* __restrict__ block_table, int max_pages, const int32_t* __restrict__ q_start,
+    const int32_t* __restrict__ kv_before, int hq, int hkv, int page_size, float scale_log2,
+    __nv_bfloat16* __restrict__ out) {
+  using TL = Tile<DH>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tile = blockIdx.x, g_kv = blockIdx.y, s = blockIdx.z;
+  const int G = hq / hkv;
+  const int qs = q_start[s];
+  const int q_len = q_start[s + 1] - qs;
+  const int rows_total = q_len * G;
+  const int r0 = tile * kRows;
+  if (r0 >= rows_total) return;
+  const int kvb = kv_before[s];
+  const int j_last = min(q_len - 1, (r0 + kRows - 1) / G);
+  const int n_keys = kvb + j_last + 1;
+  const int n_tiles = (n_keys + kKeys - 1) / kKeys;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+
+  // ---- Q fragments (A operand, row-major [16 rows × DH]) ----
+  const int rA = r0 + warp * 16 + g, rB = rA + 8;
+  const bool vA = rA < rows_total, vB = rB < rows_total;
+  const int jA = vA ? rA / G : 0, jB = vB ? rB / G : 0;
+  const int hA = g_kv * G + (vA ? rA % G : 0), hB = g_kv * G + (vB ? rB % G : 0);
+  const __nv_bfloat16* qA = q + ((size_t)(qs + jA) * hq + hA) * DH;
+  const __nv_bfloat16* qB = q + ((size_t)(qs + jB) * hq + hB) * DH;
+  const bool warp_live = (r0 + warp * 16) < rows_total;
+  uint32_t qf[DH / 16][4];
+#pragma unroll
+  for (int ks = 0; ks < DH / 16; ++ks) {
+    const int d0 = ks * 16 + 2 * c;
+    qf[ks][0] = vA ? *reinterpret_cast<const uint32_t*>(qA + d0) : 0u;
+    qf[ks][1] = vB ? *reinterpret_cast<const uint32_t*>(qB + d0) : 0u;
+    qf[ks][2] = vA ? *reinterpret_cast<const uint32_t*>(qA + d0 + 8) : 0u;
+    qf[ks][3] = vB ? *reinterpret_cast<const uint32_t*>(qB + d0 + 8) : 0u;
+  }
+  const int limA = vA ? kvb + jA : -1;  // last key this row may see
+  const int limB = vB ? kvb + jB : -1;
+
+  float o[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+  float mA = -INFINITY, mB = -INFINITY, lA = 0.0f, lB = 0.0f;
+
+  const int32_t* bt = block_table + (size_t)s * max_pages;
+  auto load_tile = [&](int kt, int buf) {
+    const int key0 = kt * kKeys;
+    const int page = bt[key0 / page_size];
+    const size_t base = (((size_t)page * hkv + g_kv) * page_size + (key0 % page_size)) * DH;
+    uint8_t* sk = smem + buf * 2 * TL::kBytes;
+    uint8_t* sv = sk + TL::kBytes;
+#pragma unroll
+    for (int i = threadIdx.x; i < kKeys * TL::kChunks; i += kThreads) {
+      const int row = i / TL::kChunks, ch = i % TL::kChunks;
+      cp_async16(sk + TL::off(row, ch), kc + base + (size_t)row * DH + ch * 8);
+      cp_async16(sv + TL::off(row, ch), vc + base + (size_t)row * DH + ch * 8);
+    }
+  };
+
+  load_tile(0, 0);
+  cp_commit();
+  for (int kt = 0; kt < n_tiles; ++kt) {
+    if (kt + 1 < n_tiles) load_tile(kt + 1, (kt + 1) & 1);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (warp_live) {
+      const uint32_t sk = smem_u32(smem + (kt & 1) * 2 * TL::kBytes);
+      const uint32_t sv = sk + TL::kBytes;
+      // ---- S = Q Kᵀ  (16 rows × 64 keys per warp) ----
+      float sfr[kKeys / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < kKeys / 8; ++nt) sfr[nt][0] = sfr[nt][1] = sfr[nt][2] = sfr[nt][3] = 0.0f;
+      const int mat = lane >> 3, mi = lane & 7;
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks) {
+#pragma unroll
+        for (int nt = 0; nt < kKeys / 8; nt += 2) {
+          const int key = (nt + (mat >> 1)) * 8 + mi;
+          const int ch = ks * 2 + (mat & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(sk + TL::off(key, ch), b0, b1, b2, b3);
+          mma_bf16(sfr[nt], qf[ks], b0, b1);
+          mma_bf16(sfr[nt + 1], qf[ks], b2, b3);
+        }
+      }
+      // ---- mask + online softmax ----
+      const int key0 = kt * kKeys;
+      float tmA = -INFINITY, tmB = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < kKeys / 8; ++nt) {
+        const int k0 = key0 + nt * 8 + 2 * c;
+        sfr[nt][0] = k0 <= limA ? sfr[nt][0] * scale_log2 : -INFINITY;
+        sfr[nt][1] = k0 + 1 <= limA ? sfr[nt][1] * scale_log2 : -INFINITY;
+        sfr[nt][2] = k0 <= limB ? sfr[nt][2] * scale_log2 : -INFINITY;
+        sfr[nt][3] = k0 + 1 <= limB ? sfr[nt][3] * scale_log2 : -INFINITY;
+        tmA = fmaxf(tmA, fmaxf(sfr[nt][0], sfr[nt][1]));
+        tmB = fmaxf(tmB, fmaxf(sfr[nt][2], sfr[nt][3]));
+      }
+      tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, 1));
+      tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, 2));
+      tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 1));
+      tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, 2));
+      const float nmA = fmaxf(mA, tmA), nmB = fmaxf(mB, tmB);
+      const float baseA = nmA == -INFINITY ? 0.0f : nmA;
+      const float baseB = nmB == -INFINITY ? 0.0f : nmB;
+      const float corrA = exp2f(mA - baseA), corrB = exp2f(mB - baseB);
+      mA = nmA;
+      mB = nmB;
+      float rsA = 0.0f, rsB = 0.0f;
+      uint32_t pf[kKeys / 16][4];
+#pragma unroll
+      for (int nt = 0; nt < kKeys / 8; ++nt) {
+        const float p0 = exp2f(sfr[nt][0] - baseA), p1 = exp2f(sfr[nt][1] - baseA);
+        const float p2 = exp2f(sfr[nt][2] - baseB), p3 = exp2f(sfr[nt][3] - baseB);
+        rsA += p0 + p1;
+        rsB += p2 + p3;
+        // C-fragment → A-fragment of the PV product (k = keys)
+        const int kk = nt >> 1;
+        if ((nt & 1) == 0) {
+          pf[kk][0] = pack_bf16(p0, p1);
+          pf[kk][1] = pack_bf16(p2, p3);
+        } else {
+          pf[kk][2] = pack_bf16(p0, p1);
+          pf[kk][3] = pack_bf16(p2, p3);
+        }
+      }
+      lA = lA * corrA + rsA;
+      lB = lB * corrB + rsB;
+#pragma unroll
+      for (int dn = 0; dn < DH / 8; ++dn) {
+        o[dn][0] *= corrA;
+        o[dn][1] *= corrA;
+        o[dn][2] *= corrB;
+        o[dn][3] *= corrB;
+      }
+      // ---- O += P V ----
+#pragma unroll
+      for (int kk = 0; kk < kKeys / 16; ++kk) {
+#pragma unroll
+        for (int dn = 0; dn < DH / 8; dn += 2) {
+          const int key = kk * 16 + (mat & 1) * 8 + mi;
+          const int ch = dn + (mat >> 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(sv + TL::off(key, ch), b0, b1, b2, b3);
+          mma_bf16(o[dn], pf[kk], b0, b1);
+          mma_bf16(o[dn + 1], pf[kk], b2, b3);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  if (!warp_live) return;
+  // ---- normalise and store ----
+  lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+  lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+  const float invA = lA > 0.0f ? 1.0f / lA : 0.0f;
+  const float invB = lB > 0.0f ? 1.0f / lB : 0.0f;
+  __nv_bfloat16* oA = out + ((size_t)(qs + jA) * hq + hA) * DH;
+  __nv_bfloat16* oB = out + ((size_t)(qs + jB) * hq + hB) * DH;
+#pragma unroll
+  for (int dn = 0; dn < DH / 8; ++dn) {
+    const int d = dn * 8 + 2 * c;
+    if (vA) *reinterpret_cast<uint32_t*>(oA + d) = pack_bf16(o[dn][0] * invA, o[dn][1] * invA);
+    if (vB) *reinterpret_cast<uint32_t*>(oB + d) = pack_bf16(o[dn][2] * invB, o[dn][3] * invB);
+  }
+}
+
+template <int DH>
+int launch(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
+           const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
+           cudaStream_t st) {
+  const int G = hq / hkv;
+  const int tiles = (max_q * G + kRows - 1) / kRows;
+  const size_t smem = 2 * 2 * (size_t)Tile<DH>::kBytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  dim3 grid(tiles, hkv, bs);
+  attn_paged_kernel<DH><<<grid, kThreads, smem, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
+      reinterpret_cast<const __nv_bfloat16*>(v), bt, max_pages, q_start, kv_before, hq, hkv, page_size,
+      scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
+}  // namespace
+
+extern "C" int so_attn_paged(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
+                             int max_pages, const int32_t* q_start, const int32_t* kv_before, int bs, int max_q,
+                             int hq, int hkv, int dh, int page_size, float scale, void* out, void* stream) {
+  SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
+  SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
+  SO_REQUIRE(page_size % kKeys == 0, SO_E_SHAPE);
+  SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
+  if (bs == 0) return SO_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dh == 128) return launch<128>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+                                    page_size, scale, out, st);
+  if (dh == 64) return launch<64>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+                                  page_size, scale, out, st);
+  return SO_E_UNSUPPORTED;
+}

@@ -1,0 +1,446 @@
+// K3/K4/K5 — bf16 GEMMs on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   C[M,N] = A[M,K] · B[N,K]ᵀ            (dense: QKV / O / LM head / draft MLP)
+//   C[r,:] = A[r,:] · B_e[N,K]ᵀ, r ∈ [offs[e], offs[e+1])   (grouped: MoE experts)
+//
+// Where the reference models this work: the per-layer `ffn_gpu` event
+// (simulator.py:185-191, cost bs·t_ffn_gpu at costmodel.py:75) and the draft
+// granules (costmodel.py:53-57).  Shapes: SURVEY.md §2c K3–K5.
+//
+// Kernel structure (one CTA = one 128×BN output tile, 6 warps):
+//   warp 0      TMA producer: A/B k-slices (64 bf16 = 128 B rows, SWIZZLE_128B)
+//               into an S-stage smem ring, completion on `full[s]` mbarriers;
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=BN, K=16 per instruction, fp32 accumulator in TMEM),
+//               tcgen05.commit frees each smem stage on `empty[s]`;
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes × 32 columns per warp quarter,
+//               fused op (bf16 / fp32 / +residual / SwiGLU / row scale), store.
+// The grouped variant derives its M-tile → (expert, row0) map on device from
+// the router's expert offsets, so no host synchronisation is needed between
+// routing and the expert GEMMs.
+#include <cuda.h>
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int kThreads = 192;
+constexpr int kEpiWarp0 = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core groups
+// 1024 B apart (SBO), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1u << 16;              // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;    // SBO
+  d |= (uint64_t)1u << 46;              // descriptor version (Blackwell)
+  d |= (uint64_t)2u << 61;              // SWIZZLE_128B
+  return d;
+}
+
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc_bf16() {
+  // D=f32 (bits 4-5 = 1), A=bf16 (7-9 = 1), B=bf16 (10-12 = 1), both K-major,
+  // N>>3 at 17-22, M>>4 at 24-28.
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = BN;  // fp32 accumulator: one column per N
+  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C,
+                   int ldc, const void* __restrict__ aux) {
+  using CF = Cfg<BN>;
+  // ---- tile → (expert, row range) -------------------------------------------
+  const int mt = blockIdx.x;
+  const int nt = blockIdx.y;
+  int expert = 0, row0 = mt * BM, row_end = M;
+  if (offs != nullptr) {
+    int before = 0;
+    expert = -1;
+    for (int e = 0; e < E; ++e) {
+      const int lo = offs[e], hi = offs[e + 1];
+      const int nt_e = (hi - lo + BM - 1) / BM;
+      if (mt < before + nt_e) {
+        expert = e;
+        row0 = lo + (mt - before) * BM;
+        row_end = hi;
+        break;
+      }
+      before += nt_e;
+    }
+    if (expert < 0) return;  // tile beyond the routed rows (uniform across the CTA)
+  } else if (row0 >= M) {
+    return;
+  }
+  const int n0 = nt * BN;
+  const int num_kb = K / BK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::kStages * CF::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::kStages * CF::kStageBytes);
+  uint64_t* empty = full + CF::kStages;
+  uint64_t* tmem_full = empty + CF::kStages;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < CF::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % CF::kStages;
+        const uint32_t ph = (kb / CF::kStages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], CF::kStageBytes);
+        tma_load_2d(sA + s * CF::kABytes, &tmA, &full[s], kb * BK, row0);
+        tma_load_3d(sB + s * CF::kBBytes, &tmB, &full[s], kb * BK, n0, expert);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer (single thread) =====
+      constexpr uint32_t idesc = instr_desc_bf16<BN>();
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % CF::kStages;
+        const uint32_t ph = (kb / CF::kStages) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + s * CF::kABytes);
+        const uint32_t b0 = smem_u32(sB + s * CF::kBBytes);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          // advance 16 bf16 = 32 B along K inside the 128-B swizzle atom
+          umma_bf16(tmem_base, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
+                    (kb | kk) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    // ===== epilogue: TMEM → registers → global =====
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp & 3;  // tcgen05.ld lane window of this warp
+    const int row = quarter * 32 + lane;
+    const int grow = row0 + row;
+    const bool valid = grow < row_end && grow < M;
+    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    if constexpr (EPI == SO_EPI_SWIGLU) {
+      // accumulator columns [128p, 128p+64) = gate, [128p+64, 128p+128) = up
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C);
+#pragma unroll 1
+      for (int p = 0; p < BN / 128; ++p) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + p * 128 + h * 32, g);
+          tmem_ld32(tbase + p * 128 + 64 + h * 32, u);
+          tmem_ld_wait();
+          const int col = (n0 + p * 128) / 2 + h * 32;
+          if (valid && n0 + p * 128 < N) {
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
+            int4* dst = reinterpret_cast<int4*>(out + (size_t)grow * ldc + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
+          }
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        if (!valid || col >= N) continue;
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+        if constexpr (EPI == SO_EPI_F32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (size_t)grow * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+        } else {
+          if constexpr (EPI == SO_EPI_BF16_RESID) {
+            const int4* res = reinterpret_cast<const int4*>(
+                reinterpret_cast<const __nv_bfloat16*>(aux) + (size_t)grow * ldc + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float rr[8];
+              unpack8(res[v], rr);
+              // round the GEMM result to bf16 first, then add (matches the
+              // bf16 `residual + o_proj(x)` of the reference models)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[8 * v + j] = __bfloat162float(__float2bfloat16_rn(f[8 * v + j])) + rr[j];
+            }
+          } else if constexpr (EPI == SO_EPI_BF16_ROWSCALE) {
+            const float w = reinterpret_cast<const float*>(aux)[grow];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] *= w;
+          }
+          int4* dst = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(C) + (size_t)grow * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(CF::kTmemCols));
+  }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+int make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SO_E_DRIVER;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SO_OK : SO_E_DRIVER;
+}
+
+int make_map_3d(CUtensorMap* m, const void* base, uint64_t groups, uint64_t rows, uint64_t cols,
+                uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SO_E_DRIVER;
+  cuuint64_t dims[3] = {cols, rows, groups};
+  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint32_t box[3] = {BK, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SO_OK : SO_E_DRIVER;
+}
+
+int g_sm_count = 0;
+int sm_count() {
+  if (g_sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+template <int BN, int EPI>
+int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs, int E, int m_tiles, int M,
+              int N, int K, void* C, int ldc, const void* aux, cudaStream_t st) {
+  using CF = Cfg<BN>;
+  auto kern = gemm_tc_kernel<BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  dim3 grid(m_tiles, (N + BN - 1) / BN);
+  kern<<<grid, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
+template <int EPI>
+int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
+               const void* aux, cudaStream_t st) {
+  const int m_tiles = offs ? (M + BM - 1) / BM + E : (M + BM - 1) / BM;
+  // prefer the wide tile unless it leaves most SMs idle
+  bool wide = (long)m_tiles * ((N + 255) / 256) >= sm_count() || EPI == SO_EPI_SWIGLU && (N % 256) == 0;
+  if (EPI == SO_EPI_SWIGLU && (N % 256) != 0) wide = false;
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, A, (uint64_t)M, (uint64_t)K, BM);
+  if (rc) return rc;
+  if (wide) {
+    rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 256);
+    if (rc) return rc;
+    return launch_bn<256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
+  }
+  rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
+  if (rc) return rc;
+  return launch_bn<128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
+}
+
+int gemm_dispatch(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C,
+                  int ldc, int epi, const void* aux, cudaStream_t st) {
+  SO_REQUIRE(A && B && C, SO_E_NULLPTR);
+  SO_REQUIRE(M >= 0 && N > 0 && K > 0 && E >= 1, SO_E_SHAPE);
+  SO_REQUIRE(K % BK == 0 && N % 32 == 0, SO_E_SHAPE);
+  SO_REQUIRE(aligned16(A) && aligned16(B) && aligned16(C), SO_E_ALIGN);
+  if (epi == SO_EPI_SWIGLU) SO_REQUIRE(N % 128 == 0 && ldc % 8 == 0 && ldc >= N / 2, SO_E_SHAPE);
+  else if (epi == SO_EPI_F32) SO_REQUIRE(ldc % 4 == 0 && ldc >= N, SO_E_SHAPE);
+  else SO_REQUIRE(ldc % 8 == 0 && ldc >= N, SO_E_SHAPE);
+  if (epi == SO_EPI_BF16_RESID || epi == SO_EPI_BF16_ROWSCALE) SO_REQUIRE(aux != nullptr, SO_E_NULLPTR);
+  if (M == 0) return SO_OK;
+  switch (epi) {
+    case SO_EPI_BF16: return launch_epi<SO_EPI_BF16>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    case SO_EPI_F32: return launch_epi<SO_EPI_F32>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    case SO_EPI_BF16_RESID: return launch_epi<SO_EPI_BF16_RESID>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    case SO_EPI_SWIGLU: return launch_epi<SO_EPI_SWIGLU>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    case SO_EPI_BF16_ROWSCALE: return launch_epi<SO_EPI_BF16_ROWSCALE>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    default: return SO_E_UNSUPPORTED;
+  }
+}
+
+}  // namespace
+
+extern "C" int so_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
+                            const void* aux, void* stream) {
+  return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, as_stream(stream));
+}
+
+extern "C" int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_offsets, int E,
+                                    int max_rows, int N, int K, void* C, int ldc, int epilogue,
+                                    const void* aux, void* stream) {
+  SO_REQUIRE(expert_offsets != nullptr, SO_E_NULLPTR);
+  return gemm_dispatch(A, B, expert_offsets, E, max_rows, N, K, C, ldc, epilogue, aux, as_stream(stream));
+}
+
+extern "C" int so_device_sm_count(void) { return sm_count(); }

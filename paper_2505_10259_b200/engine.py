@@ -1,0 +1,436 @@
+"""Ping-pong executor: the measured counterpart of the reference's pipeline engine.
+
+Reference: ``simulate_decoding(policy, workload, hw, target, draft, plan, seed)
+-> SimResult`` (simulator.py:108-227) *models* barrier-synchronised rounds in
+which one batch is verified layer by layer while the other drafts
+(simulator.py:155-215).  ``Engine.run_decoding`` keeps that
+signature and returns a *measured* ``SimResult``; ``Engine.generate`` is the
+user entry the reference lacks.
+
+Physical schedule of round r (b = r mod 2), all enqueued without host syncs:
+  copy stream    K1 chunks of the streamed FFN layers, running ahead of compute
+                 into the HBM window (streamer.py);
+  target stream  verify batch b: per layer attention (KV in HBM) → wait for
+                 the layer's FFN slot → MoE → release the slot; LM head; K7
+                 accept/reject; device→host copy of the committed tokens;
+  draft stream   batch 1−b: n_cand+1 cached-KV decode steps of the resident
+                 draft (the extra step fills the KV of d_n so both caches
+                 always agree with the committed prefix: no rollback copies);
+  barrier        host waits on both streams, reads the committed counts.
+Round accounting: one verification per round — the reference
+decrements both batches per round.
+"""
+from __future__ import annotations
+
+import dataclasses
+import time
+
+import numpy as np
+import torch
+
+from . import native
+from .acceptance import forced_counts, input_uniforms
+from .domain import Policy
+from .kvcache import PagedKVCache
+from .models import DraftModel, ForwardBatch, TargetModel
+from .trace import SimResult, Tracer, busy
+
+
+@dataclasses.dataclass(frozen=True)
+class Forced:
+    """Forced-acceptance mode: committed counts drawn from AcceptanceModel(p, n_cand)."""
+
+    p: float
+
+
+class _Batch:
+    def __init__(self, lo: int, hi: int):
+        self.lo, self.hi = lo, hi
+
+    @property
+    def n(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def ids(self) -> np.ndarray:
+        return np.arange(self.lo, self.hi)
+
+
+class DecodeSession:
+    """All per-run state: caches, per-sequence counters, committed tokens."""
+
+    def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
+                 mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int):
+        self.e = engine
+        self.n_seq = n_seq
+        self.n_cand = n_cand
+        self.mode = mode
+        self.seed = seed
+        self.temperature = temperature
+        self.forced_p = forced_p
+        self.bs_draft = bs_draft
+        self.batches = [_Batch(0, min(bs_decoding, n_seq)), _Batch(min(bs_decoding, n_seq), n_seq)]
+        dev = engine.device
+        self.tkv = PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size)
+        self.dkv = PagedKVCache(engine.draft.arch, n_seq, max_len, dev, engine.page_size)
+        self.max_len = max_len
+        self.ctx = np.zeros(n_seq, np.int64)
+        self.t_last = np.zeros(n_seq, np.int32)
+        self.remaining = np.zeros(n_seq, np.int32)
+        self.out: list[list[int]] = [[] for _ in range(n_seq)]
+        V = engine.target.arch.vocab
+        self.drafts = []
+        self.qprobs = []
+        for b in self.batches:
+            self.drafts.append(torch.zeros((n_cand, max(b.n, 1)), dtype=torch.int32, device=dev))
+            self.qprobs.append(torch.zeros((max(b.n, 1), n_cand, V), dtype=torch.float32, device=dev)
+                               if mode == "sample" else None)
+        self.res_tok = [torch.empty((max(b.n, 1), n_cand + 1), dtype=torch.int32, pin_memory=True)
+                        for b in self.batches]
+        self.res_cnt = [torch.empty(max(b.n, 1), dtype=torch.int32, pin_memory=True) for b in self.batches]
+        self.rounds = 0
+        self.committed_decode = 0
+
+
+class Engine:
+    def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 64,
+                 trace: bool = True):
+        self.target = target
+        self.draft = draft
+        self.hw = hw
+        self.device = torch.device(device)
+        self.page_size = page_size
+        self.tgt_stream = torch.cuda.Stream(device=self.device)
+        self.drf_stream = torch.cuda.Stream(device=self.device)
+        self.tracer = Tracer(trace)
+        self._cur = (None, None)  # (round, batch) being verified, for trace tags
+        self._marks: dict = {}
+        if trace:
+            self.target.hooks = self._layer_hook
+            if self.target.streamer is not None:
+                self.target.streamer.trace = True
+        native.lib()  # fail loudly now if the sm_100a library is missing
+
+    def _layer_hook(self, li: int, phase: str, stream) -> None:
+        ev = self.tracer.mark(stream)
+        rnd, bi = self._cur
+        if phase == "attn_start":
+            self._marks[li] = ev
+        elif phase == "ffn_start":
+            self.tracer.add("GPU_TARGET", "attn_gpu", self._marks.get(li), ev, bi, li, rnd)
+            self._marks[li] = ev
+        else:
+            self.tracer.add("GPU_TARGET", "ffn_gpu", self._marks.get(li), ev, bi, li, rnd)
+
+    def resolve_trace(self) -> list:
+        st = self.target.streamer
+        if st is not None and self.tracer.enabled and self.tracer.t0 is not None:
+            for k, layer, a, b in st.copy_marks:
+                if a is not None and b is not None:
+                    self.tracer.add("IO_C2G", "ffn_load", a, b, None, layer, None)
+            st.copy_marks.clear()
+        return self.tracer.resolve()
+
+    # ------------------------------------------------------------------ utils
+    def _up(self, arr: np.ndarray, stream, dtype=torch.int32) -> torch.Tensor:
+        host = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).pin_memory()
+        with torch.cuda.stream(stream):
+            return host.to(self.device, non_blocking=True)
+
+    def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
+                    seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
+                    bs_draft: int | None = None) -> DecodeSession:
+        return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
+                             bs_draft or bs_decoding)
+
+    # ---------------------------------------------------------------- prefill
+    def prefill(self, s: DecodeSession, prompts: list, max_new: int, bs_prefill: int | None = None,
+                chunk_tokens: int = 16384) -> None:
+        """Layer-major prefill of every prompt through both models; emits token 1."""
+        lens = np.array([len(p) for p in prompts], np.int64)
+        assert len(prompts) == s.n_seq and lens.max() + max_new + s.n_cand + 1 <= s.max_len
+        bs_prefill = bs_prefill or s.n_seq
+        # chunk = consecutive sequences, ≤ bs_prefill of them and ≤ chunk_tokens
+        groups, cur, cur_tok = [], [], 0
+        for i, L in enumerate(lens):
+            if cur and (len(cur) >= bs_prefill or cur_tok + L > chunk_tokens):
+                groups.append(cur)
+                cur, cur_tok = [], 0
+            cur.append(i)
+            cur_tok += int(L)
+        groups.append(cur)
+        for model, kv, stream in ((self.target, s.tkv, self.tgt_stream), (self.draft, s.dkv, self.drf_stream)):
+            chunks = []
+            row0 = 0
+            last = []
+            for g in groups:
+                toks = np.concatenate([np.asarray(prompts[i], np.int32) for i in g])
+                pos = np.concatenate([np.arange(lens[i]) for i in g])
+                seq = np.concatenate([np.full(lens[i], i) for i in g])
+                qs = np.concatenate([[0], np.cumsum(lens[g])]).astype(np.int32)
+                meta = self._up(np.concatenate([toks, pos.astype(np.int32), kv.slots(seq, pos), qs,
+                                                np.zeros(len(g), np.int32)]), stream)
+                T = len(toks)
+                o = 0
+                fb = ForwardBatch(meta[o:o + T], meta[o + T:o + 2 * T], meta[o + 2 * T:o + 3 * T],
+                                  meta[o + 3 * T:o + 3 * T + len(g) + 1], meta[o + 3 * T + len(g) + 1:],
+                                  kv.block_table[g[0]:g[-1] + 1], len(g), int(lens[g].max()), None, row0)
+                last.extend(row0 + qs[1:] - 1)
+                chunks.append(fb)
+                row0 += T
+            lr = self._up(np.asarray(last, np.int64), stream, torch.int64)
+            chunks[0].last_rows = lr
+            if model is self.target:
+                logits = model.forward(chunks, kv, stream)
+                first = torch.empty(s.n_seq, dtype=torch.int32, device=self.device)
+                with torch.cuda.stream(stream):
+                    for bi, b in enumerate(s.batches):
+                        if b.n == 0:
+                            continue
+                        u = None
+                        if s.mode == "sample":
+                            u = self._up(input_uniforms(s.seed, -2, bi, 3, b.n), stream, torch.float32)
+                        native.sample_tokens(logits[b.lo:b.hi], first[b.lo:b.hi], uniforms=u,
+                                             temperature=s.temperature, stream=stream)
+                    first_h = first.to("cpu", non_blocking=True)
+            else:
+                model.forward(chunks, kv, stream, want_logits=False)
+        self.tgt_stream.synchronize()
+        self.drf_stream.synchronize()
+        first_np = first_h.numpy()
+        for i in range(s.n_seq):
+            s.out[i].append(int(first_np[i]))
+        s.t_last[:] = first_np
+        s.ctx[:] = lens
+        s.remaining[:] = max_new - 1
+
+    def synthetic_context(self, s: DecodeSession, ctx_len: int, max_new: int, seed: int = 0) -> None:
+        """Decode-only benchmark input: caches hold ``ctx_len`` random KV rows per
+        sequence (as if prefilled), t_last random.  The prompt KV is an input
+        of the decode metric, resident in HBM before timing starts."""
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        for kv in (s.tkv, s.dkv):
+            kv.k.normal_(0.0, 1.0, generator=g)
+            kv.v.normal_(0.0, 1.0, generator=g)
+        rng = np.random.default_rng(seed)
+        s.t_last[:] = rng.integers(0, self.target.arch.vocab, s.n_seq)
+        s.ctx[:] = ctx_len
+        s.remaining[:] = max_new
+        torch.cuda.synchronize(self.device)
+
+    # ------------------------------------------------------------------ draft
+    def _draft(self, s: DecodeSession, bi: int, rnd: int) -> None:
+        b = s.batches[bi]
+        if b.n == 0:
+            return
+        st = self.drf_stream
+        n = s.n_cand
+        tr = self.tracer
+        ev0 = tr.mark(st)
+        u_all = input_uniforms(s.seed, rnd, bi, 0, (b.n, n)) if s.mode == "sample" else None
+        for c_lo in range(0, b.n, s.bs_draft):
+            c_hi = min(b.n, c_lo + s.bs_draft)
+            cm = c_hi - c_lo
+            seqs = np.arange(b.lo + c_lo, b.lo + c_hi)
+            ctx = s.ctx[seqs]
+            pos = ctx[None, :] + np.arange(n + 1)[:, None]                  # [n+1, cm]
+            slots = s.dkv.slots(np.broadcast_to(seqs, pos.shape), pos)
+            qs = np.arange(cm + 1, dtype=np.int32)
+            parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, pos.astype(np.int32).ravel()]
+            if u_all is not None:
+                parts.append(u_all[c_lo:c_hi].T.ravel().view(np.int32))
+            meta = self._up(np.concatenate(parts), st)
+            o = cm
+            P = (n + 1) * cm
+            pos_d, slot_d = meta[o:o + P], meta[o + P:o + 2 * P]
+            qs_d = meta[o + 2 * P:o + 2 * P + cm + 1]
+            kvb_d = meta[o + 2 * P + cm + 1:o + 3 * P + cm + 1]
+            u_d = meta[o + 3 * P + cm + 1:].view(torch.float32) if u_all is not None else None
+            bt = s.dkv.block_table[seqs[0]:seqs[-1] + 1]
+            for j in range(n + 1):
+                toks = meta[:cm] if j == 0 else s.drafts[bi][j - 1, c_lo:c_hi]
+                fb = ForwardBatch(toks, pos_d[j * cm:(j + 1) * cm], slot_d[j * cm:(j + 1) * cm], qs_d,
+                                  kvb_d[j * cm:(j + 1) * cm], bt, cm, 1)
+                if j == n:
+                    self.draft.forward(fb, s.dkv, st, want_logits=False)  # KV of d_n only
+                    break
+                logits = self.draft.forward(fb, s.dkv, st)
+                out_tok = s.drafts[bi][j, c_lo:c_hi]
+                if s.mode == "sample":
+                    qp = s.qprobs[bi][c_lo:c_hi, j, :]
+                    native.sample_tokens(logits, out_tok, uniforms=u_d[j * cm:(j + 1) * cm], out_probs=qp,
+                                         temperature=s.temperature, stream=st)
+                else:
+                    native.sample_tokens(logits, out_tok, stream=st)
+        tr.add("GPU_DRAFT", "draft_decode", ev0, tr.mark(st), batch=bi, rnd=rnd)
+
+    # ----------------------------------------------------------------- verify
+    def _verify(self, s: DecodeSession, bi: int, rnd: int) -> None:
+        b = s.batches[bi]
+        st = self.tgt_stream
+        n = s.n_cand
+        tr = self.tracer
+        seqs = b.ids
+        ctx = s.ctx[seqs]
+        T = b.n * (n + 1)
+        pos = ctx[:, None] + np.arange(n + 1)[None, :]
+        slots = s.tkv.slots(np.broadcast_to(seqs[:, None], pos.shape), pos)
+        qs = (np.arange(b.n + 1) * (n + 1)).astype(np.int32)
+        forced = None
+        if s.forced_p is not None and s.mode == "greedy":
+            forced = forced_counts(s.seed, rnd, bi, s.forced_p, n, b.n)
+        parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, ctx.astype(np.int32),
+                 s.remaining[seqs]]
+        if forced is not None:
+            parts.append(forced)
+        if s.mode == "sample":
+            parts.append(input_uniforms(s.seed, rnd, bi, 1, (b.n, n)).ravel().view(np.int32))
+            parts.append(input_uniforms(s.seed, rnd, bi, 2, b.n).view(np.int32))
+        meta = self._up(np.concatenate(parts), st)
+        o = 0
+        t_last_d = meta[o:o + b.n]; o += b.n
+        pos_d = meta[o:o + T]; o += T
+        slot_d = meta[o:o + T]; o += T
+        qs_d = meta[o:o + b.n + 1]; o += b.n + 1
+        kvb_d = meta[o:o + b.n]; o += b.n
+        rem_d = meta[o:o + b.n]; o += b.n
+        forced_d = None
+        if forced is not None:
+            forced_d = meta[o:o + b.n]; o += b.n
+        ev0 = tr.mark(st)
+        with torch.cuda.stream(st):
+            toks = self.target.ws.get("vtok", (b.n, n + 1), torch.int32)
+            toks[:, 0].copy_(t_last_d)
+            toks[:, 1:].copy_(s.drafts[bi][:, :b.n].t())
+            draft_rows = self.target.ws.get("vdraft", (b.n, n), torch.int32)
+            draft_rows.copy_(s.drafts[bi][:, :b.n].t())
+        fb = ForwardBatch(toks.view(-1), pos_d, slot_d, qs_d, kvb_d, s.tkv.block_table[b.lo:b.hi], b.n, n + 1)
+        logits = self.target.forward(fb, s.tkv, st)
+        ev1 = tr.mark(st)
+        out_tok = self.target.ws.get("acc_tok", (b.n, n + 1), torch.int32)
+        out_cnt = self.target.ws.get("acc_cnt", (b.n,), torch.int32)
+        if s.mode == "sample":
+            u_acc = meta[o:o + b.n * n].view(torch.float32); o += b.n * n
+            u_res = meta[o:o + b.n].view(torch.float32); o += b.n
+            native.accept_sample(draft_rows, logits, s.qprobs[bi][:b.n], u_acc, u_res, rem_d, out_tok, out_cnt,
+                                 s.temperature, st)
+        else:
+            native.accept_greedy(draft_rows, logits, rem_d, out_tok, out_cnt, forced_d, st)
+        with torch.cuda.stream(st):
+            s.res_tok[bi][:b.n].copy_(out_tok, non_blocking=True)
+            s.res_cnt[bi][:b.n].copy_(out_cnt, non_blocking=True)
+        ev2 = tr.mark(st)
+        tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
+        tr.add("GPU_TARGET", "accept", ev1, ev2, batch=bi, rnd=rnd)
+
+    def _commit(self, s: DecodeSession, bi: int) -> int:
+        b = s.batches[bi]
+        cnt = s.res_cnt[bi][:b.n].numpy()
+        tok = s.res_tok[bi][:b.n].numpy()
+        total = 0
+        for j, i in enumerate(b.ids):
+            c = int(cnt[j])
+            if c <= 0:
+                continue
+            s.out[i].extend(int(x) for x in tok[j, :c])
+            s.remaining[i] -= c
+            s.t_last[i] = tok[j, c - 1]
+            s.ctx[i] += c
+            total += c
+        return total
+
+    # ----------------------------------------------------------------- rounds
+    def first_draft(self, s: DecodeSession) -> None:
+        self._draft(s, 0, -1)
+        self.drf_stream.synchronize()
+
+    def round(self, s: DecodeSession) -> int:
+        """One barrier-synchronised round; returns tokens committed."""
+        rnd = s.rounds
+        bi = rnd % 2
+        b, o = s.batches[bi], s.batches[1 - bi]
+        verify = b.n > 0 and (s.remaining[b.lo:b.hi] > 0).any()
+        draft = o.n > 0 and (s.remaining[o.lo:o.hi] > 0).any()
+        if verify:
+            self._cur = (rnd, bi)
+            self._verify(s, bi, rnd)
+        if draft:
+            self._draft(s, 1 - bi, rnd)
+        # barrier (simulator.py:209-211): device-side join, then the host reads counts
+        done = torch.cuda.Event()
+        done.record(self.drf_stream)
+        self.tgt_stream.wait_event(done)
+        bev = self.tracer.mark(self.tgt_stream)
+        self.tracer.add("GPU_TARGET", "barrier", bev, bev, rnd=rnd)
+        self.tgt_stream.synchronize()
+        c = self._commit(s, bi) if verify else 0
+        s.rounds += 1
+        s.committed_decode += c
+        return c
+
+    def decode(self, s: DecodeSession, max_rounds: int | None = None) -> None:
+        while (s.remaining > 0).any():
+            if max_rounds is not None and s.rounds >= max_rounds:
+                break
+            self.round(s)
+
+    # ------------------------------------------------------------ public API
+    def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
+                 mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None) -> list[list[int]]:
+        """prompts (token id lists) → committed continuations, max_new_tokens each."""
+        S = len(prompts)
+        if policy is None:
+            policy = Policy(bs_prefill=min(S, 2 * ((S + 1) // 2)), bs_decoding=(S + 1) // 2,
+                            bs_draft=(S + 1) // 2, n_cand=4)
+        max_len = max(len(p) for p in prompts) + max_new_tokens + policy.n_cand + 2
+        s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, temperature, forced_p,
+                             policy.bs_draft)
+        self.prefill(s, prompts, max_new_tokens, policy.bs_prefill)
+        if (s.remaining > 0).any():
+            self.first_draft(s)
+            self.decode(s)
+        self.last_session = s
+        return [o[:max_new_tokens] for o in s.out]
+
+    def run_decoding(self, policy, workload, plan=None, seed: int = 0, acceptance="greedy", prompts=None,
+                     max_rounds: int | None = None) -> SimResult:
+        """Measured counterpart of simulate_decoding (simulator.py:108-116).
+
+        Runs workload.total_sequences sequences (two batches of
+        policy.bs_decoding) for workload.max_new_tokens tokens each and returns
+        the measured trace.  ``acceptance`` = "greedy" | "sample" | Forced(p);
+        without prompts the context is synthetic (l_input random KV rows).
+        """
+        mode = "sample" if acceptance == "sample" else "greedy"
+        forced_p = acceptance.p if isinstance(acceptance, Forced) else None
+        S = workload.total_sequences
+        max_len = workload.l_input + workload.max_new_tokens + policy.n_cand + 2
+        s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, 1.0, forced_p,
+                             policy.bs_draft)
+        if prompts is not None:
+            self.prefill(s, prompts, workload.max_new_tokens, policy.bs_prefill)
+        else:
+            self.synthetic_context(s, workload.l_input, workload.max_new_tokens, seed)
+        self.first_draft(s)
+        torch.cuda.synchronize(self.device)
+        if self.target.streamer is not None:
+            self.target.streamer.copy_marks.clear()
+        self.tracer.origin(self.tgt_stream)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(self.tgt_stream)
+        wall0 = time.perf_counter()
+        self.decode(s, max_rounds)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record(self.tgt_stream)
+        t1.synchronize()
+        wall = time.perf_counter() - wall0
+        total = t0.elapsed_time(t1) * 1e-3
+        events = self.resolve_trace()
+        tokens = s.committed_decode
+        self.last_session = s
+        return SimResult(trace=events, total_time=total, tokens_generated=tokens,
+                         throughput=tokens / total if total > 0 else 0.0,
+                         peak_gpu_bytes=int(torch.cuda.max_memory_allocated(self.device)),
+                         rounds_executed=s.rounds, per_resource_busy=busy(events),
+                         extra={"wall_s": wall})

@@ -1,0 +1,227 @@
+"""Target (Mixtral-style MoE, FFN streamed) and draft (Mistral-style dense,
+HBM-resident) models as sequences of C-ABI kernel launches.
+
+The reference defines no model; the interface here is the one
+SURVEY.md §8b asks for: ``spec()`` returns the reference ``ModelSpec``;
+``forward`` runs new tokens of a set of sequences through the model over the
+paged KV cache and returns fp32 logits.  Every op is an sm_100a kernel from
+``native`` launched on the caller's stream; nothing here computes on the CPU.
+
+Per layer (simulator.py:168-192):
+    xn = RMSNorm(x) → qkv = xn·Wqkvᵀ (tcgen05) → RoPE + KV append →
+    paged attention (mma.sync) → h = attn·Woᵀ + x (fused residual epilogue) →
+    hn = RMSNorm(h) → [MoE]  top-2 router + permute → grouped gate_up GEMM
+    with fused SwiGLU → grouped down GEMM with fused routing-weight scale →
+    deterministic two-slot combine + residual
+                     [dense] gate_up GEMM + SwiGLU → down GEMM + residual
+
+The loop is layer-major over *chunks*: a verify or draft step is one chunk;
+prefill splits the prompts into token-bounded chunks and runs every chunk
+through layer ℓ before layer ℓ+1, so each streamed layer crosses the host
+link once per prefill (the zig-zag order of PAPER.md:135-136 / FlexGen).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import native
+from .config import ModelArch
+from .kvcache import PagedKVCache
+from .weights import ModelWeights, ffn_offsets
+
+
+class Workspace:
+    """Grow-only scratch buffers, one set per stream (target / draft)."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self._bufs: dict[str, torch.Tensor] = {}
+
+    def get(self, name: str, shape, dtype) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= int(s)
+        esize = torch.empty((), dtype=dtype).element_size()
+        nbytes = max(n * esize, 16)
+        buf = self._bufs.get(name)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._bufs[name] = buf
+        return buf[: n * esize].view(dtype).view(*shape)
+
+    def bytes(self) -> int:
+        return sum(b.numel() for b in self._bufs.values())
+
+
+class ForwardBatch:
+    """Device-side metadata of one chunk of a forward call (built by the engine).
+
+    Rows [row0, row0 + T) of the call's hidden-state buffer belong to this
+    chunk; its sequences' query rows are given CSR-style by ``q_start``.
+    """
+
+    def __init__(self, tokens, positions, slots, q_start, kv_before, block_table, n_seq, max_q,
+                 last_rows=None, row0: int = 0):
+        self.tokens = tokens          # int32 [T]
+        self.positions = positions    # int32 [T]
+        self.slots = slots            # int32 [T]
+        self.q_start = q_start        # int32 [n_seq+1], relative to row0
+        self.kv_before = kv_before    # int32 [n_seq]
+        self.block_table = block_table  # int32 [n_seq, pages] (view of the cache's table)
+        self.n_seq = n_seq
+        self.max_q = max_q
+        self.last_rows = last_rows    # int64 [k] absolute rows whose logits are wanted (None = all)
+        self.row0 = row0
+
+    @property
+    def T(self) -> int:
+        return self.tokens.numel()
+
+
+class CausalLM:
+    """Shared forward of the target and the draft."""
+
+    def __init__(self, weights: ModelWeights, device, streamer=None):
+        self.w = weights
+        self.arch: ModelArch = weights.arch
+        self.device = torch.device(device)
+        self.streamer = streamer
+        self.ws = Workspace(device)
+        self.hooks = None  # optional callback(layer, phase, stream) used by the tracer
+
+    def spec(self):
+        return self.arch.spec()
+
+    # ------------------------------------------------------------------
+    def forward(self, chunks: list[ForwardBatch] | ForwardBatch, kv: PagedKVCache, stream: torch.cuda.Stream,
+                logits_out: torch.Tensor | None = None, want_logits: bool = True) -> torch.Tensor | None:
+        if isinstance(chunks, ForwardBatch):
+            chunks = [chunks]
+        with torch.cuda.stream(stream):
+            return self._forward(chunks, kv, stream, logits_out, want_logits)
+
+    def _forward(self, chunks, kv, stream, logits_out, want_logits):
+        a, ws = self.arch, self.ws
+        Ttot = sum(c.T for c in chunks)
+        Tmax = max(c.T for c in chunks)
+        H, dh, hq, hkv = a.hidden, a.head_dim, a.n_head, a.n_kv_head
+        xa = ws.get("x", (Ttot, H), torch.bfloat16)
+        xb = ws.get("x2", (Ttot, H), torch.bfloat16)
+        xn = ws.get("xn", (Tmax, H), torch.bfloat16)
+        h = ws.get("h", (Tmax, H), torch.bfloat16)
+        qkv = ws.get("qkv", (Tmax, a.qkv_rows), torch.bfloat16)
+        q = ws.get("q", (Tmax, hq * dh), torch.bfloat16)
+        att = ws.get("att", (Tmax, hq * dh), torch.bfloat16)
+        scale = 1.0 / math.sqrt(dh)
+        for c in chunks:
+            native.embed(c.tokens, self.w.embed, xa[c.row0:c.row0 + c.T], stream)
+        hook = self.hooks
+        for li, L in enumerate(self.w.layers):
+            if hook:
+                hook(li, "attn_start", stream)
+            kc, vc = kv.layer(li)
+            base = None
+            for ci, c in enumerate(chunks):
+                T = c.T
+                x = xa[c.row0:c.row0 + T]
+                out = xb[c.row0:c.row0 + T]
+                native.rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
+                native.gemm(xn[:T], L.wqkv, qkv[:T], native.EPI_BF16, None, stream)
+                native.rope_kv_append(qkv[:T], c.positions, c.slots, hq, hkv, dh, a.rope_theta, kv.page_size,
+                                      q[:T], kc, vc, stream)
+                native.attn_paged(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
+                                  kv.page_size, scale, att[:T], stream)
+                native.gemm(att[:T], L.wo, h[:T], native.EPI_BF16_RESID, x, stream)
+                native.rmsnorm(h[:T], L.ffn_norm, xn[:T], a.eps, stream)
+                if ci == 0:
+                    base = self._ffn_acquire(li, L, stream)
+                    if hook:
+                        hook(li, "ffn_start", stream)
+                if a.is_moe:
+                    self._moe(L, base, xn[:T], h[:T], out, T, stream)
+                else:
+                    self._mlp(base, xn[:T], h[:T], out, T, stream)
+            self._ffn_release(li, stream)
+            if hook:
+                hook(li, "ffn_end", stream)
+            xa, xb = xb, xa
+        if not want_logits:
+            return None
+        rows_idx = [c.last_rows for c in chunks if c.last_rows is not None]
+        x = xa
+        if rows_idx:
+            sel = torch.cat(rows_idx) if len(rows_idx) > 1 else rows_idx[0]
+            rows = ws.get("lastx", (sel.numel(), H), torch.bfloat16)
+            torch.index_select(xa, 0, sel, out=rows)
+            x = rows
+        R = x.shape[0]
+        xf = ws.get("xf", (R, H), torch.bfloat16)
+        native.rmsnorm(x, self.w.final_norm, xf, a.eps, stream)
+        if logits_out is None:
+            logits_out = ws.get("logits", (R, a.vocab), torch.float32)
+        native.gemm(xf, self.w.lm_head, logits_out, native.EPI_F32, None, stream)
+        return logits_out
+
+    # ------------------------------------------------------------------
+    def _ffn_acquire(self, li, L, stream) -> int:
+        if self.streamer is not None:
+            return self.streamer.acquire(li, stream)
+        return L.ffn.data_ptr()
+
+    def _ffn_release(self, li, stream) -> None:
+        if self.streamer is not None:
+            self.streamer.release(li, stream)
+
+    def _moe(self, L, base, xn, h, out, T, stream):
+        a, ws = self.arch, self.ws
+        E, H, I = a.n_expert, a.hidden, a.inter
+        rows = 2 * T
+        offs = ws.get("offs", (E + 1,), torch.int32)
+        perm = ws.get("perm", (rows,), torch.int32)
+        roww = ws.get("roww", (rows,), torch.float32)
+        trows = ws.get("trows", (T, 2), torch.int32)
+        xperm = ws.get("xperm", (rows, H), torch.bfloat16)
+        act = ws.get("act", (rows, I), torch.bfloat16)
+        y = ws.get("y", (rows, H), torch.bfloat16)
+        rws = ws.get("router_ws", (native.router_workspace_bytes(T, E),), torch.uint8)
+        native.router_top2(xn, L.router, offs, perm, roww, trows, xperm, rws, stream=stream)
+        gu_elems, _, _ = ffn_offsets(a)
+        native.gemm_grouped(xperm, base, offs, E, 2 * I, act, native.EPI_SWIGLU, None, stream)
+        native.gemm_grouped(act, base + 2 * gu_elems, offs, E, H, y, native.EPI_BF16_ROWSCALE, roww, stream)
+        native.moe_combine(y, trows, h, out, stream)
+
+    def _mlp(self, base, xn, h, out, T, stream):
+        a, ws = self.arch, self.ws
+        I, H = a.inter, a.hidden
+        act = ws.get("act", (T, I), torch.bfloat16)
+        gu_elems, _, _ = ffn_offsets(a)
+        gu = _raw_bf16(base, (2 * I, H), self.device)
+        dn = _raw_bf16(base + 2 * gu_elems, (H, I), self.device)
+        native.gemm(xn, gu, act, native.EPI_SWIGLU, None, stream)
+        native.gemm(act, dn, out, native.EPI_BF16_RESID, h, stream)
+
+
+class _RawView:
+    """Minimal tensor-like view of device memory by address (for native.gemm)."""
+
+    def __init__(self, ptr: int, shape):
+        self._ptr = ptr
+        self.shape = tuple(shape)
+        self.dtype = torch.bfloat16
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+
+def _raw_bf16(ptr: int, shape, device) -> _RawView:
+    return _RawView(ptr, shape)
+
+
+class TargetModel(CausalLM):
+    """Mixtral-style MoE verifier; FFN layers come through the streamer."""
+
+
+class DraftModel(CausalLM):
+    """Mistral-style dense drafter, fully HBM-resident."""

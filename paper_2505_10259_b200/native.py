@@ -1,0 +1,217 @@
+"""ctypes binding of the C ABI in ``include/specoffload_b200.h``.
+
+This is the one place the Python host layer touches native code.  Every
+wrapper takes torch tensors (device memory owned by PyTorch, SURVEY.md §8b
+"Ownership"), checks shapes/dtypes, and enqueues on the current (or given)
+CUDA stream.  A non-zero status raises :class:`NativeError`.  There is no CPU
+fallback: if the shared library is missing, :func:`lib` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import c_float, c_int, c_int64, c_size_t, c_void_p
+
+import torch
+
+from .errors import NativeError, NativeLibraryMissing
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", "libspecoffload_b200.so")
+_lib = None
+
+EPI_BF16 = 0
+EPI_F32 = 1
+EPI_BF16_RESID = 2
+EPI_SWIGLU = 3
+EPI_BF16_ROWSCALE = 4
+
+# name -> (restype, argtypes); mirrors include/specoffload_b200.h
+_P = c_void_p
+_SIGNATURES = {
+    "so_abi_version": (c_int, []),
+    "so_status_string": (ctypes.c_char_p, [c_int]),
+    "so_device_sm_count": (c_int, []),
+    "so_accept_greedy": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
+    "so_accept_sample": (c_int, [_P, _P, _P, _P, _P, _P, c_float, c_int, c_int, c_int, _P, _P, _P]),
+    "so_sample_tokens": (c_int, [_P, c_int64, _P, c_float, c_int, c_int, _P, c_int64, _P, c_int64, _P]),
+    "so_router_workspace_bytes": (c_size_t, [c_int, c_int]),
+    "so_router_top2": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "so_moe_combine": (c_int, [_P, _P, _P, c_int, c_int, _P, _P]),
+    "so_gemm_bf16": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
+    "so_gemm_grouped_bf16": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
+    "so_embed": (c_int, [_P, _P, c_int, c_int, _P, _P]),
+    "so_rmsnorm": (c_int, [_P, _P, c_int, c_int, c_float, _P, _P]),
+    "so_rope_kv_append": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_float, c_int, _P, _P, _P, _P]),
+    "so_attn_paged": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
+                              c_float, _P, _P]),
+    "so_stream_layer": (c_int, [_P, _P, c_size_t, c_size_t, _P, _P]),
+}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the native library; raise if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise NativeLibraryMissing(
+                f"{_LIB_PATH} is missing; run __graft_entry__.build() (no CPU fallback exists)"
+            )
+        handle = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES)
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().so_status_string(rc).decode()
+        raise NativeError(f"{what} failed with status {rc}: {msg}", rc)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+# ---------------------------------------------------------------- K7 accept ---
+
+def accept_greedy(draft, logits, remaining, out_tokens, out_counts, forced=None, stream=None):
+    bs, n_cand = draft.shape
+    V = logits.shape[-1]
+    _need(draft, torch.int32, "draft"); _need(logits, torch.float32, "logits")
+    _need(remaining, torch.int32, "remaining")
+    assert logits.numel() == bs * (n_cand + 1) * V
+    if forced is not None:
+        _need(forced, torch.int32, "forced")
+    _check(lib().so_accept_greedy(_ptr(draft), _ptr(logits), _ptr(remaining), _ptr(forced), bs, n_cand, V,
+                                  _ptr(out_tokens), _ptr(out_counts), _stream(stream)), "so_accept_greedy")
+
+
+def accept_sample(draft, logits, draft_probs, u_accept, u_resample, remaining, out_tokens, out_counts,
+                  temperature=1.0, stream=None):
+    bs, n_cand = draft.shape
+    V = logits.shape[-1]
+    for t, n in ((logits, "logits"), (draft_probs, "draft_probs"), (u_accept, "u_accept"),
+                 (u_resample, "u_resample")):
+        _need(t, torch.float32, n)
+    _check(lib().so_accept_sample(_ptr(draft), _ptr(logits), _ptr(draft_probs), _ptr(u_accept),
+                                  _ptr(u_resample), _ptr(remaining), 1.0 / temperature, bs, n_cand, V,
+                                  _ptr(out_tokens), _ptr(out_counts), _stream(stream)), "so_accept_sample")
+
+
+def sample_tokens(logits, out_tokens, uniforms=None, out_probs=None, temperature=1.0, stream=None):
+    """Rows of ``logits`` [rows, V] (row stride may exceed V) → one token each."""
+    rows, V = logits.shape
+    assert logits.dtype == torch.float32 and logits.stride(1) == 1
+    tok_stride = out_tokens.stride(0) if out_tokens.dim() else 1
+    probs_stride = out_probs.stride(0) if out_probs is not None else 0
+    _check(lib().so_sample_tokens(_ptr(logits), logits.stride(0), _ptr(uniforms), 1.0 / temperature, rows, V,
+                                  _ptr(out_tokens), tok_stride, _ptr(out_probs), probs_stride,
+                                  _stream(stream)), "so_sample_tokens")
+
+
+# ---------------------------------------------------------------- K2 router ---
+
+def router_workspace_bytes(T: int, E: int) -> int:
+    return int(lib().so_router_workspace_bytes(T, E))
+
+
+def router_top2(x, w_gate, expert_offsets, perm_token, row_weight, token_rows, x_perm, workspace,
+                topk_idx=None, topk_w=None, stream=None):
+    T, H = x.shape
+    E = w_gate.shape[0]
+    _need(x, torch.bfloat16, "x"); _need(w_gate, torch.bfloat16, "w_gate")
+    _check(lib().so_router_top2(_ptr(x), _ptr(w_gate), T, H, E, _ptr(topk_idx), _ptr(topk_w),
+                                _ptr(expert_offsets), _ptr(perm_token), _ptr(row_weight), _ptr(token_rows),
+                                _ptr(x_perm), _ptr(workspace), _stream(stream)), "so_router_top2")
+
+
+def moe_combine(y_perm, token_rows, resid, out, stream=None):
+    T, H = resid.shape
+    _check(lib().so_moe_combine(_ptr(y_perm), _ptr(token_rows), _ptr(resid), T, H, _ptr(out),
+                                _stream(stream)), "so_moe_combine")
+
+
+# ---------------------------------------------------------------- GEMMs ---
+
+def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None):
+    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05."""
+    M, K = a.shape
+    N = b.shape[-2]
+    assert b.shape[-1] == K
+    _need(a, torch.bfloat16, "a")
+    assert b.dtype == torch.bfloat16
+    _check(lib().so_gemm_bf16(_ptr(a), _ptr(b), M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux),
+                              _stream(stream)), "so_gemm_bf16")
+
+
+def gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None, stream=None):
+    """Grouped expert GEMM; ``b_ptr`` addresses [E, N, K] bf16 weights (e.g. a window slot)."""
+    rows, K = a.shape
+    _need(a, torch.bfloat16, "a")
+    _check(lib().so_gemm_grouped_bf16(_ptr(a), b_ptr, _ptr(expert_offsets), E, rows, N, K, _ptr(out),
+                                      out.stride(0), epilogue, _ptr(aux), _stream(stream)), "so_gemm_grouped_bf16")
+
+
+# ---------------------------------------------------------------- K8 ---
+
+def embed(tokens, table, out, stream=None):
+    T = tokens.numel()
+    H = table.shape[1]
+    _check(lib().so_embed(_ptr(tokens), _ptr(table), T, H, _ptr(out), _stream(stream)), "so_embed")
+
+
+def rmsnorm(x, w, out, eps, stream=None):
+    T, H = x.shape
+    _check(lib().so_rmsnorm(_ptr(x), _ptr(w), T, H, eps, _ptr(out), _stream(stream)), "so_rmsnorm")
+
+
+def rope_kv_append(qkv, positions, slots, hq, hkv, dh, theta, page_size, q_out, k_cache, v_cache, stream=None):
+    T = qkv.shape[0]
+    _check(lib().so_rope_kv_append(_ptr(qkv), _ptr(positions), _ptr(slots), T, hq, hkv, dh, theta, page_size,
+                                   _ptr(q_out), _ptr(k_cache), _ptr(v_cache), _stream(stream)),
+           "so_rope_kv_append")
+
+
+# ---------------------------------------------------------------- K6 ---
+
+def attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, hkv, dh, page_size, scale, out,
+               stream=None):
+    bs = kv_before.numel()
+    _check(lib().so_attn_paged(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
+                               _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,
+                               _ptr(out), _stream(stream)), "so_attn_paged")
+
+
+# ---------------------------------------------------------------- K1 ---
+
+def stream_layer(slot_ptr: int, host_ptr: int, nbytes: int, chunk: int, stream: torch.cuda.Stream,
+                 event: torch.cuda.Event | None = None) -> None:
+    ev = event.cuda_event if event is not None else None
+    _check(lib().so_stream_layer(slot_ptr, host_ptr, nbytes, chunk, stream.cuda_stream, ev), "so_stream_layer")

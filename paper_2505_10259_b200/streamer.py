@@ -1,0 +1,160 @@
+"""K1 — layer-wise target-weight streamer (pinned host DRAM → HBM window).
+
+Reference model: a two-slot GPU window for the current and next FFN layer
+(placement.py:198-199), one CPU→GPU op per non-pinned layer triggered by that
+layer (prefetch_schedule, placement.py:260-283), load time
+ffn_bytes / c2g_bandwidth (costmodel.py:74).  The reference starts layer ℓ's
+load only when layer ℓ starts (simulator.py:168-177), idling the link during
+every FFN compute.  Here the copy stream runs ``n_slots − 1``
+layers ahead: copy k is enqueued as soon as compute k−n_slots has released its
+slot, across pass (round) boundaries, so the PCIe link never waits for the
+host loop.  No SMs are involved (copy engine DMA), the compute stream waits on
+a per-slot CUDA event only right before the layer's expert GEMMs — the layer's
+attention runs while its FFN bytes are still in flight.
+"""
+from __future__ import annotations
+
+import ctypes
+import mmap
+import os
+import threading
+
+import torch
+
+from . import native
+from .errors import InsufficientTotalMemory
+
+
+class HostStore:
+    """Pinned host memory for the streamed layers.
+
+    Large regions are mmap'ed anonymously, advised to transparent huge pages,
+    pre-faulted by several threads, then page-locked with cudaHostRegister —
+    much faster than cudaHostAlloc for hundreds of GB (measured on the box,
+    DESIGN.md §K1).  Small regions fall back to torch's pinned allocator.
+    """
+
+    def __init__(self, threads: int | None = None):
+        self._maps: list[tuple[mmap.mmap, int, int]] = []
+        self.threads = threads or min(16, os.cpu_count() or 4)
+        self.bytes = 0
+
+    def alloc(self, nbytes: int) -> torch.Tensor:
+        if nbytes < (256 << 20):
+            t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            self.bytes += nbytes
+            return t
+        m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        try:
+            m.madvise(mmap.MADV_HUGEPAGE)
+        except (AttributeError, OSError):
+            pass
+        buf = (ctypes.c_uint8 * nbytes).from_buffer(m)
+        addr = ctypes.addressof(buf)
+        self._prefault(addr, nbytes)
+        rc = torch.cuda.cudart().cudaHostRegister(addr, nbytes, 0)
+        if int(rc) != 0:
+            raise InsufficientTotalMemory(f"cudaHostRegister of {nbytes} B failed ({int(rc)})")
+        self._maps.append((m, addr, nbytes))
+        self.bytes += nbytes
+        t = torch.frombuffer(buf, dtype=torch.uint8)
+        return t
+
+    def _prefault(self, addr: int, nbytes: int) -> None:
+        page = 1 << 21
+        n = self.threads
+        step = (nbytes // n + page - 1) // page * page
+
+        def touch(lo: int, hi: int) -> None:
+            ctypes.memset(addr + lo, 0, max(0, hi - lo))
+
+        ts = [threading.Thread(target=touch, args=(i * step, min(nbytes, (i + 1) * step))) for i in range(n)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    def close(self) -> None:
+        for m, addr, _ in self._maps:
+            torch.cuda.cudart().cudaHostUnregister(addr)
+        self._maps.clear()
+
+
+class LayerStreamer:
+    """Moves host-resident FFN layers through ``n_slots`` HBM slots.
+
+    Usage on the compute stream, per layer ℓ of every pass, in layer order:
+        ptr = streamer.acquire(ℓ, stream)   # waits only if ℓ is streamed
+        ... expert GEMMs reading ptr ...
+        streamer.release(ℓ, stream)
+    Resident layers return their HBM buffer and never touch the link.
+    """
+
+    def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict[int, torch.Tensor],
+                 n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False):
+        self.layer_bytes = layer_bytes
+        self.resident = resident
+        self.host = host
+        self.streamed = [li for li in range(n_layer) if li in host]
+        self.n_slots = n_slots if self.streamed else 0
+        self.chunk = chunk_bytes
+        self.device = torch.device(device)
+        self.copy_stream = torch.cuda.Stream(device=self.device) if self.streamed else None
+        self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
+        self.loaded = [torch.cuda.Event() for _ in range(self.n_slots)]
+        self.free = [torch.cuda.Event() for _ in range(self.n_slots)]
+        self.k_use = 0      # global index of the next streamed use
+        self.k_issued = 0   # copies enqueued so far
+        self.bytes_issued = 0
+        self.trace = trace
+        self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
+
+    @property
+    def window_bytes(self) -> int:
+        return self.n_slots * self.layer_bytes
+
+    def _issue(self, k: int) -> None:
+        slot = k % self.n_slots
+        layer = self.streamed[k % len(self.streamed)]
+        if k >= self.n_slots:
+            self.copy_stream.wait_event(self.free[slot])
+        src = self.host[layer]
+        start = end = None
+        if self.trace:
+            start = torch.cuda.Event(enable_timing=True)
+            start.record(self.copy_stream)
+        native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
+                            self.copy_stream, self.loaded[slot])
+        if self.trace:
+            end = torch.cuda.Event(enable_timing=True)
+            end.record(self.copy_stream)
+            self.copy_marks.append((k, layer, start, end))
+        self.bytes_issued += self.layer_bytes
+
+    def _ensure_issued(self, upto: int) -> None:
+        while self.k_issued <= upto:
+            self._issue(self.k_issued)
+            self.k_issued += 1
+
+    def prefetch(self) -> None:
+        """Start the first window's copies (e.g. before prefill begins)."""
+        if self.streamed:
+            self._ensure_issued(self.k_use + self.n_slots - 1)
+
+    def acquire(self, layer: int, stream: torch.cuda.Stream) -> int:
+        if layer not in self.host:
+            return self.resident[layer].data_ptr()
+        k = self.k_use
+        assert self.streamed[k % len(self.streamed)] == layer, "layers must be consumed in pass order"
+        self._ensure_issued(k + self.n_slots - 1)
+        stream.wait_event(self.loaded[k % self.n_slots])
+        return self.slots[k % self.n_slots].data_ptr()
+
+    def release(self, layer: int, stream: torch.cuda.Stream) -> None:
+        if layer not in self.host:
+            return
+        k = self.k_use
+        self.free[k % self.n_slots].record(stream)
+        self.k_use += 1
+        # keep the link busy: the copy that waits on this release goes out now
+        self._ensure_issued(self.k_use + self.n_slots - 1)

@@ -1,0 +1,114 @@
+"""Measured traces in the reference's trace schema.
+
+``SimEvent`` / ``SimResult`` carry the fields of simulator.py:41-60 so the
+reference's consumers (``export_trace``-style tooling, tests/_checks-style
+invariants) read measured runs unchanged.  Differences: the
+single exclusive "GPU" resource is split per CUDA stream — ``GPU_TARGET``
+(verification) and ``GPU_DRAFT`` (drafting) genuinely overlap on one B200 — and
+labels ``attn_gpu`` / ``accept`` are added; ``IO_C2G`` is the copy stream.
+Timestamps come from CUDA events, in seconds from the run's first event.
+"""
+from __future__ import annotations
+
+import dataclasses
+import json
+
+import torch
+
+RESOURCES = ("GPU_TARGET", "GPU_DRAFT", "CPU", "IO_C2G", "IO_G2C", "IO_DISK")
+LABELS = ("attn_gpu", "ffn_load", "ffn_gpu", "draft_prefill", "draft_decode", "accept", "kv_offload",
+          "disk_prefetch", "barrier", "prefill")
+
+
+@dataclasses.dataclass(frozen=True)
+class SimEvent:
+    resource: str
+    start: float
+    end: float
+    label: str
+    batch: int | None = None
+    layer: int | None = None
+    round: int | None = None
+
+
+@dataclasses.dataclass
+class SimResult:
+    trace: list
+    total_time: float
+    tokens_generated: int
+    throughput: float
+    peak_gpu_bytes: int
+    rounds_executed: int
+    per_resource_busy: dict = dataclasses.field(default_factory=dict)
+    extra: dict = dataclasses.field(default_factory=dict)
+
+
+def busy(trace) -> dict:
+    out = {r: 0.0 for r in RESOURCES}
+    for ev in trace:
+        out[ev.resource] = out.get(ev.resource, 0.0) + (ev.end - ev.start)
+    return out
+
+
+class Tracer:
+    """Collects (start, end) CUDA-event pairs and resolves them after a sync."""
+
+    def __init__(self, enabled: bool = True):
+        self.enabled = enabled
+        self.t0: torch.cuda.Event | None = None
+        self._pending: list[tuple] = []
+
+    def origin(self, stream: torch.cuda.Stream) -> None:
+        if not self.enabled:
+            return
+        self.t0 = torch.cuda.Event(enable_timing=True)
+        self.t0.record(stream)
+
+    def mark(self, stream: torch.cuda.Stream) -> torch.cuda.Event | None:
+        if not self.enabled:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def add(self, resource, label, start_ev, end_ev, batch=None, layer=None, rnd=None) -> None:
+        if self.enabled and start_ev is not None and end_ev is not None:
+            self._pending.append((resource, label, start_ev, end_ev, batch, layer, rnd))
+
+    def resolve(self) -> list[SimEvent]:
+        if not self.enabled or self.t0 is None:
+            return []
+        out = []
+        for resource, label, s, e, batch, layer, rnd in self._pending:
+            st = self.t0.elapsed_time(s) * 1e-3
+            en = self.t0.elapsed_time(e) * 1e-3
+            out.append(SimEvent(resource, st, max(st, en), label, batch, layer, rnd))
+        self._pending.clear()
+        return out
+
+
+def export_json(result: SimResult) -> str:
+    events = sorted(result.trace, key=lambda e: (e.start, e.resource, e.end, e.label))
+    doc = {
+        "total_time_s": round(result.total_time, 6),
+        "tokens_generated": result.tokens_generated,
+        "throughput": round(result.throughput, 6),
+        "peak_gpu_bytes": result.peak_gpu_bytes,
+        "rounds_executed": result.rounds_executed,
+        "per_resource_busy_s": {k: round(v, 6) for k, v in result.per_resource_busy.items()},
+        "events": [
+            {"resource": e.resource, "label": e.label, "batch": e.batch, "layer": e.layer, "round": e.round,
+             "start_s": round(e.start, 6), "end_s": round(e.end, 6)}
+            for e in events
+        ],
+    }
+    return json.dumps(doc, sort_keys=True, indent=2) + "\n"
+
+
+def export_chrome(result: SimResult) -> str:
+    tids = {r: i for i, r in enumerate(RESOURCES)}
+    evs = [{"name": e.label, "ph": "X", "pid": 0, "tid": tids.get(e.resource, 99), "ts": round(e.start * 1e6, 3),
+            "dur": round((e.end - e.start) * 1e6, 3), "args": {"batch": e.batch, "layer": e.layer, "round": e.round}}
+           for e in result.trace]
+    meta = [{"name": "thread_name", "ph": "M", "pid": 0, "tid": i, "args": {"name": r}} for r, i in tids.items()]
+    return json.dumps({"traceEvents": meta + evs}, indent=1) + "\n"

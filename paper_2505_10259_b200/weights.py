@@ -1,0 +1,149 @@
+"""Weight containers and the device/host layouts the kernels consume.
+
+Logical weights follow the Mixtral/Mistral parameterisation
+(wq/wk/wv/wo, attn/ffn RMSNorm, router, per-expert w_gate/w_up/w_down).
+Physical layouts:
+  * wqkv     [(hq+2·hkv)·dh, H]    one K-major GEMM operand for Q, K and V;
+  * FFN layer, one contiguous buffer — the unit the streamer moves:
+        gate_up [E, 2I, H]  gate/up rows interleaved in 64-row blocks so one
+                            tcgen05 N-tile holds matching gate and up rows and
+                            the SwiGLU is fused into the GEMM epilogue;
+        down    [E, H, I]
+    Its byte size equals the reference's ffn_bytes_per_layer
+    (presets.py:33-35: 2·3·H·I·E) exactly.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import torch
+
+from .config import ModelArch
+
+SWIGLU_BLOCK = 64
+
+
+def _bf16(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(torch.bfloat16)
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16)
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[.., I, H] ×2 → [.., 2I, H] with 64-row gate/up blocks alternating."""
+    *lead, I, H = w_gate.shape
+    assert I % SWIGLU_BLOCK == 0
+    g = w_gate.reshape(*lead, I // SWIGLU_BLOCK, 1, SWIGLU_BLOCK, H)
+    u = w_up.reshape(*lead, I // SWIGLU_BLOCK, 1, SWIGLU_BLOCK, H)
+    return torch.cat([g, u], dim=-3).reshape(*lead, 2 * I, H)
+
+
+def pack_ffn(w_gate, w_up, w_down) -> torch.Tensor:
+    """Flat bf16 buffer [gate_up | down] of one layer (E leading, or dense)."""
+    gu = interleave_gate_up(_bf16(w_gate), _bf16(w_up))
+    return torch.cat([gu.reshape(-1), _bf16(w_down).reshape(-1)])
+
+
+def ffn_offsets(arch: ModelArch) -> tuple[int, int, int]:
+    """(elements of gate_up, elements of down, total bytes) of one layer."""
+    E = max(arch.n_expert, 1)
+    gu = E * 2 * arch.inter * arch.hidden
+    dn = E * arch.hidden * arch.inter
+    return gu, dn, (gu + dn) * 2
+
+
+@dataclasses.dataclass
+class LayerWeights:
+    attn_norm: torch.Tensor
+    wqkv: torch.Tensor
+    wo: torch.Tensor
+    ffn_norm: torch.Tensor
+    router: torch.Tensor | None
+    ffn: torch.Tensor | None  # packed FFN when HBM-resident (None when host-streamed)
+
+
+@dataclasses.dataclass
+class ModelWeights:
+    arch: ModelArch
+    embed: torch.Tensor
+    final_norm: torch.Tensor
+    lm_head: torch.Tensor
+    layers: list[LayerWeights]
+    host_ffn: dict[int, torch.Tensor]  # layer -> pinned host buffer (streamed layers)
+
+    def resident_bytes(self) -> int:
+        n = self.embed.numel() + self.final_norm.numel() + self.lm_head.numel()
+        for L in self.layers:
+            for t in (L.attn_norm, L.wqkv, L.wo, L.ffn_norm, L.router, L.ffn):
+                if t is not None:
+                    n += t.numel()
+        return 2 * n
+
+
+def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset()) -> ModelWeights:
+    """Build device weights from logical (HF-shaped) arrays — numpy or torch."""
+    dev = torch.device(device)
+    layers = []
+    host = {}
+    for li, L in enumerate(W["layers"]):
+        wqkv = torch.cat([_bf16(L["wq"]), _bf16(L["wk"]), _bf16(L["wv"])], dim=0).to(dev).contiguous()
+        packed = pack_ffn(L["w_gate"], L["w_up"], L["w_down"])
+        if li in stream_layers:
+            host[li] = packed.pin_memory() if dev.type == "cuda" else packed
+            ffn = None
+        else:
+            ffn = packed.to(dev)
+        layers.append(LayerWeights(
+            attn_norm=_bf16(L["attn_norm"]).to(dev),
+            wqkv=wqkv,
+            wo=_bf16(L["wo"]).to(dev).contiguous(),
+            ffn_norm=_bf16(L["ffn_norm"]).to(dev),
+            router=_bf16(L["router"]).to(dev).contiguous() if arch.is_moe else None,
+            ffn=ffn,
+        ))
+    return ModelWeights(arch, _bf16(W["embed"]).to(dev).contiguous(), _bf16(W["final_norm"]).to(dev),
+                        _bf16(W["lm_head"]).to(dev).contiguous(), layers, host)
+
+
+def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
+              host_alloc=None, std: float = 0.02) -> ModelWeights:
+    """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
+
+    Generated on the GPU; streamed FFN layers are generated in HBM one at a
+    time and copied into pinned host buffers from ``host_alloc(nbytes)``.
+    """
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+
+    def randn(*shape):
+        t = torch.empty(*shape, dtype=torch.bfloat16, device=dev)
+        t.normal_(0.0, std, generator=g)
+        return t
+
+    ones = lambda n: torch.ones(n, dtype=torch.bfloat16, device=dev)  # noqa: E731
+    _, _, ffn_bytes = ffn_offsets(arch)
+    layers = []
+    host = {}
+    for li in range(arch.n_layer):
+        ffn = randn(ffn_bytes // 2)
+        if li in stream_layers:
+            buf = host_alloc(ffn_bytes) if host_alloc is not None else torch.empty(
+                ffn_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
+            buf = buf.view(torch.bfloat16)
+            buf.copy_(ffn)
+            host[li] = buf
+            del ffn
+            ffn = None
+        layers.append(LayerWeights(
+            attn_norm=ones(arch.hidden),
+            wqkv=randn(arch.qkv_rows, arch.hidden),
+            wo=randn(arch.hidden, arch.n_head * arch.head_dim),
+            ffn_norm=ones(arch.hidden),
+            router=randn(arch.n_expert, arch.hidden) if arch.is_moe else None,
+            ffn=ffn,
+        ))
+    torch.cuda.synchronize(dev) if dev.type == "cuda" else None
+    return ModelWeights(arch, randn(arch.vocab, arch.hidden), ones(arch.hidden), randn(arch.vocab, arch.hidden),
+                        layers, host)

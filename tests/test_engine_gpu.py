@@ -1,0 +1,117 @@
+"""End-to-end parity of the B200 engine on the tiny pair (config 1) against the
+CPU oracle, plus the executor's trace and forced-acceptance contracts."""
+import collections
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import accept_ref, decode_ref, model_ref, tiny
+from paper_2505_10259_b200 import TINY_DRAFT, TINY_TARGET, Policy, Workload
+from paper_2505_10259_b200.api import build_engine
+from paper_2505_10259_b200.engine import Forced
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pair():
+    return tiny.weights()
+
+
+@pytest.mark.parametrize("stream_layers,S,bs,n_cand,max_new", [
+    ({1, 3}, 8, 4, 4, 12),
+    (set(), 6, 3, 2, 9),
+    ({0, 1, 2, 3}, 7, 4, 6, 20),   # odd split: batches of 4 and 3
+    ({2}, 16, 8, 4, 16),            # config 1: batch 8, draft length 4, greedy
+])
+def test_generate_greedy_matches_oracle(pair, stream_layers, S, bs, n_cand, max_new):
+    tw, dw = pair
+    prompts = tiny.prompts(S, seed=S)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=stream_layers)
+    got = eng.generate(prompts, max_new, Policy(2 * bs, bs, bs, n_cand))
+    rec = []
+    want, rounds = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts, max_new, n_cand, bs, record=rec)
+    assert got == want
+    assert eng.last_session.rounds == rounds
+    counts = collections.Counter(int(c) for r in rec for c in r["counts"] if c > 0)
+    assert len(counts) >= 3, counts  # several accept lengths exercised
+
+
+def test_draft_chunking_matches(pair):
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=3)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0})
+    got = eng.generate(prompts, 10, Policy(8, 4, 1, 4))   # bs_draft = 1: four draft chunks
+    want, _ = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts, 10, 4, 4)
+    assert got == want
+
+
+def test_verify_logits_within_tolerance(pair):
+    """Target logits of a prefill vs the bf16-mirroring oracle: |Δ| ≤ 0.05 + 2% (bf16 activations)."""
+    tw, dw = pair
+    prompts = tiny.prompts(3, seed=7)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1})
+    s = eng.new_session(3, 2, 64, 4)
+    eng.prefill(s, prompts, 8)
+    kv = model_ref.KV(tiny.TARGET, 3, 64)
+    want = model_ref.forward(tiny.TARGET, tw, kv, [0, 1, 2], prompts, [0, 0, 0], True, "last")
+    got = eng.target.ws.get("logits", (3, tiny.TARGET.vocab), torch.float32).cpu().numpy()
+    np.testing.assert_allclose(got, np.concatenate(want), atol=0.05, rtol=0.02)
+
+
+def test_sampling_mode_runs_and_respects_budget(pair):
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=11)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={3})
+    out = eng.generate(prompts, 15, Policy(8, 4, 4, 3), mode="sample", seed=5, temperature=0.8)
+    assert all(len(o) == 15 for o in out)
+    assert all(0 <= t < TINY_TARGET.vocab for o in out for t in o)
+
+
+def test_forced_acceptance_matches_reference_pmf(pair):
+    """Forced mode commits counts drawn from AcceptanceModel(p, n): the empirical
+    histogram matches specpipe's pmf (acceptance.py:29-38) within 5σ."""
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 2})
+    p, n = 0.7, 4
+    res = eng.run_decoding(Policy(32, 32, 32, n), Workload(64, 40, 400, p), acceptance=Forced(p), max_rounds=24)
+    s = eng.last_session
+    # rebuild the per-round counts from the committed token lists (none hit the budget)
+    assert (s.remaining > 0).all()
+    hist = collections.Counter()
+    for rnd in range(res.rounds_executed):
+        b = rnd % 2
+        hist.update(decode_ref.forced_counts(0, rnd, b, p, n, 32).tolist())
+    total = sum(hist.values())
+    committed = sum(len(o) for o in s.out)
+    assert committed == sum(k * v for k, v in hist.items())
+    pmf = accept_ref.pmf(p, n)
+    for k in range(1, n + 2):
+        mu = total * pmf[k - 1]
+        assert abs(hist[k] - mu) <= 5 * np.sqrt(mu * (1 - pmf[k - 1])) + 1
+
+
+def test_run_decoding_trace_contracts(pair):
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2})
+    res = eng.run_decoding(Policy(16, 8, 8, 4), Workload(16, 32, 24, 0.8), acceptance=Forced(0.8))
+    assert res.tokens_generated == 16 * 24
+    assert res.total_time > 0 and res.throughput > 0
+    by_round = collections.defaultdict(lambda: {"verify": set(), "draft": set()})
+    for ev in res.trace:
+        assert ev.end >= ev.start
+        if ev.round is None or ev.batch is None:
+            continue
+        side = "draft" if ev.label.startswith("draft") else "verify"
+        by_round[ev.round][side].add(ev.batch)
+    for rnd, sides in by_round.items():
+        assert sides["verify"].isdisjoint(sides["draft"])
+    # per-stream exclusivity (T7: one timeline per CUDA stream)
+    for res_name in ("GPU_TARGET",):
+        evs = sorted((e for e in res.trace if e.resource == res_name and e.label in ("attn_gpu", "ffn_gpu")),
+                     key=lambda e: e.start)
+        for a, b in zip(evs, evs[1:]):
+            assert b.start >= a.end - 1e-6
+    loads = [e for e in res.trace if e.label == "ffn_load"]
+    assert loads, "streamed layers must show copy-engine events"

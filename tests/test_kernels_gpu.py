@@ -1,0 +1,327 @@
+"""Kernel-level parity of every C-ABI entry point on the B200.
+
+Integer / index work (accept/reject, sampling, routing permutation, gathers)
+is checked bit-exact against the CPU oracle or an exact numpy restatement;
+floating-point kernels against fp32 references with the tolerance stated in
+each test (bf16 storage: one bf16 ulp is 2^-8 relative).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import accept_ref
+from paper_2505_10259_b200 import native
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _i32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(DEV)
+
+
+def _f32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(DEV)
+
+
+# ----------------------------------------------------------------- K7 ---
+
+def _teacher_forced(rng, bs, n, V, ties=True):
+    logits = rng.normal(0, 3, size=(bs, n + 1, V)).astype(np.float32)
+    if ties:  # exact ties on some rows: argmax must be the lowest index
+        for s in range(0, bs, 3):
+            row = logits[s, 0]
+            m = row.max() + 1.0
+            row[7] = m
+            row[V - 3] = m
+    amax = logits.argmax(-1)
+    k = rng.integers(0, n + 1, size=bs)  # forced mismatch position (n = all accepted)
+    draft = amax[:, :n].copy()
+    for s in range(bs):
+        if k[s] < n:
+            draft[s, k[s]] = (amax[s, k[s]] + 1 + rng.integers(0, V - 1)) % V
+    return logits, draft.astype(np.int32), k
+
+
+@pytest.mark.parametrize("bs,n,V", [(1, 1, 17), (37, 4, 1024), (64, 8, 32768), (5, 31, 1000)])
+def test_accept_greedy_bit_exact(bs, n, V):
+    rng = np.random.default_rng(bs * 100 + n)
+    logits, draft, k = _teacher_forced(rng, bs, n, V)
+    remaining = rng.integers(0, n + 3, size=bs).astype(np.int32)
+    tok = torch.empty((bs, n + 1), dtype=torch.int32, device=DEV)
+    cnt = torch.empty(bs, dtype=torch.int32, device=DEV)
+    native.accept_greedy(_i32(draft), _f32(logits), _i32(remaining), tok, cnt)
+    torch.cuda.synchronize()
+    want_tok, want_cnt = accept_ref.accept_greedy(draft, logits, remaining)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), want_cnt)
+    np.testing.assert_array_equal(tok.cpu().numpy(), want_tok)
+    # every accept length 0..n is exercised and counted as k+1 (clamped)
+    np.testing.assert_array_equal(want_cnt, np.minimum(k + 1, remaining))
+
+
+def test_accept_greedy_forced():
+    rng = np.random.default_rng(5)
+    bs, n, V = 50, 4, 512
+    logits, draft, _ = _teacher_forced(rng, bs, n, V, ties=False)
+    forced = rng.integers(1, n + 2, size=bs).astype(np.int32)
+    remaining = np.full(bs, 100, np.int32)
+    tok = torch.empty((bs, n + 1), dtype=torch.int32, device=DEV)
+    cnt = torch.empty(bs, dtype=torch.int32, device=DEV)
+    native.accept_greedy(_i32(draft), _f32(logits), _i32(remaining), tok, cnt, forced=_i32(forced))
+    torch.cuda.synchronize()
+    want_tok, want_cnt = accept_ref.accept_greedy(draft, logits, remaining, forced)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), forced)
+    np.testing.assert_array_equal(tok.cpu().numpy(), want_tok)
+
+
+@pytest.mark.parametrize("bs,n,V,temp", [(16, 4, 1024, 1.0), (8, 6, 32768, 0.7), (3, 1, 300, 1.3)])
+def test_accept_sample_bit_exact(bs, n, V, temp):
+    rng = np.random.default_rng(V + n)
+    logits = rng.normal(0, 2, size=(bs, n + 1, V)).astype(np.float32)
+    dlog = (logits[:, :n] + rng.normal(0, 1.0, size=(bs, n, V))).astype(np.float32)
+    u_d = rng.random((bs, n), dtype=np.float32)
+    draft = np.zeros((bs, n), np.int32)
+    q = np.zeros((bs, n, V), np.float32)
+    for j in range(n):
+        t, p = accept_ref.sample_tokens(dlog[:, j], u_d[:, j], temp, want_probs=True)
+        draft[:, j] = t
+        q[:, j] = p
+    u_acc = rng.random((bs, n), dtype=np.float32)
+    u_res = rng.random(bs, dtype=np.float32)
+    # place some uniforms exactly on the acceptance boundary u·q = p
+    rem = np.full(bs, 1000, np.int32)
+    tok = torch.empty((bs, n + 1), dtype=torch.int32, device=DEV)
+    cnt = torch.empty(bs, dtype=torch.int32, device=DEV)
+    native.accept_sample(_i32(draft), _f32(logits), _f32(q), _f32(u_acc), _f32(u_res), _i32(rem), tok, cnt, temp)
+    torch.cuda.synchronize()
+    want_tok, want_cnt = accept_ref.accept_sample(draft, logits, q, u_acc, u_res, rem, temp)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), want_cnt)
+    np.testing.assert_array_equal(tok.cpu().numpy(), want_tok)
+
+
+@pytest.mark.parametrize("rows,V", [(7, 1024), (33, 32768), (4, 100)])
+def test_sample_tokens_bit_exact(rows, V):
+    rng = np.random.default_rng(rows)
+    logits = rng.normal(0, 4, size=(rows, V)).astype(np.float32)
+    u = rng.random(rows, dtype=np.float32)
+    tok = torch.empty(rows, dtype=torch.int32, device=DEV)
+    probs = torch.empty((rows, V), dtype=torch.float32, device=DEV)
+    native.sample_tokens(_f32(logits), tok, uniforms=_f32(u), out_probs=probs, temperature=0.9)
+    torch.cuda.synchronize()
+    wt, wp = accept_ref.sample_tokens(logits, u, 0.9, want_probs=True)
+    np.testing.assert_array_equal(tok.cpu().numpy(), wt)
+    np.testing.assert_array_equal(probs.cpu().numpy(), wp)  # bit-exact probabilities
+    native.sample_tokens(_f32(logits), tok)  # greedy
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(tok.cpu().numpy(), logits.argmax(-1))
+
+
+# ----------------------------------------------------------------- K2 ---
+
+@pytest.mark.parametrize("T,H,E", [(1, 256, 8), (300, 256, 8), (1280, 6144, 8), (2049, 512, 4)])
+def test_router_top2(T, H, E):
+    g = torch.Generator(device=DEV).manual_seed(T)
+    x = torch.randn(T, H, device=DEV, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(E, H, device=DEV, generator=g) * 0.1).to(torch.bfloat16)
+    offs = torch.empty(E + 1, dtype=torch.int32, device=DEV)
+    perm = torch.empty(2 * T, dtype=torch.int32, device=DEV)
+    roww = torch.empty(2 * T, dtype=torch.float32, device=DEV)
+    trows = torch.empty((T, 2), dtype=torch.int32, device=DEV)
+    xperm = torch.empty((2 * T, H), dtype=torch.bfloat16, device=DEV)
+    idx = torch.empty((T, 2), dtype=torch.int32, device=DEV)
+    w = torch.empty((T, 2), dtype=torch.float32, device=DEV)
+    ws = torch.empty(native.router_workspace_bytes(T, E), dtype=torch.uint8, device=DEV)
+    native.router_top2(x, wg, offs, perm, roww, trows, xperm, ws, topk_idx=idx, topk_w=w)
+    torch.cuda.synchronize()
+    logits = (x.float() @ wg.float().T).double().cpu().numpy()
+    order = np.argsort(-logits, axis=1, kind="stable")
+    gap = logits[np.arange(T), order[:, 1]] - logits[np.arange(T), order[:, 2]]
+    gap01 = logits[np.arange(T), order[:, 0]] - logits[np.arange(T), order[:, 1]]
+    ok = (gap > 1e-3) & (gap01 > 1e-3)  # decisions not within fp32 accumulation noise
+    got_idx = idx.cpu().numpy()
+    np.testing.assert_array_equal(got_idx[ok], order[ok, :2])
+    # renormalised pair weights, fp32 softmax tolerance 1e-5
+    l0 = logits[np.arange(T), got_idx[:, 0]]
+    l1 = logits[np.arange(T), got_idx[:, 1]]
+    w1 = 1.0 / (1.0 + np.exp(l0 - l1))
+    np.testing.assert_allclose(w.cpu().numpy(), np.stack([1 - w1, w1], 1), atol=2e-5)
+    # permutation: stable expert-major order, exact
+    flat = got_idx.reshape(-1)
+    counts = np.bincount(flat, minlength=E)
+    np.testing.assert_array_equal(offs.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
+    want_perm = np.concatenate([np.nonzero(flat == e)[0] for e in range(E)]) // 2
+    np.testing.assert_array_equal(perm.cpu().numpy(), want_perm)
+    tr = trows.cpu().numpy().reshape(-1)
+    np.testing.assert_array_equal(perm.cpu().numpy()[tr], np.arange(2 * T) // 2)
+    np.testing.assert_array_equal(roww.cpu().numpy()[tr], w.cpu().numpy().reshape(-1))
+    assert torch.equal(xperm, x[perm.long()])
+
+
+def test_moe_combine():
+    T, H = 77, 512
+    y = torch.randn(2 * T, H, device=DEV).to(torch.bfloat16)
+    resid = torch.randn(T, H, device=DEV).to(torch.bfloat16)
+    trows = torch.randperm(2 * T, device=DEV).to(torch.int32).view(T, 2)
+    out = torch.empty(T, H, dtype=torch.bfloat16, device=DEV)
+    native.moe_combine(y, trows, resid, out)
+    moe = (y[trows[:, 0].long()].float() + y[trows[:, 1].long()].float()).to(torch.bfloat16)
+    want = (resid.float() + moe.float()).to(torch.bfloat16)
+    assert torch.equal(out, want)
+
+
+# ------------------------------------------------------------- K3/K4/K5 ---
+
+def _bf16_close(got, want, rel=1.5e-2):
+    """bf16 output: |err| ≤ rel·(|want| + rms(want)) (fp32 accumulation-order + one rounding)."""
+    got, want = got.float(), want.float()
+    scale = want.abs() + want.pow(2).mean().sqrt()
+    bad = ((got - want).abs() > rel * scale).sum().item()
+    assert bad == 0, f"{bad} elements off; max err {(got - want).abs().max().item()}"
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (128, 128, 128), (200, 384, 256), (1280, 8192, 6144),
+                                   (77, 32768, 512), (4096, 4096, 4096), (3, 32, 64)])
+def test_gemm_dense(M, N, K):
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ref = a.float() @ b.float().T
+    out = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
+    native.gemm(a, b, out)
+    _bf16_close(out, ref)
+    out32 = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    native.gemm(a, b, out32, native.EPI_F32)
+    torch.testing.assert_close(out32, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+    r = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
+    outr = torch.empty_like(out)
+    native.gemm(a, b, outr, native.EPI_BF16_RESID, r)
+    _bf16_close(outr, ref.to(torch.bfloat16).float() + r.float())
+
+
+@pytest.mark.parametrize("M,I,K", [(5, 128, 64), (300, 512, 256), (257, 16384 // 8, 6144 // 4)])
+def test_gemm_swiglu(M, I, K):
+    g = torch.Generator(device=DEV).manual_seed(M)
+    a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(I, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    wu = (torch.randn(I, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    from paper_2505_10259_b200.weights import interleave_gate_up
+
+    b = interleave_gate_up(wg, wu).contiguous()
+    out = torch.empty(M, I, dtype=torch.bfloat16, device=DEV)
+    native.gemm(a, b, out, native.EPI_SWIGLU)
+    gate = a.float() @ wg.float().T
+    up = a.float() @ wu.float().T
+    _bf16_close(out, torch.nn.functional.silu(gate) * up)
+
+
+@pytest.mark.parametrize("counts", [[0, 3, 130, 0, 1, 255, 256, 7], [320] * 8, [1, 0, 0, 0, 0, 0, 0, 0],
+                                    [1000, 24, 0, 0, 513, 2, 2, 9]])
+def test_gemm_grouped(counts):
+    E, N, K = len(counts), 256, 384
+    rows = sum(counts)
+    g = torch.Generator(device=DEV).manual_seed(rows)
+    a = torch.randn(rows, K, device=DEV, generator=g).to(torch.bfloat16)
+    b = (torch.randn(E, N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=DEV)
+    w = torch.rand(rows, device=DEV, generator=g)
+    out = torch.zeros(rows, N, dtype=torch.bfloat16, device=DEV)
+    native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, native.EPI_BF16_ROWSCALE, w)
+    ref = torch.zeros(rows, N, device=DEV)
+    o = offs.cpu().numpy()
+    for e in range(E):
+        ref[o[e]:o[e + 1]] = (a[o[e]:o[e + 1]].float() @ b[e].float().T) * w[o[e]:o[e + 1], None]
+    _bf16_close(out, ref)
+
+
+# ----------------------------------------------------------------- K8 ---
+
+def test_embed_rmsnorm():
+    V, H, T = 1000, 6144, 33
+    table = torch.randn(V, H, device=DEV).to(torch.bfloat16)
+    tok = torch.randint(0, V, (T,), device=DEV, dtype=torch.int32)
+    x = torch.empty(T, H, dtype=torch.bfloat16, device=DEV)
+    native.embed(tok, table, x)
+    assert torch.equal(x, table[tok.long()])
+    w = (1 + 0.1 * torch.randn(H, device=DEV)).to(torch.bfloat16)
+    out = torch.empty_like(x)
+    native.rmsnorm(x, w, out, 1e-5)
+    xf = x.float()
+    r = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)
+    want = ((xf * r).to(torch.bfloat16).float() * w.float()).to(torch.bfloat16)
+    diff = (out.float() - want.float()).abs() / want.float().abs().clamp_min(1e-3)
+    assert (diff > 1e-2).sum().item() == 0  # ≤ 1 bf16 ulp (rsqrt rounding)
+
+
+def test_rope_kv_append():
+    T, hq, hkv, dh, ps = 10, 6, 2, 128, 64
+    qkv = torch.randn(T, (hq + 2 * hkv) * dh, device=DEV).to(torch.bfloat16)
+    pos = torch.tensor([0, 1, 2, 100, 500, 63, 64, 65, 700, 3], dtype=torch.int32, device=DEV)
+    slots = torch.tensor([0, 1, 2, 3, 4, 70, 71, 128, 200, 255], dtype=torch.int32, device=DEV)
+    kc = torch.zeros(4, hkv, ps, dh, dtype=torch.bfloat16, device=DEV)
+    vc = torch.zeros_like(kc)
+    q = torch.empty(T, hq * dh, dtype=torch.bfloat16, device=DEV)
+    native.rope_kv_append(qkv, pos, slots, hq, hkv, dh, 1e6, ps, q, kc, vc)
+    torch.cuda.synchronize()
+    import oracle.model_ref as M
+
+    x = qkv.float().cpu().numpy()
+    P = pos.cpu().numpy()
+    qr = M.rope(x[:, :hq * dh].reshape(T, hq, dh), P, 1e6)
+    kr = M.rope(x[:, hq * dh:(hq + hkv) * dh].reshape(T, hkv, dh), P, 1e6)
+    np.testing.assert_allclose(q.float().cpu().numpy().reshape(T, hq, dh), qr, atol=2e-2, rtol=1e-2)
+    kcn, vcn = kc.float().cpu().numpy(), vc.float().cpu().numpy()
+    for t in range(T):
+        s = int(slots[t])
+        np.testing.assert_allclose(kcn[s // ps, :, s % ps], kr[t], atol=2e-2, rtol=1e-2)
+        np.testing.assert_array_equal(vcn[s // ps, :, s % ps], x[t, (hq + hkv) * dh:].reshape(hkv, dh))
+
+
+# ----------------------------------------------------------------- K6 ---
+
+def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
+    out = torch.zeros_like(q, dtype=torch.float32)
+    G = hq // hkv
+    for s in range(len(kvb)):
+        a, b = int(q_start[s]), int(q_start[s + 1])
+        n = b - a
+        nk = int(kvb[s]) + n
+        pages = bt[s]
+        K = torch.cat([kc[pages[i]] for i in range((nk + ps - 1) // ps)], dim=1)[:, :nk].float()  # [hkv, nk, dh]
+        V = torch.cat([vc[pages[i]] for i in range((nk + ps - 1) // ps)], dim=1)[:, :nk].float()
+        Q = q[a:b].view(n, hq, dh).float()
+        for h in range(hq):
+            S = Q[:, h] @ K[h // G].T / math.sqrt(dh)
+            mask = torch.arange(nk, device=DEV)[None, :] > (int(kvb[s]) + torch.arange(n, device=DEV))[:, None]
+            S = S.masked_fill(mask, float("-inf"))
+            out[a:b, h * dh:(h + 1) * dh] = torch.softmax(S, -1) @ V[h // G]
+    return out
+
+
+@pytest.mark.parametrize("dh,hq,hkv,qlens,kvbs", [
+    (128, 48, 8, [5] * 6, [503, 0, 64, 1, 777, 130]),   # verify, 8x22B heads
+    (64, 4, 2, [5, 5, 5], [10, 100, 0]),                 # verify, tiny heads
+    (128, 32, 8, [17, 1, 64, 100], [0, 0, 0, 0]),        # prefill
+    (64, 4, 2, [33, 1], [3, 200]),                       # mixed
+])
+def test_attn_paged(dh, hq, hkv, qlens, kvbs):
+    ps = 64
+    bs = len(qlens)
+    max_len = max(q + k for q, k in zip(qlens, kvbs))
+    pps = (max_len + ps - 1) // ps + 1
+    npages = bs * pps
+    g = torch.Generator(device=DEV).manual_seed(dh + bs)
+    kc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
+    vc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
+    perm = torch.randperm(npages, device=DEV, generator=g).to(torch.int32)  # scattered pages
+    bt = perm.view(bs, pps)
+    qs = torch.tensor(np.concatenate([[0], np.cumsum(qlens)]), dtype=torch.int32, device=DEV)
+    kvb = torch.tensor(kvbs, dtype=torch.int32, device=DEV)
+    T = sum(qlens)
+    q = torch.randn(T, hq * dh, device=DEV, generator=g).to(torch.bfloat16)
+    out = torch.empty(T, hq * dh, dtype=torch.bfloat16, device=DEV)
+    native.attn_paged(q, kc, vc, bt, qs, kvb, max(qlens), hq, hkv, dh, ps, 1 / math.sqrt(dh), out)
+    ref = _attn_ref(q, kc, vc, bt.long().cpu().numpy(), qs.cpu().numpy(), kvb.cpu().numpy(), hq, hkv, dh, ps)
+    # P is rounded to bf16 for the PV product: |err| ≤ 2e-2 absolute on O(1) outputs
+    torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
