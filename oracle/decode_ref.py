@@ -35,8 +35,19 @@ def forced_counts(seed: int, rnd: int, batch: int, p: float, n_cand: int, size: 
 
 def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_new: int, n_cand: int,
              bs_decoding: int, mode: str = "greedy", seed: int = 0, forced_p: float | None = None,
-             temperature: float = 1.0, mirror: bool = True, record: list | None = None):
+             temperature: float = 1.0, mirror: bool = True, record: list | None = None,
+             margins: list | None = None):
+    """Returns (committed token lists, rounds).  ``margins`` (optional, filled
+    per sequence) receives the top-1 − top-2 logit gap of the target row that
+    produced each committed token: a GPU/oracle divergence is legitimate only
+    where that gap is inside the bf16 noise of the two computations."""
     S = len(prompts)
+    gap = [[] for _ in range(S)]
+
+    def top2_gap(row):
+        part = np.partition(row, -2)
+        return float(part[-1] - part[-2])
+
     assert 1 <= S <= 2 * bs_decoding
     batches = [list(range(0, min(bs_decoding, S))), list(range(bs_decoding, S))]
     max_len = max(len(p) for p in prompts) + max_new + n_cand + 2
@@ -59,6 +70,7 @@ def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_ne
             first = accept_ref.sample_tokens(lg, uniforms(seed, -2, b, 3, len(members)), temperature)
         for j, i in enumerate(members):
             out[i].append(int(first[j]))
+            gap[i].append(top2_gap(lg[j]))
             remaining[i] -= 1
             t_last[i] = first[j]
 
@@ -108,6 +120,7 @@ def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_ne
                 c = int(cnt[j])
                 if c > 0:
                     out[i].extend(int(x) for x in tok[j, :c])
+                    gap[i].extend(top2_gap(lg[j, m]) for m in range(c))
                     remaining[i] -= c
                     t_last[i] = tok[j, c - 1]
                     ctx[i] += c
@@ -115,4 +128,6 @@ def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_ne
         if batches[o] and (remaining[batches[o]] > 0).any():
             drafts[o] = draft(o, rnd)
         rnd += 1
+    if margins is not None:
+        margins.extend(gap)
     return out, rnd

@@ -171,20 +171,21 @@ def forward(arch: Arch, W: dict, kv: KV, seqs: list[int], tokens: list[np.ndarra
         hn = rmsnorm(h, L["ffn_norm"], arch.eps, mirror)
         if arch.n_expert:
             logits_r = (hn.astype(np.float64) @ L["router"].T.astype(np.float64)).astype(np.float32)
-            out = np.zeros_like(h)
-            for t in range(h.shape[0]):
-                order = sorted(range(arch.n_expert), key=lambda e: (-logits_r[t, e], e))
-                e0, e1 = order[0], order[1]
-                w1 = np.float32(1.0) / (np.float32(1.0) + np.exp(np.float32(logits_r[t, e0] - logits_r[t, e1])))
-                w0 = np.float32(1.0) - w1
-                ys = []
-                for e, wt in ((e0, w0), (e1, w1)):
-                    g = hn[t] @ L["w_gate"][e].T
-                    u = hn[t] @ L["w_up"][e].T
-                    act = rnd(silu(g) * u)
-                    ys.append(rnd((act @ L["w_down"][e].T) * wt))
-                out[t] = rnd(ys[0] + ys[1])
-            x = rnd(h + out)
+            # top-2, ties → lower expert index (stable sort of −logit)
+            top = np.argsort(-logits_r, axis=1, kind="stable")[:, :2]
+            rows = np.arange(h.shape[0])
+            l0, l1 = logits_r[rows, top[:, 0]], logits_r[rows, top[:, 1]]
+            w1 = (np.float32(1.0) / (np.float32(1.0) + np.exp(l0 - l1))).astype(np.float32)
+            wts = np.stack([np.float32(1.0) - w1, w1], axis=1)
+            ys = np.zeros((h.shape[0], 2, h.shape[1]), np.float32)
+            for e in range(arch.n_expert):  # experts process their routed rows as one batch
+                tok, slot = np.nonzero(top == e)
+                if tok.size == 0:
+                    continue
+                xe = hn[tok]
+                act = rnd(silu(xe @ L["w_gate"][e].T) * (xe @ L["w_up"][e].T))
+                ys[tok, slot] = rnd((act @ L["w_down"][e].T) * wts[tok, slot][:, None])
+            x = rnd(h + rnd(ys[:, 0] + ys[:, 1]))
         else:
             g = hn @ L["w_gate"].T
             u = hn @ L["w_up"].T

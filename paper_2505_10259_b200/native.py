@@ -73,7 +73,22 @@ def exported_symbols() -> list[str]:
     return sorted(_SIGNATURES)
 
 
+# kernels (or copy-engine DMA batches) each entry point enqueues; summed into
+# ``launches`` so bench.py can report how many of our kernels ran
+_KERNELS_PER_CALL = {"so_router_top2": 3, "so_stream_layer": 0}
+launches = {"kernels": 0, "copies": 0}
+
+
+def reset_launch_counter() -> None:
+    launches["kernels"] = 0
+    launches["copies"] = 0
+
+
 def _check(rc: int, what: str) -> None:
+    if what == "so_stream_layer":
+        launches["copies"] += 1
+    else:
+        launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
     if rc != 0:
         msg = lib().so_status_string(rc).decode()
         raise NativeError(f"{what} failed with status {rc}: {msg}", rc)

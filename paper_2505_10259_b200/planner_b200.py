@@ -1,0 +1,136 @@
+"""B200 re-fit of the reference's placement + cost model (north-star item 4).
+
+Reference pieces and what changes on B200:
+  * assign_tiers (placement.py:167-257): mandatory GPU set = 2-slot FFN window
+    + draft params + draft KV, then FFN layers pinned in ascending order while
+    they fit.  Target KV and attention weights are *not* in its GPU set
+    because the paper runs attention on the CPU.  Here
+    attention runs on the GPU, so target attention weights, embeddings, the
+    router and the paged target KV join the mandatory set, and the host DRAM
+    budget caps how many layers can be streamed.
+  * target_round_time (costmodel.py:60-76): n_layer·(max(attn_cpu, load) +
+    ffn_gpu) assumes no prefetch-ahead (T5).  The streamer keeps the copy
+    engine busy across layers and rounds, so a verification pass costs
+    max(streamed_bytes / B_h2d, compute) plus a per-round host overhead.
+  * decoding_rounds (costmodel.py:79-81): one verification per round (T1).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+from .acceptance import AcceptanceModel, expected_accepted
+from .config import ModelArch
+from .errors import InfeasiblePlan
+from .kvcache import PagedKVCache
+from .weights import ffn_offsets
+
+GB = 1e9
+
+
+@dataclasses.dataclass(frozen=True)
+class B200Rates:
+    """Measured rates of one B200 box (defaults: this pool)."""
+
+    h2d_bytes_per_s: float = 55.5e9        # pinned H2D, measured 55.5 GB/s
+    hbm_bytes_per_s: float = 6552e9        # MEASURED_PEAKS.json
+    tensor_flops: float = 1375.5e12        # sustained bf16, MEASURED_PEAKS.json
+    tensor_efficiency: float = 0.5         # achieved fraction for skinny MoE tiles (re-fit by calibrate)
+    round_overhead_s: float = 0.004        # host enqueue + barrier per round
+
+
+@dataclasses.dataclass(frozen=True)
+class OffloadPlan:
+    bs_decoding: int
+    n_cand: int
+    stream_layers: tuple[int, ...]
+    pinned_layers: tuple[int, ...]
+    n_slots: int
+    hbm_bytes: dict
+    host_bytes: int
+    streamed_bytes_per_pass: int
+    t_stream_s: float
+    t_compute_s: float
+    t_round_s: float
+    expected_tokens_per_round: float
+    tokens_per_s: float
+
+    def as_dict(self) -> dict:
+        d = dataclasses.asdict(self)
+        d["stream_layers"] = len(self.stream_layers)
+        d["pinned_layers"] = len(self.pinned_layers)
+        return d
+
+
+def resident_bytes(arch: ModelArch, include_ffn: bool) -> int:
+    """HBM bytes of a model's always-resident tensors."""
+    per_layer = (arch.qkv_rows * arch.hidden + arch.hidden * arch.n_head * arch.head_dim) * 2
+    small = arch.small_resident_bytes()
+    b = arch.embed_bytes() + arch.n_layer * per_layer + small
+    if include_ffn:
+        b += arch.n_layer * ffn_offsets(arch)[2]
+    return b
+
+
+def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 64) -> int:
+    return (PagedKVCache.bytes_needed(target, n_seq, max_len, page_size)
+            + PagedKVCache.bytes_needed(draft, n_seq, max_len, page_size))
+
+
+def workspace_bytes(target: ModelArch, draft: ModelArch, bs: int, n_cand: int) -> int:
+    T = bs * (n_cand + 1)
+    H, I = target.hidden, target.inter
+    tgt = T * (6 * H + target.qkv_rows + 2 * target.n_head * target.head_dim) * 2 + 2 * T * (2 * H + I) * 2 \
+        + T * target.vocab * 4
+    drf = bs * (6 * draft.hidden + draft.qkv_rows + draft.inter) * 2 + bs * draft.vocab * 4
+    return tgt + drf + (1 << 30)  # + allocator / cuBLAS-free slack
+
+
+def verify_flops(target: ModelArch, bs: int, n_cand: int, ctx: int) -> float:
+    return bs * (n_cand + 1) * target.verify_flops_per_token(ctx)
+
+
+def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
+                 acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
+                 n_slots: int = 2, bs_candidates=None, page_size: int = 64) -> OffloadPlan:
+    """Choose bs_decoding and the pinned / streamed split that maximise
+    predicted decode tokens/s under both memory budgets."""
+    layer_bytes = ffn_offsets(target)[2]
+    fixed = resident_bytes(target, False) + resident_bytes(draft, True) + n_slots * layer_bytes
+    e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
+    max_len = ctx_len + max_new + n_cand + 2
+    best = None
+    cands = bs_candidates or [b for b in range(8, 2049, 8)]
+    for bs in cands:
+        kv = kv_bytes(target, draft, 2 * bs, max_len, page_size)
+        ws = workspace_bytes(target, draft, bs, n_cand)
+        free = hbm_budget - fixed - kv - ws
+        if free < 0:
+            continue
+        pinned = min(target.n_layer, int(free // layer_bytes))
+        streamed = target.n_layer - pinned
+        if streamed * layer_bytes > host_budget:
+            continue
+        S = streamed * layer_bytes
+        t_stream = S / rates.h2d_bytes_per_s
+        t_comp = verify_flops(target, bs, n_cand, ctx_len) / (rates.tensor_flops * rates.tensor_efficiency)
+        t_round = max(t_stream, t_comp) + rates.round_overhead_s
+        tps = bs * e_tok / t_round
+        if best is None or tps > best[0]:
+            best = (tps, bs, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round)
+    if best is None:
+        raise InfeasiblePlan("no batch size fits the HBM and host budgets")
+    tps, bs, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round = best
+    # pin the first layers (ascending order, placement.py:220-231); stream the rest
+    pinned_l = tuple(range(pinned))
+    stream_l = tuple(range(pinned, target.n_layer))
+    return OffloadPlan(bs, n_cand, stream_l, pinned_l, n_slots if streamed else 0,
+                       {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_ffn": pinned * layer_bytes},
+                       streamed * layer_bytes, S, t_stream, t_comp, t_round, bs * e_tok, tps)
+
+
+def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,
+                          h2d_peak: float, tensor_peak: float) -> float:
+    """C / max(S / B_h2d, F / peak)."""
+    t = max(streamed_bytes / h2d_peak, flops / tensor_peak)
+    return committed_per_round / t if t > 0 else math.inf
