@@ -219,8 +219,10 @@ def main():
             st.copy_marks.clear()
     ev0.record(eng.tgt_stream)
     w0 = time.perf_counter()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects the timed rounds
     for _ in range(steps):
         eng.round(s)  # public API: H2D inputs, verify+draft, barrier, D2H committed tokens
+    torch.cuda.nvtx.range_pop()
     ev1.record(eng.tgt_stream)
     ev1.synchronize()
     wall = time.perf_counter() - w0
@@ -257,7 +259,8 @@ def main():
         E, H, I = tgt.n_expert, tgt.hidden, tgt.inter
         g = torch.Generator(device=device).manual_seed(0)
         a = torch.randn(2 * T, H, device=device, generator=g).to(torch.bfloat16)
-        w = (torch.randn(E * 2 * I, H, device=device, generator=g) * 0.02).to(torch.bfloat16)
+        # weights: the gate_up part of an FFN layer already in an HBM window slot
+        w = st.slots[0] if st else eng.target.w.layers[0].ffn
         cnt = np.full(E, 2 * T // E)
         cnt[: 2 * T - cnt.sum()] += 1
         offs = torch.tensor(np.concatenate([[0], np.cumsum(cnt)]), dtype=torch.int32, device=device)
@@ -277,7 +280,7 @@ def main():
                 "achieved": flops / t_k / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": flops / t_k / 1e12 / peaks["bf16_tflops"], "ms": t_k * 1e3,
                 "shape": f"rows {2 * T} x N {2 * I} x K {H}, {E} experts", "peak_kind": "burst (measured)"}
-        del a, w, act
+        del a, act
     except Exception as exc:  # the headline must still print
         kern = {"error": str(exc)}
 

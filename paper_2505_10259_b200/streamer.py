@@ -103,6 +103,12 @@ class LayerStreamer:
         self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
         self.loaded = [torch.cuda.Event() for _ in range(self.n_slots)]
         self.free = [torch.cuda.Event() for _ in range(self.n_slots)]
+        # torch creates the CUDA event lazily at the first record(); the native
+        # streamer records `loaded` itself, so materialise every handle now
+        # (an uncreated event has handle 0 and both record and wait no-op)
+        for ev in self.loaded + self.free:
+            ev.record(self.copy_stream)
+        assert all(ev.cuda_event != 0 for ev in self.loaded)
         self.k_use = 0      # global index of the next streamed use
         self.k_issued = 0   # copies enqueued so far
         self.bytes_issued = 0

@@ -71,6 +71,25 @@ def test_draft_chunking_matches(pair):
     assert_greedy_parity(got, want, margins)
 
 
+def test_streamer_orders_compute_after_copy(pair):
+    """The expert GEMMs of a streamed layer must wait for its copy: with the
+    copy stream stalled ~100 ms and the window slots poisoned with zeros, the
+    output must still equal the all-resident run."""
+    tw, dw = pair
+    prompts = tiny.prompts(6, seed=21)
+    ref = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=set()).generate(prompts, 8, Policy(6, 3, 3, 4))
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3})
+    st = eng.target.streamer
+    assert all(ev.cuda_event != 0 for ev in st.loaded + st.free)
+    for slot in st.slots:
+        slot.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st.copy_stream):
+        torch.cuda._sleep(200_000_000)  # ≈100 ms of spinning ahead of the first copy
+    got = eng.generate(prompts, 8, Policy(6, 3, 3, 4))
+    assert got == ref
+
+
 def test_verify_logits_within_tolerance(pair):
     """Target logits of a prefill vs the bf16-mirroring oracle: |Δ| ≤ 0.05 + 2% (bf16 activations)."""
     tw, dw = pair
