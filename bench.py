@@ -43,13 +43,17 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("8x22b", "8x7b", "tiny"), default="8x22b")
-    ap.add_argument("--n-cand", type=int, default=4)
+    ap.add_argument("--n-cand", type=int, default=8, help="draft length (8 = the paper's best 8x22B policy)")
     ap.add_argument("--p", type=float, default=0.8)
     ap.add_argument("--ctx", type=int, default=503)
     ap.add_argument("--bs", type=int, default=0, help="per-batch size (0 = planner)")
     ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget (0 = MemAvailable − 14 GB)")
     ap.add_argument("--hbm-gb", type=float, default=0.0, help="HBM budget (0 = device; 8x7b config: 24 GiB cap)")
     ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill"), default="auto",
+                    help="draft KV policy (auto = planner)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="profiling only: override the target's layer count (same per-layer shapes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-out", default="")
     return ap.parse_args()
@@ -113,10 +117,15 @@ def h2d_peak(torch, device) -> float:
     return best
 
 
-def pair(cfg):
+def pair(cfg, layers: int = 0):
+    import dataclasses
+
     from paper_2505_10259_b200 import PAIRS
 
-    return PAIRS[cfg]
+    t, d = PAIRS[cfg]
+    if layers:
+        t = dataclasses.replace(t, n_layer=layers, name=f"{t.name}-{layers}L")
+    return t, d
 
 
 def run_reference(args, rank: int) -> None:
@@ -156,7 +165,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline  # checker only: timed beside the GPU path, never part of it
 
-        tgt, drf = pair(args.config)
+        tgt, drf = pair(args.config)  # full-depth shapes
         cpu = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4)
 
     import torch
@@ -173,7 +182,7 @@ def main():
     torch.cuda.set_device(device)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    tgt, drf = pair(args.config)
+    tgt, drf = pair(args.config, args.layers)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
                                                          "bf16_tflops_sustained": 1400.0}
@@ -188,16 +197,17 @@ def main():
     from paper_2505_10259_b200.planner_b200 import B200Rates
 
     rates = B200Rates(h2d_bytes_per_s=link)
+    modes = ("cached", "reprefill") if args.draft_kv == "auto" else (args.draft_kv,)
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
-                        bs_candidates=[args.bs] if args.bs else None)
+                        bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes)
     t_setup = time.perf_counter()
     store = HostStore()
     eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
                        seed=1 + rank, trace=bool(args.trace_out), host_store=store)
     bs = plan.bs_decoding
     S = 2 * bs
-    policy = Policy(bs_prefill=S, bs_decoding=bs, bs_draft=bs, n_cand=args.n_cand)
-    s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank)
+    s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
+                        bs_draft=plan.bs_draft, draft_kv=plan.draft_kv)
     eng.synthetic_context(s, args.ctx, max_new, seed=rank)
     eng.first_draft(s)
     setup_s = time.perf_counter() - t_setup
@@ -303,7 +313,8 @@ def main():
         "ms_per_step": dev_s / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, random prompt KV, forced acceptance p)",
         "config": {"workload": f"configs[2]: {tgt.name} offloaded + {drf.name} draft, 1 B200, full HBM",
-                   "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand, "acceptance_p": args.p,
+                   "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
+                   "draft_kv": plan.draft_kv, "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "streamed_bytes_per_round": len(plan.stream_layers) * layer_bytes,

@@ -60,7 +60,8 @@ class DecodeSession:
     """All per-run state: caches, per-sequence counters, committed tokens."""
 
     def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
-                 mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int):
+                 mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int,
+                 draft_kv: str = "cached"):
         self.e = engine
         self.n_seq = n_seq
         self.n_cand = n_cand
@@ -69,10 +70,20 @@ class DecodeSession:
         self.temperature = temperature
         self.forced_p = forced_p
         self.bs_draft = bs_draft
+        if draft_kv not in ("cached", "reprefill"):
+            raise ValueError(f"draft_kv must be 'cached' or 'reprefill', got {draft_kv!r}")
+        self.draft_kv = draft_kv
         self.batches = [_Batch(0, min(bs_decoding, n_seq)), _Batch(min(bs_decoding, n_seq), n_seq)]
         dev = engine.device
         self.tkv = PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size)
-        self.dkv = PagedKVCache(engine.draft.arch, n_seq, max_len, dev, engine.page_size)
+        # cached: one persistent draft KV row per sequence.  reprefill (the
+        # paper's draft, PAPER.md:511-519 / costmodel.py:53-57,132-137): the
+        # draft re-reads the whole context each round into a scratch cache
+        # sized for one bs_draft chunk, so HBM goes to a larger batch instead.
+        self.dkv = PagedKVCache(engine.draft.arch, n_seq if draft_kv == "cached" else bs_draft, max_len, dev,
+                                engine.page_size)
+        # token history (position-indexed) for the re-prefilling draft
+        self.hist = torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev) if draft_kv == "reprefill" else None
         self.max_len = max_len
         self.ctx = np.zeros(n_seq, np.int64)
         self.t_last = np.zeros(n_seq, np.int32)
@@ -100,8 +111,11 @@ class Engine:
         self.hw = hw
         self.device = torch.device(device)
         self.page_size = page_size
-        self.tgt_stream = torch.cuda.Stream(device=self.device)
-        self.drf_stream = torch.cuda.Stream(device=self.device)
+        # the verify stream gets the higher priority: each layer's expert GEMMs
+        # must release its window slot promptly or the copy engine idles, while
+        # the draft's (re-)prefill work only has to finish by the barrier
+        self.tgt_stream = torch.cuda.Stream(device=self.device, priority=-1)
+        self.drf_stream = torch.cuda.Stream(device=self.device, priority=0)
         self.tracer = Tracer(trace)
         self._cur = (None, None)  # (round, batch) being verified, for trace tags
         self._marks: dict = {}
@@ -139,9 +153,19 @@ class Engine:
 
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
-                    bs_draft: int | None = None) -> DecodeSession:
+                    bs_draft: int | None = None, draft_kv: str = "cached") -> DecodeSession:
         return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
-                             bs_draft or bs_decoding)
+                             bs_draft or bs_decoding, draft_kv)
+
+    def _hist_write(self, s: DecodeSession, seqs, positions, tokens, stream) -> None:
+        """Record committed tokens in the device-side history (reprefill drafts)."""
+        if s.hist is None or len(seqs) == 0:
+            return
+        flat = (np.asarray(seqs, np.int64) * s.max_len + np.asarray(positions, np.int64))
+        idx = self._up(flat, stream, torch.int64)
+        val = self._up(np.asarray(tokens, np.int32), stream)
+        with torch.cuda.stream(stream):
+            s.hist.view(-1).index_copy_(0, idx, val)
 
     # ---------------------------------------------------------------- prefill
     def prefill(self, s: DecodeSession, prompts: list, max_new: int, bs_prefill: int | None = None,
@@ -159,7 +183,15 @@ class Engine:
             cur.append(i)
             cur_tok += int(L)
         groups.append(cur)
-        for model, kv, stream in ((self.target, s.tkv, self.tgt_stream), (self.draft, s.dkv, self.drf_stream)):
+        models = [(self.target, s.tkv, self.tgt_stream)]
+        if s.draft_kv == "cached":
+            models.append((self.draft, s.dkv, self.drf_stream))
+        else:  # the re-prefilling draft only needs the prompt tokens
+            seqs = np.concatenate([np.full(L, i) for i, L in enumerate(lens)])
+            pos = np.concatenate([np.arange(L) for L in lens])
+            self._hist_write(s, seqs, pos, np.concatenate([np.asarray(p, np.int32) for p in prompts]),
+                             self.drf_stream)
+        for model, kv, stream in models:
             chunks = []
             row0 = 0
             last = []
@@ -203,6 +235,8 @@ class Engine:
         s.t_last[:] = first_np
         s.ctx[:] = lens
         s.remaining[:] = max_new - 1
+        self._hist_write(s, np.arange(s.n_seq), lens, first_np, self.drf_stream)
+        self.drf_stream.synchronize()
 
     def synthetic_context(self, s: DecodeSession, ctx_len: int, max_new: int, seed: int = 0) -> None:
         """Decode-only benchmark input: caches hold ``ctx_len`` random KV rows per
@@ -217,6 +251,9 @@ class Engine:
         s.t_last[:] = rng.integers(0, self.target.arch.vocab, s.n_seq)
         s.ctx[:] = ctx_len
         s.remaining[:] = max_new
+        if s.hist is not None:
+            s.hist.random_(0, self.target.arch.vocab, generator=g)
+            self._hist_write(s, np.arange(s.n_seq), s.ctx, s.t_last, self.drf_stream)
         torch.cuda.synchronize(self.device)
 
     # ------------------------------------------------------------------ draft
@@ -234,6 +271,9 @@ class Engine:
             cm = c_hi - c_lo
             seqs = np.arange(b.lo + c_lo, b.lo + c_hi)
             ctx = s.ctx[seqs]
+            if s.draft_kv == "reprefill":
+                self._draft_chunk_reprefill(s, bi, c_lo, c_hi, seqs, ctx, u_all)
+                continue
             pos = ctx[None, :] + np.arange(n + 1)[:, None]                  # [n+1, cm]
             slots = s.dkv.slots(np.broadcast_to(seqs, pos.shape), pos)
             qs = np.arange(cm + 1, dtype=np.int32)
@@ -264,6 +304,58 @@ class Engine:
                 else:
                     native.sample_tokens(logits, out_tok, stream=st)
         tr.add("GPU_DRAFT", "draft_decode", ev0, tr.mark(st), batch=bi, rnd=rnd)
+
+    def _draft_chunk_reprefill(self, s: DecodeSession, bi: int, c_lo: int, c_hi: int, seqs, ctx, u_all) -> None:
+        """One bs_draft chunk of the paper's draft: prefill the whole context
+        (prompt + committed tokens + t_last) into the scratch cache, take d_1
+        from its last row, then n_cand−1 cached decode steps."""
+        st = self.drf_stream
+        n = s.n_cand
+        cm = c_hi - c_lo
+        local = np.arange(cm)
+        lens = ctx + 1                                    # positions 0..ctx (t_last at ctx)
+        T = int(lens.sum())
+        flat = np.concatenate([seq * s.max_len + np.arange(L) for seq, L in zip(seqs, lens)])
+        pos = np.concatenate([np.arange(L) for L in lens])
+        slots = s.dkv.slots(np.repeat(local, lens), pos)
+        qs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        dpos = ctx[None, :] + np.arange(1, n)[:, None]    # decode steps j = 1..n-1: [n-1, cm]
+        dslots = s.dkv.slots(np.broadcast_to(local, dpos.shape), dpos)
+        parts = [pos.astype(np.int32), slots, qs, np.zeros(cm, np.int32), (qs[1:] - 1).astype(np.int32),
+                 dpos.astype(np.int32).ravel(), dslots.ravel(), np.arange(cm + 1, dtype=np.int32)]
+        if u_all is not None:
+            parts.append(u_all[c_lo:c_hi].T.ravel().view(np.int32))
+        meta = self._up(np.concatenate(parts), st)
+        idx = self._up(flat, st, torch.int64)
+        o = 0
+        pos_d = meta[o:o + T]; o += T
+        slot_d = meta[o:o + T]; o += T
+        qs_d = meta[o:o + cm + 1]; o += cm + 1
+        zero_d = meta[o:o + cm]; o += cm
+        last_d = meta[o:o + cm]; o += cm
+        D = (n - 1) * cm
+        dpos_d = meta[o:o + D]; o += D
+        dslot_d = meta[o:o + D]; o += D
+        dqs_d = meta[o:o + cm + 1]; o += cm + 1
+        u_d = meta[o:].view(torch.float32) if u_all is not None else None
+        with torch.cuda.stream(st):
+            toks = torch.index_select(s.hist.view(-1), 0, idx)
+            last_rows = last_d.long()
+        bt = s.dkv.block_table[:cm]
+        for j in range(n):
+            if j == 0:
+                fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_rows)
+            else:
+                sl = slice((j - 1) * cm, j * cm)
+                fb = ForwardBatch(s.drafts[bi][j - 1, c_lo:c_hi], dpos_d[sl], dslot_d[sl], dqs_d, dpos_d[sl], bt,
+                                  cm, 1)
+            logits = self.draft.forward(fb, s.dkv, st)
+            out_tok = s.drafts[bi][j, c_lo:c_hi]
+            if s.mode == "sample":
+                native.sample_tokens(logits, out_tok, uniforms=u_d[j * cm:(j + 1) * cm],
+                                     out_probs=s.qprobs[bi][c_lo:c_hi, j, :], temperature=s.temperature, stream=st)
+            else:
+                native.sample_tokens(logits, out_tok, stream=st)
 
     # ----------------------------------------------------------------- verify
     def _verify(self, s: DecodeSession, bi: int, rnd: int) -> None:
@@ -329,15 +421,22 @@ class Engine:
         cnt = s.res_cnt[bi][:b.n].numpy()
         tok = s.res_tok[bi][:b.n].numpy()
         total = 0
+        hs, hp, hv = [], [], []
         for j, i in enumerate(b.ids):
             c = int(cnt[j])
             if c <= 0:
                 continue
             s.out[i].extend(int(x) for x in tok[j, :c])
+            if s.hist is not None:  # committed tokens land at positions ctx+1 .. ctx+c
+                hs.append(np.full(c, i))
+                hp.append(s.ctx[i] + 1 + np.arange(c))
+                hv.append(tok[j, :c])
             s.remaining[i] -= c
             s.t_last[i] = tok[j, c - 1]
             s.ctx[i] += c
             total += c
+        if hs:
+            self._hist_write(s, np.concatenate(hs), np.concatenate(hp), np.concatenate(hv), self.drf_stream)
         return total
 
     # ----------------------------------------------------------------- rounds
@@ -377,7 +476,8 @@ class Engine:
 
     # ------------------------------------------------------------ public API
     def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
-                 mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None) -> list[list[int]]:
+                 mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None,
+                 draft_kv: str = "cached") -> list[list[int]]:
         """prompts (token id lists) → committed continuations, max_new_tokens each."""
         S = len(prompts)
         if policy is None:
@@ -385,7 +485,7 @@ class Engine:
                             bs_draft=(S + 1) // 2, n_cand=4)
         max_len = max(len(p) for p in prompts) + max_new_tokens + policy.n_cand + 2
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, temperature, forced_p,
-                             policy.bs_draft)
+                             policy.bs_draft, draft_kv)
         self.prefill(s, prompts, max_new_tokens, policy.bs_prefill)
         if (s.remaining > 0).any():
             self.first_draft(s)
@@ -394,7 +494,7 @@ class Engine:
         return [o[:max_new_tokens] for o in s.out]
 
     def run_decoding(self, policy, workload, plan=None, seed: int = 0, acceptance="greedy", prompts=None,
-                     max_rounds: int | None = None) -> SimResult:
+                     max_rounds: int | None = None, draft_kv: str = "cached") -> SimResult:
         """Measured counterpart of simulate_decoding (simulator.py:108-116).
 
         Runs workload.total_sequences sequences (two batches of
@@ -407,7 +507,7 @@ class Engine:
         S = workload.total_sequences
         max_len = workload.l_input + workload.max_new_tokens + policy.n_cand + 2
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, 1.0, forced_p,
-                             policy.bs_draft)
+                             policy.bs_draft, draft_kv)
         if prompts is not None:
             self.prefill(s, prompts, workload.max_new_tokens, policy.bs_prefill)
         else:

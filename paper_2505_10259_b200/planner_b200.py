@@ -43,6 +43,8 @@ class B200Rates:
 class OffloadPlan:
     bs_decoding: int
     n_cand: int
+    draft_kv: str          # "cached" | "reprefill"
+    bs_draft: int
     stream_layers: tuple[int, ...]
     pinned_layers: tuple[int, ...]
     n_slots: int
@@ -72,59 +74,79 @@ def resident_bytes(arch: ModelArch, include_ffn: bool) -> int:
     return b
 
 
-def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 64) -> int:
+def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 64,
+             draft_seqs: int | None = None) -> int:
+    """Target KV for every sequence; draft KV for ``draft_seqs`` (all of them when
+    cached, one bs_draft chunk when the draft re-prefills: costmodel.py:132-137)."""
+    ds = n_seq if draft_seqs is None else draft_seqs
     return (PagedKVCache.bytes_needed(target, n_seq, max_len, page_size)
-            + PagedKVCache.bytes_needed(draft, n_seq, max_len, page_size))
+            + PagedKVCache.bytes_needed(draft, ds, max_len, page_size))
 
 
-def workspace_bytes(target: ModelArch, draft: ModelArch, bs: int, n_cand: int) -> int:
+def _act_bytes(a: ModelArch, T: int, moe: bool) -> int:
+    rows = 2 * T if moe else T
+    return (T * (6 * a.hidden + a.qkv_rows + 2 * a.n_head * a.head_dim) + rows * (2 * a.hidden + a.inter)) * 2
+
+
+def workspace_bytes(target: ModelArch, draft: ModelArch, bs: int, n_cand: int, draft_tokens: int | None = None) -> int:
+    """Scratch of one verify pass + one draft call (draft_tokens = prefill chunk size)."""
     T = bs * (n_cand + 1)
-    H, I = target.hidden, target.inter
-    tgt = T * (6 * H + target.qkv_rows + 2 * target.n_head * target.head_dim) * 2 + 2 * T * (2 * H + I) * 2 \
-        + T * target.vocab * 4
-    drf = bs * (6 * draft.hidden + draft.qkv_rows + draft.inter) * 2 + bs * draft.vocab * 4
-    return tgt + drf + (1 << 30)  # + allocator / cuBLAS-free slack
+    tgt = _act_bytes(target, T, True) + T * target.vocab * 4
+    dt = bs if draft_tokens is None else draft_tokens
+    drf = _act_bytes(draft, dt, False) + bs * draft.vocab * 4
+    return tgt + drf + (1 << 30)  # + allocator slack
 
 
 def verify_flops(target: ModelArch, bs: int, n_cand: int, ctx: int) -> float:
     return bs * (n_cand + 1) * target.verify_flops_per_token(ctx)
 
 
+def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str) -> float:
+    """One batch's draft work per round: n+1 cached steps, or a context re-prefill + n−1 steps."""
+    if draft_kv == "cached":
+        return bs * (n_cand + 1) * draft.verify_flops_per_token(ctx)
+    return bs * (ctx * draft.verify_flops_per_token(ctx // 2) + (n_cand - 1) * draft.verify_flops_per_token(ctx))
+
+
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
-                 n_slots: int = 2, bs_candidates=None, page_size: int = 64) -> OffloadPlan:
-    """Choose bs_decoding and the pinned / streamed split that maximise
-    predicted decode tokens/s under both memory budgets."""
+                 n_slots: int = 2, bs_candidates=None, page_size: int = 64, draft_kv_modes=("cached", "reprefill"),
+                 max_draft_chunk: int = 64) -> OffloadPlan:
+    """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
+    maximise predicted decode tokens/s under both memory budgets."""
     layer_bytes = ffn_offsets(target)[2]
     fixed = resident_bytes(target, False) + resident_bytes(draft, True) + n_slots * layer_bytes
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     best = None
     cands = bs_candidates or [b for b in range(8, 2049, 8)]
-    for bs in cands:
-        kv = kv_bytes(target, draft, 2 * bs, max_len, page_size)
-        ws = workspace_bytes(target, draft, bs, n_cand)
-        free = hbm_budget - fixed - kv - ws
-        if free < 0:
-            continue
-        pinned = min(target.n_layer, int(free // layer_bytes))
-        streamed = target.n_layer - pinned
-        if streamed * layer_bytes > host_budget:
-            continue
-        S = streamed * layer_bytes
-        t_stream = S / rates.h2d_bytes_per_s
-        t_comp = verify_flops(target, bs, n_cand, ctx_len) / (rates.tensor_flops * rates.tensor_efficiency)
-        t_round = max(t_stream, t_comp) + rates.round_overhead_s
-        tps = bs * e_tok / t_round
-        if best is None or tps > best[0]:
-            best = (tps, bs, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round)
+    for mode in draft_kv_modes:
+        for bs in cands:
+            bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
+            kv = kv_bytes(target, draft, 2 * bs, max_len, page_size, None if mode == "cached" else bs_draft)
+            ws = workspace_bytes(target, draft, bs, n_cand, None if mode == "cached" else bs_draft * max_len)
+            free = hbm_budget - fixed - kv - ws
+            if free < 0:
+                continue
+            pinned = min(target.n_layer, int(free // layer_bytes))
+            streamed = target.n_layer - pinned
+            if streamed * layer_bytes > host_budget:
+                continue
+            S = streamed * layer_bytes
+            t_stream = S / rates.h2d_bytes_per_s
+            eff = rates.tensor_flops * rates.tensor_efficiency
+            t_comp = (verify_flops(target, bs, n_cand, ctx_len) + draft_flops(draft, bs, n_cand, ctx_len, mode)) / eff
+            t_round = max(t_stream, t_comp) + rates.round_overhead_s
+            tps = bs * e_tok / t_round
+            if best is None or tps > best[0] * 1.001:
+                best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
-    tps, bs, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round = best
+    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round = best
     # pin the first layers (ascending order, placement.py:220-231); stream the rest
     pinned_l = tuple(range(pinned))
     stream_l = tuple(range(pinned, target.n_layer))
-    return OffloadPlan(bs, n_cand, stream_l, pinned_l, n_slots if streamed else 0,
+    return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if streamed else 0,
                        {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_ffn": pinned * layer_bytes},
                        streamed * layer_bytes, S, t_stream, t_comp, t_round, bs * e_tok, tps)
 

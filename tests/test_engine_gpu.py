@@ -61,6 +61,20 @@ def test_generate_greedy_matches_oracle(pair, stream_layers, S, bs, n_cand, max_
     assert len(counts) >= 3, counts  # several accept lengths exercised
 
 
+@pytest.mark.parametrize("bs_draft", [4, 3])
+def test_reprefill_draft_matches_oracle(pair, bs_draft):
+    """The paper's re-prefilling draft (scratch KV for one bs_draft chunk) commits
+    the same greedy tokens: drafts only change the round structure."""
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=13)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2})
+    got = eng.generate(prompts, 14, Policy(8, 4, bs_draft, 4), draft_kv="reprefill")
+    margins = []
+    want, _ = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts, 14, 4, 4, margins=margins)
+    assert_greedy_parity(got, want, margins)
+    assert eng.last_session.dkv.n_seq == bs_draft
+
+
 def test_draft_chunking_matches(pair):
     tw, dw = pair
     prompts = tiny.prompts(8, seed=3)
