@@ -48,6 +48,9 @@ extern "C" {
 int so_abi_version(void);
 const char* so_status_string(int status);
 int so_device_sm_count(void);
+/* Make `device` current for the calling host thread (each enqueuing thread —
+ * the verify and the draft streams are fed from two — calls this once). */
+int so_set_device(int device);
 
 /* ---- K7: speculative accept / reject ------------------------------------
  * Replaces the statistical draw `sample_accepted` (acceptance.py:55-72,

@@ -29,6 +29,8 @@ extern "C" int so_stream_layer(void* slot, const void* pinned_src, size_t bytes,
 
 extern "C" int so_abi_version(void) { return 1; }
 
+extern "C" int so_set_device(int device) { return (int)cudaSetDevice(device); }
+
 extern "C" const char* so_status_string(int status) {
   switch (status) {
     case SO_OK: return "ok";

@@ -23,6 +23,7 @@ decrements both batches per round.
 from __future__ import annotations
 
 import dataclasses
+import threading
 import time
 
 import numpy as np
@@ -124,6 +125,7 @@ class Engine:
             if self.target.streamer is not None:
                 self.target.streamer.trace = True
         native.lib()  # fail loudly now if the sm_100a library is missing
+        native.set_device(self.device.index or 0)
 
     def _layer_hook(self, li: int, phase: str, stream) -> None:
         ev = self.tracer.mark(stream)
@@ -451,11 +453,29 @@ class Engine:
         b, o = s.batches[bi], s.batches[1 - bi]
         verify = b.n > 0 and (s.remaining[b.lo:b.hi] > 0).any()
         draft = o.n > 0 and (s.remaining[o.lo:o.hi] > 0).any()
+        # Two host enqueuers: the verify's launches drain only as fast as its
+        # layers arrive over PCIe, so a single thread would block on a full
+        # launch queue and enqueue the draft late (serialising the streams).
+        worker = None
+        err: list = []
+        if draft:
+            def run_draft():
+                try:
+                    torch.cuda.set_device(self.device)
+                    native.set_device(self.device.index or 0)
+                    self._draft(s, 1 - bi, rnd)
+                except BaseException as exc:  # re-raised on the caller's thread
+                    err.append(exc)
+
+            worker = threading.Thread(target=run_draft, name="draft-enqueue")
+            worker.start()
         if verify:
             self._cur = (rnd, bi)
             self._verify(s, bi, rnd)
-        if draft:
-            self._draft(s, 1 - bi, rnd)
+        if worker is not None:
+            worker.join()
+            if err:
+                raise err[0]
         # barrier (simulator.py:209-211): device-side join, then the host reads counts
         done = torch.cuda.Event()
         done.record(self.drf_stream)

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from ctypes import c_float, c_int, c_int64, c_size_t, c_void_p
 
 import torch
@@ -31,6 +32,7 @@ _SIGNATURES = {
     "so_abi_version": (c_int, []),
     "so_status_string": (ctypes.c_char_p, [c_int]),
     "so_device_sm_count": (c_int, []),
+    "so_set_device": (c_int, [c_int]),
     "so_accept_greedy": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_accept_sample": (c_int, [_P, _P, _P, _P, _P, _P, c_float, c_int, c_int, c_int, _P, _P, _P]),
     "so_sample_tokens": (c_int, [_P, c_int64, _P, c_float, c_int, c_int, _P, c_int64, _P, c_int64, _P]),
@@ -77,18 +79,26 @@ def exported_symbols() -> list[str]:
 # ``launches`` so bench.py can report how many of our kernels ran
 _KERNELS_PER_CALL = {"so_router_top2": 3, "so_stream_layer": 0}
 launches = {"kernels": 0, "copies": 0}
+_count_lock = threading.Lock()  # the verify and draft streams are enqueued from two threads
 
 
 def reset_launch_counter() -> None:
-    launches["kernels"] = 0
-    launches["copies"] = 0
+    with _count_lock:
+        launches["kernels"] = 0
+        launches["copies"] = 0
+
+
+def set_device(index: int) -> None:
+    """Make ``index`` current for this thread in the library's runtime as well."""
+    _check(lib().so_set_device(index), "so_set_device")
 
 
 def _check(rc: int, what: str) -> None:
-    if what == "so_stream_layer":
-        launches["copies"] += 1
-    else:
-        launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
+    with _count_lock:
+        if what == "so_stream_layer":
+            launches["copies"] += 1
+        elif what != "so_set_device":
+            launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
     if rc != 0:
         msg = lib().so_status_string(rc).decode()
         raise NativeError(f"{what} failed with status {rc}: {msg}", rc)
