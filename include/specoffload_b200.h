@@ -52,6 +52,27 @@ int so_device_sm_count(void);
  * the verify and the draft streams are fed from two — calls this once). */
 int so_set_device(int device);
 
+/* Stream plumbing for the per-layer loops (events, async copies).  They wrap
+ * the CUDA runtime so a host binding never blocks on a full launch queue
+ * while holding its own interpreter lock. */
+int so_event_create(int timing, void** out_event);
+int so_event_destroy(void* event);
+int so_event_record(void* event, void* stream);
+int so_stream_wait_event(void* stream, void* event);
+int so_event_synchronize(void* event);
+int so_event_elapsed_ms(void* start, void* end, float* ms);
+int so_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+int so_stream_synchronize(void* stream);
+
+/* Verify-batch assembly: tokens[s] = [t_last[s], drafts[0..n-1][s]] and
+ * draft_rows[s] = drafts[..][s] from the step-major draft buffer [n, ld]. */
+int so_build_verify_tokens(const int32_t* t_last, const int32_t* drafts, int ld, int bs, int n_cand,
+                           int32_t* tokens, int32_t* draft_rows, void* stream);
+/* out[i] = src[idx[i]] (int32 gather, e.g. the token history of a re-prefill). */
+int so_gather_i32(const int32_t* src, const int64_t* idx, int n, int32_t* out, void* stream);
+/* dst[idx[i]] = val[i] (int32 scatter into the token history). */
+int so_scatter_i32(int32_t* dst, const int64_t* idx, const int32_t* val, int n, void* stream);
+
 /* ---- K7: speculative accept / reject ------------------------------------
  * Replaces the statistical draw `sample_accepted` (acceptance.py:55-72,
  * called at simulator.py:213) and the clamp `remaining - accepted`

@@ -111,6 +111,31 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const 
   }
 }
 
+__global__ void build_verify_tokens_kernel(const int32_t* __restrict__ t_last, const int32_t* __restrict__ drafts,
+                                           int ld, int bs, int n, int32_t* __restrict__ tokens,
+                                           int32_t* __restrict__ rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= bs * (n + 1)) return;
+  const int s = i / (n + 1), j = i % (n + 1);
+  if (j == 0) {
+    tokens[i] = t_last[s];
+  } else {
+    const int d = drafts[(size_t)(j - 1) * ld + s];
+    tokens[i] = d;
+    rows[(size_t)s * n + j - 1] = d;
+  }
+}
+
+__global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ idx, int n,
+                                  int32_t* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+
+__global__ void scatter_i32_kernel(int32_t* __restrict__ dst, const int64_t* __restrict__ idx,
+                                   const int32_t* __restrict__ val, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[idx[i]] = val[i];
+}
+
 int grid_for(size_t work, int threads) {
   size_t g = (work + threads - 1) / threads;
   if (g > 148 * 16) g = 148 * 16;
@@ -127,6 +152,34 @@ extern "C" int so_embed(const int32_t* tokens, const void* table, int T, int H, 
   if (T == 0) return SO_OK;
   embed_kernel<<<grid_for((size_t)T * (H / 8), 256), 256, 0, as_stream(stream)>>>(
       tokens, reinterpret_cast<const __nv_bfloat16*>(table), T, H, reinterpret_cast<__nv_bfloat16*>(out));
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
+extern "C" int so_build_verify_tokens(const int32_t* t_last, const int32_t* drafts, int ld, int bs, int n_cand,
+                                      int32_t* tokens, int32_t* draft_rows, void* stream) {
+  SO_REQUIRE(t_last && drafts && tokens && draft_rows, SO_E_NULLPTR);
+  SO_REQUIRE(bs >= 0 && n_cand >= 1 && ld >= bs, SO_E_SHAPE);
+  if (bs == 0) return SO_OK;
+  const int total = bs * (n_cand + 1);
+  build_verify_tokens_kernel<<<(total + 255) / 256, 256, 0, as_stream(stream)>>>(t_last, drafts, ld, bs, n_cand,
+                                                                                  tokens, draft_rows);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
+extern "C" int so_gather_i32(const int32_t* src, const int64_t* idx, int n, int32_t* out, void* stream) {
+  SO_REQUIRE(src && idx && out, SO_E_NULLPTR);
+  if (n <= 0) return SO_OK;
+  gather_i32_kernel<<<grid_for((size_t)n, 256), 256, 0, as_stream(stream)>>>(src, idx, n, out);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
+extern "C" int so_scatter_i32(int32_t* dst, const int64_t* idx, const int32_t* val, int n, void* stream) {
+  SO_REQUIRE(dst && idx && val, SO_E_NULLPTR);
+  if (n <= 0) return SO_OK;
+  scatter_i32_kernel<<<grid_for((size_t)n, 256), 256, 0, as_stream(stream)>>>(dst, idx, val, n);
   SO_CHECK_LAUNCH();
   return SO_OK;
 }

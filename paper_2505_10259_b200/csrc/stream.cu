@@ -31,6 +31,51 @@ extern "C" int so_abi_version(void) { return 1; }
 
 extern "C" int so_set_device(int device) { return (int)cudaSetDevice(device); }
 
+// ---- stream plumbing used inside the per-layer loops ---------------------
+// These exist so the host layer never makes a potentially blocking stream
+// call while holding the Python GIL: a full launch queue blocks the caller,
+// and the verify and draft streams are fed from two host threads.
+
+extern "C" int so_event_create(int timing, void** out_event) {
+  SO_REQUIRE(out_event, SO_E_NULLPTR);
+  cudaEvent_t e;
+  cudaError_t r = cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+  *out_event = r == cudaSuccess ? reinterpret_cast<void*>(e) : nullptr;
+  return (int)r;
+}
+
+extern "C" int so_event_destroy(void* event) {
+  return event ? (int)cudaEventDestroy(reinterpret_cast<cudaEvent_t>(event)) : SO_OK;
+}
+
+extern "C" int so_event_record(void* event, void* stream) {
+  SO_REQUIRE(event, SO_E_NULLPTR);
+  return (int)cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), as_stream(stream));
+}
+
+extern "C" int so_stream_wait_event(void* stream, void* event) {
+  SO_REQUIRE(event, SO_E_NULLPTR);
+  return (int)cudaStreamWaitEvent(as_stream(stream), reinterpret_cast<cudaEvent_t>(event), 0);
+}
+
+extern "C" int so_event_synchronize(void* event) {
+  SO_REQUIRE(event, SO_E_NULLPTR);
+  return (int)cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(event));
+}
+
+extern "C" int so_event_elapsed_ms(void* start, void* end, float* ms) {
+  SO_REQUIRE(start && end && ms, SO_E_NULLPTR);
+  return (int)cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(end));
+}
+
+extern "C" int so_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  SO_REQUIRE(dst && src, SO_E_NULLPTR);
+  if (bytes == 0) return SO_OK;
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream));
+}
+
+extern "C" int so_stream_synchronize(void* stream) { return (int)cudaStreamSynchronize(as_stream(stream)); }
+
 extern "C" const char* so_status_string(int status) {
   switch (status) {
     case SO_OK: return "ok";

@@ -120,6 +120,9 @@ class Engine:
         self.tracer = Tracer(trace)
         self._cur = (None, None)  # (round, batch) being verified, for trace tags
         self._marks: dict = {}
+        self._keep: list = []     # pinned staging buffers of in-flight H2D copies
+        self._keep_lock = threading.Lock()
+        self._join = native.Event()
         if trace:
             self.target.hooks = self._layer_hook
             if self.target.streamer is not None:
@@ -149,9 +152,21 @@ class Engine:
 
     # ------------------------------------------------------------------ utils
     def _up(self, arr: np.ndarray, stream, dtype=torch.int32) -> torch.Tensor:
+        """Host array → device tensor, copied asynchronously on ``stream``.
+
+        The copy goes through the C ABI (GIL released if the queue is full);
+        the pinned staging tensor is kept alive until the next barrier."""
         host = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).pin_memory()
         with torch.cuda.stream(stream):
-            return host.to(self.device, non_blocking=True)
+            dev = torch.empty(host.shape, dtype=dtype, device=self.device)
+        native.memcpy_async(dev.data_ptr(), host.data_ptr(), host.numel() * host.element_size(), stream)
+        with self._keep_lock:
+            self._keep.append(host)
+        return dev
+
+    def _release_staging(self) -> None:
+        with self._keep_lock:
+            self._keep.clear()
 
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
@@ -166,8 +181,7 @@ class Engine:
         flat = (np.asarray(seqs, np.int64) * s.max_len + np.asarray(positions, np.int64))
         idx = self._up(flat, stream, torch.int64)
         val = self._up(np.asarray(tokens, np.int32), stream)
-        with torch.cuda.stream(stream):
-            s.hist.view(-1).index_copy_(0, idx, val)
+        native.scatter_i32(s.hist, idx, val, stream)
 
     # ---------------------------------------------------------------- prefill
     def prefill(self, s: DecodeSession, prompts: list, max_new: int, bs_prefill: int | None = None,
@@ -212,7 +226,7 @@ class Engine:
                 last.extend(row0 + qs[1:] - 1)
                 chunks.append(fb)
                 row0 += T
-            lr = self._up(np.asarray(last, np.int64), stream, torch.int64)
+            lr = self._up(np.asarray(last, np.int32), stream)
             chunks[0].last_rows = lr
             if model is self.target:
                 logits = model.forward(chunks, kv, stream)
@@ -239,6 +253,7 @@ class Engine:
         s.remaining[:] = max_new - 1
         self._hist_write(s, np.arange(s.n_seq), lens, first_np, self.drf_stream)
         self.drf_stream.synchronize()
+        self._release_staging()
 
     def synthetic_context(self, s: DecodeSession, ctx_len: int, max_new: int, seed: int = 0) -> None:
         """Decode-only benchmark input: caches hold ``ctx_len`` random KV rows per
@@ -257,6 +272,7 @@ class Engine:
             s.hist.random_(0, self.target.arch.vocab, generator=g)
             self._hist_write(s, np.arange(s.n_seq), s.ctx, s.t_last, self.drf_stream)
         torch.cuda.synchronize(self.device)
+        self._release_staging()
 
     # ------------------------------------------------------------------ draft
     def _draft(self, s: DecodeSession, bi: int, rnd: int) -> None:
@@ -340,9 +356,9 @@ class Engine:
         dslot_d = meta[o:o + D]; o += D
         dqs_d = meta[o:o + cm + 1]; o += cm + 1
         u_d = meta[o:].view(torch.float32) if u_all is not None else None
-        with torch.cuda.stream(st):
-            toks = torch.index_select(s.hist.view(-1), 0, idx)
-            last_rows = last_d.long()
+        toks = self.draft.ws.get("rp_tokens", (T,), torch.int32)
+        native.gather_i32(s.hist, idx, toks, st)
+        last_rows = last_d
         bt = s.dkv.block_table[:cm]
         for j in range(n):
             if j == 0:
@@ -393,12 +409,9 @@ class Engine:
         if forced is not None:
             forced_d = meta[o:o + b.n]; o += b.n
         ev0 = tr.mark(st)
-        with torch.cuda.stream(st):
-            toks = self.target.ws.get("vtok", (b.n, n + 1), torch.int32)
-            toks[:, 0].copy_(t_last_d)
-            toks[:, 1:].copy_(s.drafts[bi][:, :b.n].t())
-            draft_rows = self.target.ws.get("vdraft", (b.n, n), torch.int32)
-            draft_rows.copy_(s.drafts[bi][:, :b.n].t())
+        toks = self.target.ws.get("vtok", (b.n, n + 1), torch.int32)
+        draft_rows = self.target.ws.get("vdraft", (b.n, n), torch.int32)
+        native.build_verify_tokens(t_last_d, s.drafts[bi], b.n, n, toks, draft_rows, st)
         fb = ForwardBatch(toks.view(-1), pos_d, slot_d, qs_d, kvb_d, s.tkv.block_table[b.lo:b.hi], b.n, n + 1)
         logits = self.target.forward(fb, s.tkv, st)
         ev1 = tr.mark(st)
@@ -411,9 +424,9 @@ class Engine:
                                  s.temperature, st)
         else:
             native.accept_greedy(draft_rows, logits, rem_d, out_tok, out_cnt, forced_d, st)
-        with torch.cuda.stream(st):
-            s.res_tok[bi][:b.n].copy_(out_tok, non_blocking=True)
-            s.res_cnt[bi][:b.n].copy_(out_cnt, non_blocking=True)
+        # device → host: the round's result (committed tokens and counts)
+        native.memcpy_async(s.res_tok[bi].data_ptr(), out_tok.data_ptr(), out_tok.numel() * 4, st)
+        native.memcpy_async(s.res_cnt[bi].data_ptr(), out_cnt.data_ptr(), out_cnt.numel() * 4, st)
         ev2 = tr.mark(st)
         tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
         tr.add("GPU_TARGET", "accept", ev1, ev2, batch=bi, rnd=rnd)
@@ -444,7 +457,8 @@ class Engine:
     # ----------------------------------------------------------------- rounds
     def first_draft(self, s: DecodeSession) -> None:
         self._draft(s, 0, -1)
-        self.drf_stream.synchronize()
+        native.stream_synchronize(self.drf_stream)
+        self._release_staging()
 
     def round(self, s: DecodeSession) -> int:
         """One barrier-synchronised round; returns tokens committed."""
@@ -477,12 +491,12 @@ class Engine:
             if err:
                 raise err[0]
         # barrier (simulator.py:209-211): device-side join, then the host reads counts
-        done = torch.cuda.Event()
-        done.record(self.drf_stream)
-        self.tgt_stream.wait_event(done)
+        self._join.record(self.drf_stream)
+        self._join.wait(self.tgt_stream)
         bev = self.tracer.mark(self.tgt_stream)
         self.tracer.add("GPU_TARGET", "barrier", bev, bev, rnd=rnd)
-        self.tgt_stream.synchronize()
+        native.stream_synchronize(self.tgt_stream)
+        self._release_staging()
         c = self._commit(s, bi) if verify else 0
         s.rounds += 1
         s.committed_decode += c

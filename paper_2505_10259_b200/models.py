@@ -72,7 +72,7 @@ class ForwardBatch:
         self.block_table = block_table  # int32 [n_seq, pages] (view of the cache's table)
         self.n_seq = n_seq
         self.max_q = max_q
-        self.last_rows = last_rows    # int64 [k] absolute rows whose logits are wanted (None = all)
+        self.last_rows = last_rows    # int32 [k] absolute rows whose logits are wanted (None = all)
         self.row0 = row0
 
     @property
@@ -152,9 +152,10 @@ class CausalLM:
         rows_idx = [c.last_rows for c in chunks if c.last_rows is not None]
         x = xa
         if rows_idx:
-            sel = torch.cat(rows_idx) if len(rows_idx) > 1 else rows_idx[0]
+            assert len(rows_idx) == 1, "last_rows are given once, on the first chunk"
+            sel = rows_idx[0]
             rows = ws.get("lastx", (sel.numel(), H), torch.bfloat16)
-            torch.index_select(xa, 0, sel, out=rows)
+            native.embed(sel, xa, rows, stream)  # row gather: rows[i] = x[sel[i]]
             x = rows
         R = x.shape[0]
         xf = ws.get("xf", (R, H), torch.bfloat16)

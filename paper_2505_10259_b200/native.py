@@ -47,7 +47,21 @@ _SIGNATURES = {
     "so_attn_paged": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
                               c_float, _P, _P]),
     "so_stream_layer": (c_int, [_P, _P, c_size_t, c_size_t, _P, _P]),
+    "so_event_create": (c_int, [c_int, ctypes.POINTER(c_void_p)]),
+    "so_event_destroy": (c_int, [_P]),
+    "so_event_record": (c_int, [_P, _P]),
+    "so_stream_wait_event": (c_int, [_P, _P]),
+    "so_event_synchronize": (c_int, [_P]),
+    "so_event_elapsed_ms": (c_int, [_P, _P, ctypes.POINTER(c_float)]),
+    "so_memcpy_async": (c_int, [_P, _P, c_size_t, _P]),
+    "so_stream_synchronize": (c_int, [_P]),
+    "so_build_verify_tokens": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P]),
+    "so_gather_i32": (c_int, [_P, _P, c_int, _P, _P]),
+    "so_scatter_i32": (c_int, [_P, _P, _P, c_int, _P]),
 }
+
+_PLUMBING = {"so_event_create", "so_event_destroy", "so_event_record", "so_stream_wait_event", "so_event_synchronize",
+             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device"}
 
 
 def library_path() -> str:
@@ -94,11 +108,12 @@ def set_device(index: int) -> None:
 
 
 def _check(rc: int, what: str) -> None:
-    with _count_lock:
-        if what == "so_stream_layer":
-            launches["copies"] += 1
-        elif what != "so_set_device":
-            launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
+    if what not in _PLUMBING:
+        with _count_lock:
+            if what == "so_stream_layer":
+                launches["copies"] += 1
+            else:
+                launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
     if rc != 0:
         msg = lib().so_status_string(rc).decode()
         raise NativeError(f"{what} failed with status {rc}: {msg}", rc)
@@ -234,9 +249,69 @@ def attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, 
                                _ptr(out), _stream(stream)), "so_attn_paged")
 
 
+# ------------------------------------------------------ stream plumbing ---
+
+def _sp(stream) -> int:
+    """Raw handle of a torch stream (or an int handle)."""
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+class Event:
+    """A CUDA event driven through the C ABI (GIL released on every call)."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self, timing: bool = False):
+        h = c_void_p()
+        _check(lib().so_event_create(1 if timing else 0, ctypes.byref(h)), "so_event_create")
+        self.handle = h.value
+
+    def record(self, stream) -> "Event":
+        _check(lib().so_event_record(self.handle, _sp(stream)), "so_event_record")
+        return self
+
+    def wait(self, stream) -> None:
+        """Make ``stream`` wait for the most recent record of this event."""
+        _check(lib().so_stream_wait_event(_sp(stream), self.handle), "so_stream_wait_event")
+
+    def synchronize(self) -> None:
+        _check(lib().so_event_synchronize(self.handle), "so_event_synchronize")
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = c_float()
+        _check(lib().so_event_elapsed_ms(self.handle, end.handle, ctypes.byref(ms)), "so_event_elapsed_ms")
+        return float(ms.value)
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "handle", None):
+            _lib.so_event_destroy(self.handle)
+            self.handle = None
+
+
+def memcpy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream) -> None:
+    _check(lib().so_memcpy_async(dst_ptr, src_ptr, nbytes, _sp(stream)), "so_memcpy_async")
+
+
+def stream_synchronize(stream) -> None:
+    _check(lib().so_stream_synchronize(_sp(stream)), "so_stream_synchronize")
+
+
+def build_verify_tokens(t_last, drafts, bs: int, n_cand: int, tokens, draft_rows, stream=None):
+    _check(lib().so_build_verify_tokens(_ptr(t_last), _ptr(drafts), drafts.shape[1], bs, n_cand, _ptr(tokens),
+                                        _ptr(draft_rows), _stream(stream)), "so_build_verify_tokens")
+
+
+def gather_i32(src, idx, out, stream=None):
+    _check(lib().so_gather_i32(_ptr(src), _ptr(idx), idx.numel(), _ptr(out), _stream(stream)), "so_gather_i32")
+
+
+def scatter_i32(dst, idx, val, stream=None):
+    _check(lib().so_scatter_i32(_ptr(dst), _ptr(idx), _ptr(val), idx.numel(), _stream(stream)), "so_scatter_i32")
+
+
 # ---------------------------------------------------------------- K1 ---
 
-def stream_layer(slot_ptr: int, host_ptr: int, nbytes: int, chunk: int, stream: torch.cuda.Stream,
-                 event: torch.cuda.Event | None = None) -> None:
-    ev = event.cuda_event if event is not None else None
-    _check(lib().so_stream_layer(slot_ptr, host_ptr, nbytes, chunk, stream.cuda_stream, ev), "so_stream_layer")
+def stream_layer(slot_ptr: int, host_ptr: int, nbytes: int, chunk: int, stream,
+                 event: "Event | None" = None) -> None:
+    ev = event.handle if event is not None else None
+    _check(lib().so_stream_layer(slot_ptr, host_ptr, nbytes, chunk, _sp(stream), ev), "so_stream_layer")

@@ -101,14 +101,10 @@ class LayerStreamer:
         self.device = torch.device(device)
         self.copy_stream = torch.cuda.Stream(device=self.device) if self.streamed else None
         self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
-        self.loaded = [torch.cuda.Event() for _ in range(self.n_slots)]
-        self.free = [torch.cuda.Event() for _ in range(self.n_slots)]
-        # torch creates the CUDA event lazily at the first record(); the native
-        # streamer records `loaded` itself, so materialise every handle now
-        # (an uncreated event has handle 0 and both record and wait no-op)
-        for ev in self.loaded + self.free:
-            ev.record(self.copy_stream)
-        assert all(ev.cuda_event != 0 for ev in self.loaded)
+        # events are created eagerly through the C ABI (a lazily created torch
+        # event has handle 0, and record/wait on it silently no-op)
+        self.loaded = [native.Event() for _ in range(self.n_slots)]
+        self.free = [native.Event() for _ in range(self.n_slots)]
         self.k_use = 0      # global index of the next streamed use
         self.k_issued = 0   # copies enqueued so far
         self.bytes_issued = 0
@@ -123,18 +119,15 @@ class LayerStreamer:
         slot = k % self.n_slots
         layer = self.streamed[k % len(self.streamed)]
         if k >= self.n_slots:
-            self.copy_stream.wait_event(self.free[slot])
+            self.free[slot].wait(self.copy_stream)
         src = self.host[layer]
-        start = end = None
+        start = None
         if self.trace:
-            start = torch.cuda.Event(enable_timing=True)
-            start.record(self.copy_stream)
+            start = native.Event(timing=True).record(self.copy_stream)
         native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
                             self.copy_stream, self.loaded[slot])
         if self.trace:
-            end = torch.cuda.Event(enable_timing=True)
-            end.record(self.copy_stream)
-            self.copy_marks.append((k, layer, start, end))
+            self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.copy_stream)))
         self.bytes_issued += self.layer_bytes
 
     def _ensure_issued(self, upto: int) -> None:
@@ -153,7 +146,7 @@ class LayerStreamer:
         k = self.k_use
         assert self.streamed[k % len(self.streamed)] == layer, "layers must be consumed in pass order"
         self._ensure_issued(k + self.n_slots - 1)
-        stream.wait_event(self.loaded[k % self.n_slots])
+        self.loaded[k % self.n_slots].wait(stream)
         return self.slots[k % self.n_slots].data_ptr()
 
     def release(self, layer: int, stream: torch.cuda.Stream) -> None:

@@ -51,25 +51,30 @@ def busy(trace) -> dict:
 
 
 class Tracer:
-    """Collects (start, end) CUDA-event pairs and resolves them after a sync."""
+    """Collects (start, end) CUDA-event pairs and resolves them after a sync.
+
+    Events are recorded through the C ABI (``native.Event``) so that marking
+    never blocks a host thread while it holds the GIL.
+    """
 
     def __init__(self, enabled: bool = True):
         self.enabled = enabled
-        self.t0: torch.cuda.Event | None = None
+        self.t0 = None
         self._pending: list[tuple] = []
 
-    def origin(self, stream: torch.cuda.Stream) -> None:
+    def origin(self, stream) -> None:
         if not self.enabled:
             return
-        self.t0 = torch.cuda.Event(enable_timing=True)
-        self.t0.record(stream)
+        from . import native
 
-    def mark(self, stream: torch.cuda.Stream) -> torch.cuda.Event | None:
+        self.t0 = native.Event(timing=True).record(stream)
+
+    def mark(self, stream):
         if not self.enabled:
             return None
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
-        return e
+        from . import native
+
+        return native.Event(timing=True).record(stream)
 
     def add(self, resource, label, start_ev, end_ev, batch=None, layer=None, rnd=None) -> None:
         if self.enabled and start_ev is not None and end_ev is not None:
@@ -80,8 +85,8 @@ class Tracer:
             return []
         out = []
         for resource, label, s, e, batch, layer, rnd in self._pending:
-            st = self.t0.elapsed_time(s) * 1e-3
-            en = self.t0.elapsed_time(e) * 1e-3
+            st = self.t0.elapsed_ms(s) * 1e-3
+            en = self.t0.elapsed_ms(e) * 1e-3
             out.append(SimEvent(resource, st, max(st, en), label, batch, layer, rnd))
         self._pending.clear()
         return out

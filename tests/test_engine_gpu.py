@@ -94,7 +94,7 @@ def test_streamer_orders_compute_after_copy(pair):
     ref = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=set()).generate(prompts, 8, Policy(6, 3, 3, 4))
     eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3})
     st = eng.target.streamer
-    assert all(ev.cuda_event != 0 for ev in st.loaded + st.free)
+    assert all(ev.handle for ev in st.loaded + st.free)
     for slot in st.slots:
         slot.zero_()
     torch.cuda.synchronize()
