@@ -63,6 +63,10 @@ int so_event_synchronize(void* event);
 int so_event_elapsed_ms(void* start, void* end, float* ms);
 int so_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 int so_stream_synchronize(void* stream);
+/* Small transfer (KBs) between pinned host memory and HBM done by SMs over
+ * UVA, so per-round metadata never queues behind layer copies on the copy
+ * engine. */
+int so_copy_sm(void* dst, const void* src, size_t bytes, void* stream);
 
 /* Verify-batch assembly: tokens[s] = [t_last[s], drafts[0..n-1][s]] and
  * draft_rows[s] = drafts[..][s] from the step-major draft buffer [n, ld]. */

@@ -76,6 +76,40 @@ extern "C" int so_memcpy_async(void* dst, const void* src, size_t bytes, void* s
 
 extern "C" int so_stream_synchronize(void* stream) { return (int)cudaStreamSynchronize(as_stream(stream)); }
 
+// Small host↔device transfers executed by SMs over UVA (zero-copy) instead of
+// the copy engine.  The H2D copy engine is busy streaming 4.8 GB layers whose
+// copies are gated on the verify's slot releases; a metadata copy queued
+// behind them on the same engine would stall the draft stream for a whole
+// layer.  Pinned host memory is device-addressable under UVA, so a kernel
+// moves the few KB directly.
+namespace {
+__global__ void copy_sm_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t bytes) {
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  size_t done = 0;
+  if (vec) {
+    const size_t n16 = bytes / 16;
+    for (size_t i = tid; i < n16; i += stride)
+      reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+    done = n16 * 16;
+  }
+  for (size_t i = done + tid; i < bytes; i += stride) dst[i] = src[i];
+}
+}  // namespace
+
+extern "C" int so_copy_sm(void* dst, const void* src, size_t bytes, void* stream) {
+  SO_REQUIRE(dst && src, SO_E_NULLPTR);
+  if (bytes == 0) return SO_OK;
+  size_t blocks = (bytes / 16 + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 64) blocks = 64;
+  copy_sm_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(reinterpret_cast<uint8_t*>(dst),
+                                                                   reinterpret_cast<const uint8_t*>(src), bytes);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
 extern "C" const char* so_status_string(int status) {
   switch (status) {
     case SO_OK: return "ok";

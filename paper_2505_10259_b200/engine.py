@@ -159,7 +159,8 @@ class Engine:
         host = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).pin_memory()
         with torch.cuda.stream(stream):
             dev = torch.empty(host.shape, dtype=dtype, device=self.device)
-        native.memcpy_async(dev.data_ptr(), host.data_ptr(), host.numel() * host.element_size(), stream)
+        # SM zero-copy, not the copy engine (which is streaming layers)
+        native.copy_sm(dev.data_ptr(), host.data_ptr(), host.numel() * host.element_size(), stream)
         with self._keep_lock:
             self._keep.append(host)
         return dev
@@ -425,8 +426,8 @@ class Engine:
         else:
             native.accept_greedy(draft_rows, logits, rem_d, out_tok, out_cnt, forced_d, st)
         # device → host: the round's result (committed tokens and counts)
-        native.memcpy_async(s.res_tok[bi].data_ptr(), out_tok.data_ptr(), out_tok.numel() * 4, st)
-        native.memcpy_async(s.res_cnt[bi].data_ptr(), out_cnt.data_ptr(), out_cnt.numel() * 4, st)
+        native.copy_sm(s.res_tok[bi].data_ptr(), out_tok.data_ptr(), out_tok.numel() * 4, st)
+        native.copy_sm(s.res_cnt[bi].data_ptr(), out_cnt.data_ptr(), out_cnt.numel() * 4, st)
         ev2 = tr.mark(st)
         tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
         tr.add("GPU_TARGET", "accept", ev1, ev2, batch=bi, rnd=rnd)

@@ -55,6 +55,7 @@ _SIGNATURES = {
     "so_event_elapsed_ms": (c_int, [_P, _P, ctypes.POINTER(c_float)]),
     "so_memcpy_async": (c_int, [_P, _P, c_size_t, _P]),
     "so_stream_synchronize": (c_int, [_P]),
+    "so_copy_sm": (c_int, [_P, _P, c_size_t, _P]),
     "so_build_verify_tokens": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_gather_i32": (c_int, [_P, _P, c_int, _P, _P]),
     "so_scatter_i32": (c_int, [_P, _P, _P, c_int, _P]),
@@ -290,6 +291,11 @@ class Event:
 
 def memcpy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream) -> None:
     _check(lib().so_memcpy_async(dst_ptr, src_ptr, nbytes, _sp(stream)), "so_memcpy_async")
+
+
+def copy_sm(dst_ptr: int, src_ptr: int, nbytes: int, stream) -> None:
+    """Zero-copy transfer by SMs (pinned host ↔ HBM over UVA); for KB-sized data."""
+    _check(lib().so_copy_sm(dst_ptr, src_ptr, nbytes, _sp(stream)), "so_copy_sm")
 
 
 def stream_synchronize(stream) -> None:
