@@ -57,6 +57,47 @@ class _Batch:
         return np.arange(self.lo, self.hi)
 
 
+class _StagingArena:
+    """Bump allocator over a pinned host buffer and an HBM buffer of the same size.
+
+    Each ``put`` writes a host array into the next free host slice, copies it
+    to the matching device slice with an SM copy on the given stream and
+    returns the device view.  Slices are reused only after ``reset`` (called
+    at the round barrier, when every copy has completed).  Growth allocates a
+    larger pair and retires the old one at the next reset.
+    """
+
+    ALIGN = 256
+
+    def __init__(self, device, capacity: int = 8 << 20):
+        self.device = device
+        self.off = 0
+        self.retired: list = []
+        self._alloc(capacity)
+
+    def _alloc(self, capacity: int) -> None:
+        self.cap = capacity
+        self.host = torch.empty(capacity, dtype=torch.uint8, pin_memory=True)
+        self.dev = torch.empty(capacity, dtype=torch.uint8, device=self.device)
+        self.off = 0
+
+    def put(self, a: np.ndarray, dtype: torch.dtype, stream) -> torch.Tensor:
+        nbytes = a.nbytes
+        if self.off + nbytes > self.cap:
+            self.retired.append((self.host, self.dev))
+            self._alloc(max(2 * self.cap, 2 * nbytes))
+        lo = self.off
+        self.off = (lo + nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        hv = self.host[lo:lo + nbytes].numpy()
+        hv[:] = a.view(np.uint8).reshape(-1)
+        native.copy_sm(self.dev.data_ptr() + lo, self.host.data_ptr() + lo, nbytes, stream)
+        return self.dev[lo:lo + nbytes].view(dtype).view(a.shape)
+
+    def reset(self) -> None:
+        self.off = 0
+        self.retired.clear()
+
+
 class DecodeSession:
     """All per-run state: caches, per-sequence counters, committed tokens."""
 
@@ -120,8 +161,7 @@ class Engine:
         self.tracer = Tracer(trace)
         self._cur = (None, None)  # (round, batch) being verified, for trace tags
         self._marks: dict = {}
-        self._keep: list = []     # pinned staging buffers of in-flight H2D copies
-        self._keep_lock = threading.Lock()
+        self._arenas: dict = {}   # stream handle -> _StagingArena (per-round H2D metadata)
         self._join = native.Event()
         if trace:
             self.target.hooks = self._layer_hook
@@ -154,20 +194,20 @@ class Engine:
     def _up(self, arr: np.ndarray, stream, dtype=torch.int32) -> torch.Tensor:
         """Host array → device tensor, copied asynchronously on ``stream``.
 
-        The copy goes through the C ABI (GIL released if the queue is full);
-        the pinned staging tensor is kept alive until the next barrier."""
-        host = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype).pin_memory()
-        with torch.cuda.stream(stream):
-            dev = torch.empty(host.shape, dtype=dtype, device=self.device)
-        # SM zero-copy, not the copy engine (which is streaming layers)
-        native.copy_sm(dev.data_ptr(), host.data_ptr(), host.numel() * host.element_size(), stream)
-        with self._keep_lock:
-            self._keep.append(host)
-        return dev
+        Per-stream staging arenas (pinned host + HBM, allocated once, reset at
+        every barrier) mean the round loop never calls the device allocator
+        (whose reclaim path would cudaFree = synchronise the whole GPU) and
+        the copy is done by SMs, never queued behind a layer on the copy
+        engine."""
+        a = np.ascontiguousarray(arr).astype(torch.empty((), dtype=dtype).numpy().dtype, copy=False)
+        arena = self._arenas.get(stream.cuda_stream)
+        if arena is None:
+            arena = self._arenas[stream.cuda_stream] = _StagingArena(self.device)
+        return arena.put(a, dtype, stream)
 
     def _release_staging(self) -> None:
-        with self._keep_lock:
-            self._keep.clear()
+        for arena in self._arenas.values():
+            arena.reset()
 
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,

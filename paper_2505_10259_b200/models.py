@@ -47,7 +47,12 @@ class Workspace:
         nbytes = max(n * esize, 16)
         buf = self._bufs.get(name)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            # grow with 50% headroom: the re-prefill chunk grows a little every
+            # round, and each device allocation risks an allocator reclaim
+            # (cudaFree = whole-device synchronisation) inside the round loop
+            grown = nbytes if buf is None else max(nbytes, buf.numel() * 3 // 2)
+            grown = (grown + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+            buf = torch.empty(grown, dtype=torch.uint8, device=self.device)
             self._bufs[name] = buf
         return buf[: n * esize].view(dtype).view(*shape)
 
