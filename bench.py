@@ -189,8 +189,8 @@ def main():
     link = h2d_peak(torch, device)
     free, total = torch.cuda.mem_get_info(device)
     hbm = int(args.hbm_gb * 1e9) if args.hbm_gb else (int(24 * 2**30) if args.config == "8x7b" else free)
+    # one host copy of the streamed layers serves every rank (SharedHostStore)
     host = int(args.host_gb * 1e9) if args.host_gb else max(0, mem_available() - int(14e9))
-    host //= max(1, torch.cuda.device_count() if world > 1 else 1)
     steps, warm = args.steps, args.warmup
     verifies_per_batch = (warm + steps) // 2 + 2
     max_new = verifies_per_batch * (args.n_cand + 1) + 1
@@ -201,9 +201,19 @@ def main():
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes)
     t_setup = time.perf_counter()
-    store = HostStore()
-    eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
-                       seed=1 + rank, trace=bool(args.trace_out), host_store=store)
+    layer_bytes = ffn_offsets(tgt)[2]
+    if world > 1:
+        from paper_2505_10259_b200.streamer import SharedHostStore
+
+        store = SharedHostStore(f"specoffload_{os.environ.get('MASTER_PORT', '0')}", list(plan.stream_layers),
+                                layer_bytes, rank, world, barrier=dist.barrier)
+        eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
+                           seed=1, trace=bool(args.trace_out), rank=rank, world=world, shared_store=store)
+        dist.barrier()  # every slice of the shared store is written
+    else:
+        store = HostStore()
+        eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
+                           seed=1, trace=bool(args.trace_out), host_store=store)
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
@@ -259,7 +269,7 @@ def main():
     achieved_link = streamed / dev_s if dev_s > 0 else 0.0
     e_tok = expected_accepted(AcceptanceModel(args.p, args.n_cand))
     F = verify_flops(tgt, bs, args.n_cand, args.ctx)
-    roof = roofline_tokens_per_s(bs * e_tok * world, len(plan.stream_layers) * layer_bytes, F, link,
+    roof = roofline_tokens_per_s(bs * e_tok * world, len(plan.stream_layers) * layer_bytes // world, F, link,
                                  peaks["bf16_tflops_sustained"] * 1e12)
 
     # ---- tensor-core kernel sample: MoE gate_up grouped GEMM at this round's shape ----
@@ -304,6 +314,9 @@ def main():
         with open(args.trace_out, "w") as f:
             f.write(export_chrome(res))
 
+    if world > 1:
+        dist.barrier()
+        store.close(unlink=rank == 0)
     if rank != 0:
         return
     meta_bytes = bs * (args.n_cand + 1) * 4 * 2 + bs * 4 * 4
@@ -312,7 +325,7 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": dev_s / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, random prompt KV, forced acceptance p)",
-        "config": {"workload": f"configs[2]: {tgt.name} offloaded + {drf.name} draft, 1 B200, full HBM",
+        "config": {"workload": f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM",
                    "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
                    "draft_kv": plan.draft_kv, "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
@@ -337,7 +350,6 @@ def main():
         line["cpu_baseline"] = {"value": cpu.tokens_per_s, "unit": "tokens/s", "cores": cpu.cores, "kind": "port",
                                 "sample": cpu.sample}
     print(json.dumps(line))
-    store.close() if False else None
 
 
 if __name__ == "__main__":

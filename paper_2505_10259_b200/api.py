@@ -13,23 +13,28 @@ from . import weights as W
 from .config import ModelArch
 from .engine import Engine
 from .models import DraftModel, TargetModel
-from .streamer import HostStore, LayerStreamer
+from .streamer import HostStore, LayerStreamer, SharedHostStore
 
 
 def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: dict | None = None,
                  draft_weights: dict | None = None, device="cuda:0", stream_layers=None, n_slots: int = 2,
                  seed: int = 0, trace: bool = True, page_size: int = 64, host_store: HostStore | None = None,
-                 chunk_bytes: int = 256 << 20) -> Engine:
+                 chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
+                 shared_store: SharedHostStore | None = None) -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
-    all of them — the fully offloaded configuration)."""
+    all of them — the fully offloaded configuration).  With ``world > 1`` the
+    streamed layers live once in ``shared_store`` and each rank pulls its
+    1/N slice, reassembled by an NCCL all-gather."""
     dev = torch.device(device)
     if stream_layers is None:
         stream_layers = set(range(target_arch.n_layer))
     stream_layers = set(stream_layers)
     if target_weights is not None:
         tw = W.from_logical(target_arch, target_weights, dev, stream_layers)
+    elif shared_store is not None:
+        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=shared_store.write_slice)
     else:
         store = host_store or HostStore()
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc)
@@ -41,7 +46,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
     host = {li: t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
-                             chunk_bytes=chunk_bytes) if host else None
+                             chunk_bytes=chunk_bytes, rank=rank, world=world, group=group) if host else None
     target = TargetModel(tw, dev, streamer)
     draft = DraftModel(dw, dev)
     return Engine(target, draft, device=dev, page_size=page_size, trace=trace)

@@ -80,6 +80,84 @@ class HostStore:
         self._maps.clear()
 
 
+def slice_bounds(nbytes: int, rank: int, world: int) -> tuple[int, int]:
+    """Byte range of ``rank``'s 1/N share of an ``nbytes`` layer (equal, page-aligned shares)."""
+    if nbytes % world or (nbytes // world) % 4096:
+        raise ValueError(f"layer of {nbytes} B does not split into {world} page-aligned slices")
+    share = nbytes // world
+    return rank * share, (rank + 1) * share
+
+
+class SharedHostStore:
+    """One host copy of the streamed layers for all ranks of a box.
+
+    Rank 0 creates a file in /dev/shm; every rank maps it MAP_SHARED and
+    page-locks only its own 1/N slice of each layer (the bytes it will push
+    over its own PCIe link).  ``write_slice`` fills that slice from a GPU
+    tensor, so the N ranks initialise the store in parallel, each over its own
+    link.  Layer ℓ lives at offset ℓ·layer_bytes.
+    """
+
+    def __init__(self, name: str, layers: list[int], layer_bytes: int, rank: int, world: int, barrier=None):
+        self.layers = {li: i for i, li in enumerate(layers)}
+        self.layer_bytes = layer_bytes
+        self.rank, self.world = rank, world
+        self.path = f"/dev/shm/{name}"
+        self.bytes = len(layers) * layer_bytes
+        if rank == 0:
+            fd = os.open(self.path, os.O_RDWR | os.O_CREAT | os.O_TRUNC, 0o600)
+            os.ftruncate(fd, self.bytes)
+            os.close(fd)
+        if barrier is not None:
+            barrier()
+        fd = os.open(self.path, os.O_RDWR)
+        self._map = mmap.mmap(fd, self.bytes, flags=mmap.MAP_SHARED)
+        os.close(fd)
+        self._buf = (ctypes.c_uint8 * self.bytes).from_buffer(self._map)
+        self.base = ctypes.addressof(self._buf)
+        self._registered: list[int] = []
+        self.lo, self.hi = slice_bounds(layer_bytes, rank, world)
+        if torch.cuda.is_available():
+            for i in range(len(layers)):
+                addr = self.base + i * layer_bytes + self.lo
+                rc = torch.cuda.cudart().cudaHostRegister(addr, self.hi - self.lo, 0)
+                if int(rc) != 0:
+                    raise InsufficientTotalMemory(f"cudaHostRegister of a {self.hi - self.lo} B slice failed ({int(rc)})")
+                self._registered.append(addr)
+
+    def layer_view(self, layer: int) -> torch.Tensor:
+        off = self.layers[layer] * self.layer_bytes
+        return torch.frombuffer(self._buf, dtype=torch.uint8, count=self.layer_bytes, offset=off)
+
+    def write_slice(self, layer: int, src: torch.Tensor) -> torch.Tensor:
+        """Copy this rank's slice of ``src`` (the full layer, any device) into the store."""
+        view = self.layer_view(layer)
+        flat = src.reshape(-1).view(torch.uint8)
+        view[self.lo:self.hi].copy_(flat[self.lo:self.hi])
+        return view
+
+    def close(self, unlink: bool = False) -> None:
+        for addr in self._registered:
+            torch.cuda.cudart().cudaHostUnregister(addr)
+        self._registered.clear()
+        if unlink and os.path.exists(self.path):
+            os.unlink(self.path)
+
+
+def gather_layer(slot: torch.Tensor, rank: int, world: int, group=None) -> None:
+    """In-place all-gather of the 1/N slices of one layer into ``slot`` (every
+    rank ends with the full layer).  NCCL reassembles over NVLink; gloo (CPU
+    tests) takes the list form."""
+    import torch.distributed as dist
+
+    lo, hi = slice_bounds(slot.numel(), rank, world)
+    if slot.is_cuda:
+        dist.all_gather_into_tensor(slot, slot[lo:hi], group=group)
+    else:
+        parts = list(slot.view(world, -1).unbind(0))
+        dist.all_gather(parts, slot[lo:hi].clone(), group=group)
+
+
 class LayerStreamer:
     """Moves host-resident FFN layers through ``n_slots`` HBM slots.
 
@@ -91,7 +169,8 @@ class LayerStreamer:
     """
 
     def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict[int, torch.Tensor],
-                 n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False):
+                 n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False,
+                 rank: int = 0, world: int = 1, group=None):
         self.layer_bytes = layer_bytes
         self.resident = resident
         self.host = host
@@ -100,6 +179,12 @@ class LayerStreamer:
         self.chunk = chunk_bytes
         self.device = torch.device(device)
         self.copy_stream = torch.cuda.Stream(device=self.device) if self.streamed else None
+        # N > 1: each rank pushes its 1/N slice over its own PCIe link, then an
+        # in-place NCCL all-gather on the comm stream rebuilds the layer
+        self.rank, self.world, self.group = rank, world, group
+        self.lo, self.hi = slice_bounds(layer_bytes, rank, world) if world > 1 else (0, layer_bytes)
+        self.comm_stream = torch.cuda.Stream(device=self.device) if (self.streamed and world > 1) else None
+        self.copied = [native.Event() for _ in range(self.n_slots)] if world > 1 else []
         self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
         # events are created eagerly through the C ABI (a lazily created torch
         # event has handle 0, and record/wait on it silently no-op)
@@ -124,11 +209,20 @@ class LayerStreamer:
         start = None
         if self.trace:
             start = native.Event(timing=True).record(self.copy_stream)
-        native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
-                            self.copy_stream, self.loaded[slot])
+        if self.world == 1:
+            native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
+                                self.copy_stream, self.loaded[slot])
+        else:
+            native.stream_layer(self.slots[slot].data_ptr() + self.lo, src.data_ptr() + self.lo, self.hi - self.lo,
+                                self.chunk, self.copy_stream, self.copied[slot])
+            self.copied[slot].wait(self.comm_stream)
+            with torch.cuda.stream(self.comm_stream):
+                gather_layer(self.slots[slot], self.rank, self.world, self.group)
+            self.loaded[slot].record(self.comm_stream)
         if self.trace:
-            self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.copy_stream)))
-        self.bytes_issued += self.layer_bytes
+            end_stream = self.copy_stream if self.world == 1 else self.comm_stream
+            self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream)))
+        self.bytes_issued += self.hi - self.lo
 
     def _ensure_issued(self, upto: int) -> None:
         while self.k_issued <= upto:

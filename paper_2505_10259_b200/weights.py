@@ -107,11 +107,14 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 
 
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
-              host_alloc=None, std: float = 0.02) -> ModelWeights:
+              host_alloc=None, std: float = 0.02, host_sink=None) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
-    time and copied into pinned host buffers from ``host_alloc(nbytes)``.
+    time and copied into pinned host buffers from ``host_alloc(nbytes)`` — or
+    handed to ``host_sink(layer, tensor) -> host view`` (multi-GPU: each rank
+    writes only its slice of the shared store; every rank draws the same
+    weights from the same seed).
     """
     dev = torch.device(device)
     g = torch.Generator(device=dev)
@@ -128,7 +131,11 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
     host = {}
     for li in range(arch.n_layer):
         ffn = randn(ffn_bytes // 2)
-        if li in stream_layers:
+        if li in stream_layers and host_sink is not None:
+            host[li] = host_sink(li, ffn).view(torch.bfloat16)
+            del ffn
+            ffn = None
+        elif li in stream_layers:
             buf = host_alloc(ffn_bytes) if host_alloc is not None else torch.empty(
                 ffn_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
             buf = buf.view(torch.bfloat16)
