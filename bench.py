@@ -189,6 +189,9 @@ def main():
     link = h2d_peak(torch, device)
     free, total = torch.cuda.mem_get_info(device)
     hbm = int(args.hbm_gb * 1e9) if args.hbm_gb else (int(24 * 2**30) if args.config == "8x7b" else free)
+    if hbm < free:
+        # enforce the cap (configs[1]: "HBM capped to 24 GB") on the allocator itself
+        torch.cuda.set_per_process_memory_fraction(min(1.0, hbm / total), device)
     # one host copy of the streamed layers serves every rank (SharedHostStore)
     host = int(args.host_gb * 1e9) if args.host_gb else max(0, mem_available() - int(14e9))
     steps, warm = args.steps, args.warmup
@@ -208,12 +211,13 @@ def main():
         store = SharedHostStore(f"specoffload_{os.environ.get('MASTER_PORT', '0')}", list(plan.stream_layers),
                                 layer_bytes, rank, world, barrier=dist.barrier)
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
-                           seed=1, trace=bool(args.trace_out), rank=rank, world=world, shared_store=store)
+                           seed=1, trace=bool(args.trace_out), rank=rank, world=world, shared_store=store,
+                           stream_attn=plan.stream_attn)
         dist.barrier()  # every slice of the shared store is written
     else:
         store = HostStore()
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
-                           seed=1, trace=bool(args.trace_out), host_store=store)
+                           seed=1, trace=bool(args.trace_out), host_store=store, stream_attn=plan.stream_attn)
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,

@@ -20,7 +20,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  draft_weights: dict | None = None, device="cuda:0", stream_layers=None, n_slots: int = 2,
                  seed: int = 0, trace: bool = True, page_size: int = 64, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
-                 shared_store: SharedHostStore | None = None) -> Engine:
+                 shared_store: SharedHostStore | None = None, stream_attn: bool = False) -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
@@ -32,17 +32,19 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
         stream_layers = set(range(target_arch.n_layer))
     stream_layers = set(stream_layers)
     if target_weights is not None:
-        tw = W.from_logical(target_arch, target_weights, dev, stream_layers)
+        tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn)
     elif shared_store is not None:
-        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=shared_store.write_slice)
+        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=shared_store.write_slice,
+                         stream_attn=stream_attn)
     else:
         store = host_store or HostStore()
-        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc)
+        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc,
+                         stream_attn=stream_attn)
     if draft_weights is not None:
         dw = W.from_logical(draft_arch, draft_weights, dev)
     else:
         dw = W.synthetic(draft_arch, dev, seed=seed + 1)
-    _, _, ffn_bytes = W.ffn_offsets(target_arch)
+    _, ffn_bytes = W.unit_layout(target_arch, stream_attn)  # bytes of one streamed layer unit
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
     host = {li: t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,

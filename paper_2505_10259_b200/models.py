@@ -123,25 +123,33 @@ class CausalLM:
         for c in chunks:
             native.embed(c.tokens, self.w.embed, xa[c.row0:c.row0 + c.T], stream)
         hook = self.hooks
+        q_dim = hq * dh
         for li, L in enumerate(self.w.layers):
             if hook:
                 hook(li, "attn_start", stream)
             kc, vc = kv.layer(li)
             base = None
+            wqkv, wo = L.wqkv, L.wo
+            if wqkv is None:  # attention weights stream with the layer: wait before QKV
+                unit = self._ffn_acquire(li, L, stream)
+                wqkv = _RawView(unit, (a.qkv_rows, H))
+                wo = _RawView(unit + a.qkv_rows * H * 2, (H, q_dim))
+                base = unit + (a.qkv_rows * H + H * q_dim) * 2
             for ci, c in enumerate(chunks):
                 T = c.T
                 x = xa[c.row0:c.row0 + T]
                 out = xb[c.row0:c.row0 + T]
                 native.rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
-                native.gemm(xn[:T], L.wqkv, qkv[:T], native.EPI_BF16, None, stream)
+                native.gemm(xn[:T], wqkv, qkv[:T], native.EPI_BF16, None, stream)
                 native.rope_kv_append(qkv[:T], c.positions, c.slots, hq, hkv, dh, a.rope_theta, kv.page_size,
                                       q[:T], kc, vc, stream)
                 native.attn_paged(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
                                   kv.page_size, scale, att[:T], stream)
-                native.gemm(att[:T], L.wo, h[:T], native.EPI_BF16_RESID, x, stream)
+                native.gemm(att[:T], wo, h[:T], native.EPI_BF16_RESID, x, stream)
                 native.rmsnorm(h[:T], L.ffn_norm, xn[:T], a.eps, stream)
                 if ci == 0:
-                    base = self._ffn_acquire(li, L, stream)
+                    if base is None:
+                        base = self._ffn_acquire(li, L, stream)
                     if hook:
                         hook(li, "ffn_start", stream)
                 if a.is_moe:

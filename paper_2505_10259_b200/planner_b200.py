@@ -23,7 +23,7 @@ from .acceptance import AcceptanceModel, expected_accepted
 from .config import ModelArch
 from .errors import InfeasiblePlan
 from .kvcache import PagedKVCache
-from .weights import ffn_offsets
+from .weights import attn_elems, ffn_offsets, unit_layout
 
 GB = 1e9
 
@@ -56,6 +56,7 @@ class OffloadPlan:
     t_round_s: float
     expected_tokens_per_round: float
     tokens_per_s: float
+    stream_attn: bool = False  # attention projections streamed with each layer (H3)
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -111,16 +112,20 @@ def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str)
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
                  n_slots: int = 2, bs_candidates=None, page_size: int = 64, draft_kv_modes=("cached", "reprefill"),
-                 max_draft_chunk: int = 64) -> OffloadPlan:
+                 max_draft_chunk: int = 64, stream_attn_modes=(False, True)) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets."""
-    layer_bytes = ffn_offsets(target)[2]
-    fixed = resident_bytes(target, False) + resident_bytes(draft, True) + n_slots * layer_bytes
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     best = None
     cands = bs_candidates or [b for b in range(8, 2049, 8)]
-    for mode in draft_kv_modes:
+    attn_layer = attn_elems(target) * 2
+    for stream_attn, mode in [(sa, m) for sa in stream_attn_modes for m in draft_kv_modes]:
+        # unit = bytes of one streamed (or pinned) layer; with stream_attn the
+        # attention projections travel with the FFN and leave the resident set
+        layer_bytes = unit_layout(target, stream_attn)[1]
+        fixed = (resident_bytes(target, False) - (target.n_layer * attn_layer if stream_attn else 0)
+                 + resident_bytes(draft, True) + n_slots * layer_bytes)
         for bs in cands:
             bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
             kv = kv_bytes(target, draft, 2 * bs, max_len, page_size, None if mode == "cached" else bs_draft)
@@ -139,16 +144,17 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
             t_round = max(t_stream, t_comp) + rates.round_overhead_s
             tps = bs * e_tok / t_round
             if best is None or tps > best[0] * 1.001:
-                best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round)
+                best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
+                        stream_attn, fixed, layer_bytes)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
-    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round = best
+    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes = best
     # pin the first layers (ascending order, placement.py:220-231); stream the rest
     pinned_l = tuple(range(pinned))
     stream_l = tuple(range(pinned, target.n_layer))
     return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if streamed else 0,
-                       {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_ffn": pinned * layer_bytes},
-                       streamed * layer_bytes, S, t_stream, t_comp, t_round, bs * e_tok, tps)
+                       {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes},
+                       streamed * layer_bytes, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

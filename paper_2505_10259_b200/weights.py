@@ -53,11 +53,29 @@ def ffn_offsets(arch: ModelArch) -> tuple[int, int, int]:
     return gu, dn, (gu + dn) * 2
 
 
+def attn_elems(arch: ModelArch) -> int:
+    """bf16 elements of one layer's attention projections (Wqkv + Wo)."""
+    return arch.qkv_rows * arch.hidden + arch.hidden * arch.n_head * arch.head_dim
+
+
+def unit_layout(arch: ModelArch, stream_attn: bool) -> tuple[int, int]:
+    """(byte offset of the FFN inside a streamed layer unit, unit bytes).
+
+    The streamed unit is the FFN alone, or [Wqkv | Wo | FFN] when the HBM
+    budget cannot hold the attention weights either (the
+    8x7B config capped at 24 GB)."""
+    ffn_bytes = ffn_offsets(arch)[2]
+    if not stream_attn:
+        return 0, ffn_bytes
+    a = attn_elems(arch) * 2
+    return a, a + ffn_bytes
+
+
 @dataclasses.dataclass
 class LayerWeights:
     attn_norm: torch.Tensor
-    wqkv: torch.Tensor
-    wo: torch.Tensor
+    wqkv: torch.Tensor | None  # None when the attention weights stream with the layer
+    wo: torch.Tensor | None
     ffn_norm: torch.Tensor
     router: torch.Tensor | None
     ffn: torch.Tensor | None  # packed FFN when HBM-resident (None when host-streamed)
@@ -81,23 +99,28 @@ class ModelWeights:
         return 2 * n
 
 
-def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset()) -> ModelWeights:
+def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset(),
+                 stream_attn: bool = False) -> ModelWeights:
     """Build device weights from logical (HF-shaped) arrays — numpy or torch."""
     dev = torch.device(device)
     layers = []
     host = {}
     for li, L in enumerate(W["layers"]):
-        wqkv = torch.cat([_bf16(L["wq"]), _bf16(L["wk"]), _bf16(L["wv"])], dim=0).to(dev).contiguous()
+        wqkv = torch.cat([_bf16(L["wq"]), _bf16(L["wk"]), _bf16(L["wv"])], dim=0).contiguous()
+        wo = _bf16(L["wo"]).contiguous()
         packed = pack_ffn(L["w_gate"], L["w_up"], L["w_down"])
         if li in stream_layers:
+            if stream_attn:
+                packed = torch.cat([wqkv.reshape(-1), wo.reshape(-1), packed])
+                wqkv = wo = None
             host[li] = packed.pin_memory() if dev.type == "cuda" else packed
             ffn = None
         else:
             ffn = packed.to(dev)
         layers.append(LayerWeights(
             attn_norm=_bf16(L["attn_norm"]).to(dev),
-            wqkv=wqkv,
-            wo=_bf16(L["wo"]).to(dev).contiguous(),
+            wqkv=wqkv.to(dev) if wqkv is not None else None,
+            wo=wo.to(dev) if wo is not None else None,
             ffn_norm=_bf16(L["ffn_norm"]).to(dev),
             router=_bf16(L["router"]).to(dev).contiguous() if arch.is_moe else None,
             ffn=ffn,
@@ -107,7 +130,7 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 
 
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
-              host_alloc=None, std: float = 0.02, host_sink=None) -> ModelWeights:
+              host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
@@ -130,23 +153,23 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
     layers = []
     host = {}
     for li in range(arch.n_layer):
-        ffn = randn(ffn_bytes // 2)
-        if li in stream_layers and host_sink is not None:
-            host[li] = host_sink(li, ffn).view(torch.bfloat16)
-            del ffn
-            ffn = None
-        elif li in stream_layers:
-            buf = host_alloc(ffn_bytes) if host_alloc is not None else torch.empty(
-                ffn_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
+        streamed = li in stream_layers
+        with_attn = streamed and stream_attn
+        unit = randn((ffn_bytes + (attn_elems(arch) * 2 if with_attn else 0)) // 2)
+        if streamed and host_sink is not None:
+            host[li] = host_sink(li, unit).view(torch.bfloat16)
+        elif streamed:
+            buf = host_alloc(unit.numel() * 2) if host_alloc is not None else torch.empty(
+                unit.numel(), dtype=torch.bfloat16, pin_memory=True)
             buf = buf.view(torch.bfloat16)
-            buf.copy_(ffn)
+            buf.copy_(unit)
             host[li] = buf
-            del ffn
-            ffn = None
+        ffn = None if streamed else unit
+        del unit
         layers.append(LayerWeights(
             attn_norm=ones(arch.hidden),
-            wqkv=randn(arch.qkv_rows, arch.hidden),
-            wo=randn(arch.hidden, arch.n_head * arch.head_dim),
+            wqkv=None if with_attn else randn(arch.qkv_rows, arch.hidden),
+            wo=None if with_attn else randn(arch.hidden, arch.n_head * arch.head_dim),
             ffn_norm=ones(arch.hidden),
             router=randn(arch.n_expert, arch.hidden) if arch.is_moe else None,
             ffn=ffn,

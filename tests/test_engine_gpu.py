@@ -75,6 +75,17 @@ def test_reprefill_draft_matches_oracle(pair, bs_draft):
     assert eng.last_session.dkv.n_seq == bs_draft
 
 
+def test_streamed_attention_weights_match(pair):
+    """H3 mode: [Wqkv | Wo | FFN] units streamed per layer give the resident result."""
+    tw, dw = pair
+    prompts = tiny.prompts(6, seed=17)
+    pol = Policy(6, 3, 3, 4)
+    ref = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=set()).generate(prompts, 10, pol)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 2, 3}, stream_attn=True)
+    assert eng.target.w.layers[0].wqkv is None and eng.target.w.layers[1].wqkv is not None
+    assert eng.generate(prompts, 10, pol) == ref
+
+
 def test_draft_chunking_matches(pair):
     tw, dw = pair
     prompts = tiny.prompts(8, seed=3)
