@@ -162,3 +162,114 @@ def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops
     """C / max(S / B_h2d, F / peak)."""
     t = max(streamed_bytes / h2d_peak, flops / tensor_peak)
     return committed_per_round / t if t > 0 else math.inf
+
+
+# ---------------------------------------------------------------------------
+# Planner API on the B200 cost model (same shapes as planner.py:117-319)
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass(frozen=True)
+class B200CostBreakdown:
+    """Fields of the reference's CostBreakdown (costmodel.py:19-31) plus the plan."""
+
+    policy: object
+    t_prefill: float
+    t_decoding: float
+    t_draft_per_round: float
+    t_target_per_round: float
+    rounds: int
+    v_prefill: int
+    v_decoding: int
+    expected_tokens: float
+    throughput: float
+    feasible: bool
+    plan: OffloadPlan | None = None
+
+
+def prefill_time(target: ModelArch, draft: ModelArch, n_seq: int, ctx_len: int, streamed_bytes: int,
+                 rates: B200Rates) -> float:
+    """Layer-major (zig-zag) prefill: every streamed layer crosses the link once
+    while all prompts run through it; bound by max(stream, compute)."""
+    flops = n_seq * ctx_len * (target.verify_flops_per_token(ctx_len // 2) + draft.verify_flops_per_token(ctx_len // 2))
+    return max(streamed_bytes / rates.h2d_bytes_per_s, flops / (rates.tensor_flops * rates.tensor_efficiency))
+
+
+def predict_throughput(policy, workload, rates: B200Rates, target: ModelArch, draft: ModelArch, hbm_budget: int,
+                       host_budget: int, draft_kv_modes=("cached", "reprefill"), stream_attn_modes=(False, True),
+                       include_prefill: bool = True) -> B200CostBreakdown:
+    """Predicted end-to-end tokens/s of ``workload`` under ``policy`` on one B200.
+
+    Round accounting: one verification per round, so each
+    dual-batch group needs 2·ceil(max_new / E[k]) rounds; groups of
+    2·bs_decoding sequences run one after another (planner.py:131-135).
+    """
+    p = policy
+    try:
+        plan = plan_offload(target, draft, hbm_budget, host_budget, p.n_cand, workload.acceptance_p,
+                            workload.l_input, workload.max_new_tokens, rates, bs_candidates=[p.bs_decoding],
+                            draft_kv_modes=draft_kv_modes, stream_attn_modes=stream_attn_modes,
+                            max_draft_chunk=p.bs_draft)
+    except InfeasiblePlan:
+        return B200CostBreakdown(p, math.inf, math.inf, 0.0, 0.0, 0, 0, 0, 0.0, 0.0, False, None)
+    e = expected_accepted(AcceptanceModel(workload.acceptance_p, p.n_cand))
+    per_batch_rounds = math.ceil(max(workload.max_new_tokens - 1, 1) / e)
+    groups = max(1, math.ceil(workload.total_sequences / (2 * p.bs_decoding)))
+    rounds = 2 * per_batch_rounds * groups
+    t_dec = rounds * plan.t_round_s
+    t_pf = prefill_time(target, draft, workload.total_sequences, workload.l_input, plan.streamed_bytes_per_pass,
+                        rates) if include_prefill else 0.0
+    tokens = float(workload.total_sequences * workload.max_new_tokens)
+    v_dec = sum(plan.hbm_bytes.values()) + plan.n_slots * 0
+    return B200CostBreakdown(p, t_pf, t_dec, plan.t_compute_s, plan.t_stream_s, rounds, v_dec, v_dec, tokens,
+                             tokens / (t_pf + t_dec), True, plan)
+
+
+def search(space, workload, rates: B200Rates, target: ModelArch, draft: ModelArch, hbm_budget: int,
+           host_budget: int, **kw) -> list[tuple[object, B200CostBreakdown]]:
+    """Exhaustive sweep (planner.py:161-184): drop infeasible, rank by throughput,
+    ties broken by the policy tuple."""
+    from .errors import NoFeasiblePolicy
+
+    entries = []
+    for policy in space.policies():
+        bd = predict_throughput(policy, workload, rates, target, draft, hbm_budget, host_budget, **kw)
+        if bd.feasible:
+            entries.append((policy, bd))
+    if not entries:
+        raise NoFeasiblePolicy("every policy in the grid violates the memory budgets")
+    entries.sort(key=lambda e: (-e[1].throughput, e[0].as_tuple()))
+    return entries
+
+
+CALIBRATABLE = ("h2d_bytes_per_s", "tensor_efficiency", "round_overhead_s")
+
+
+def calibrate(observations, workload, rates: B200Rates, target: ModelArch, draft: ModelArch, hbm_budget: int,
+              host_budget: int, free_params=CALIBRATABLE, include_prefill: bool = False, **kw) -> B200Rates:
+    """Fit the B200 rates to measured (policy, tokens/s) pairs (planner.py:215-319
+    restated for this cost model): log-space least squares on relative error."""
+    import numpy as np
+    from scipy.optimize import least_squares
+
+    from .errors import Underdetermined, ValidationError
+
+    for name in free_params:
+        if name not in CALIBRATABLE:
+            raise ValidationError(f"'{name}' is not a calibratable rate")
+    if len(observations) < len(free_params):
+        raise Underdetermined(f"{len(observations)} observations cannot identify {len(free_params)} parameters")
+    measured = np.array([t for _, t in observations], dtype=np.float64)
+    z0 = np.log([getattr(rates, n) for n in free_params])
+
+    def with_z(z):
+        return dataclasses.replace(rates, **{n: float(np.exp(v)) for n, v in zip(free_params, z)})
+
+    def resid(z):
+        r = with_z(z)
+        pred = np.array([predict_throughput(p, workload, r, target, draft, hbm_budget, host_budget,
+                                            include_prefill=include_prefill, **kw).throughput
+                         for p, _ in observations])
+        return np.concatenate([pred / measured - 1.0, 0.05 * (z - z0)])
+
+    sol = least_squares(resid, z0, method="lm", max_nfev=400)
+    return with_z(sol.x)

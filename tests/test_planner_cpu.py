@@ -1,0 +1,100 @@
+"""CPU: the B200 planner (placement + cost model re-fit, SURVEY.md §8 a5–a11, a14–a15)."""
+import dataclasses
+
+import pytest
+
+from paper_2505_10259_b200 import MIXTRAL_8X7B, MIXTRAL_8X22B, MISTRAL_7B, MISTRAL_7B_V3, Policy, Workload
+from paper_2505_10259_b200.errors import InfeasiblePlan, NoFeasiblePolicy, Underdetermined
+from paper_2505_10259_b200.planner_b200 import (B200Rates, calibrate, plan_offload, predict_throughput,
+                                                roofline_tokens_per_s, search)
+from paper_2505_10259_b200.weights import ffn_offsets
+
+GiB = 1 << 30
+RATES = B200Rates(h2d_bytes_per_s=55.5e9)
+
+
+class Space:
+    """Minimal SearchSpace (planner.py:42-76 shape): lexicographic valid grid."""
+
+    def __init__(self, *axes):
+        self.axes = axes
+
+    def policies(self):
+        import itertools
+
+        out = []
+        for c in itertools.product(*[sorted(a) for a in self.axes]):
+            try:
+                out.append(Policy(*c))
+            except Exception:
+                continue
+        return out
+
+
+def test_plan_respects_both_budgets():
+    p = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9), 8, 0.8, 503, 45, RATES)
+    assert sum(p.hbm_bytes.values()) <= 190e9
+    assert p.host_bytes <= 191e9
+    assert len(p.stream_layers) + len(p.pinned_layers) == 56
+    # the pinned layers are the first ones (placement.py:220-231 ascending order)
+    assert p.pinned_layers == tuple(range(len(p.pinned_layers)))
+    assert p.t_round_s >= p.t_stream_s
+
+
+def test_capped_8x7b_needs_attention_streaming():
+    """at 24 GiB the resident set leaves no room unless attention streams."""
+    with pytest.raises(InfeasiblePlan):
+        plan_offload(MIXTRAL_8X7B, MISTRAL_7B, 24 * GiB, int(180e9), 4, 0.8, 503, 45, RATES, stream_attn_modes=(False,))
+    p = plan_offload(MIXTRAL_8X7B, MISTRAL_7B, 24 * GiB, int(180e9), 4, 0.8, 503, 45, RATES)
+    assert p.stream_attn and len(p.stream_layers) == 32
+    assert sum(p.hbm_bytes.values()) <= 24 * GiB
+
+
+def test_more_host_memory_never_hurts():
+    a = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(150e9), 4, 0.8, 503, 45, RATES)
+    b = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(250e9), 4, 0.8, 503, 45, RATES)
+    assert b.tokens_per_s >= a.tokens_per_s
+
+
+def test_reprefill_draft_frees_kv_for_a_bigger_batch():
+    c = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9), 8, 0.8, 503, 45, RATES,
+                     draft_kv_modes=("cached",))
+    r = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9), 8, 0.8, 503, 45, RATES,
+                     draft_kv_modes=("reprefill",))
+    assert r.bs_decoding > c.bs_decoding and r.tokens_per_s > c.tokens_per_s
+
+
+def test_search_ranks_and_rejects():
+    wl = Workload(464, 503, 16, 0.8)
+    ranked = search(Space((64,), (64, 128, 232), (32, 64), (2, 4, 8)), wl, RATES, MIXTRAL_8X22B, MISTRAL_7B_V3,
+                    int(190e9), int(191e9))
+    tps = [b.throughput for _, b in ranked]
+    assert tps == sorted(tps, reverse=True)
+    with pytest.raises(NoFeasiblePolicy):
+        search(Space((64,), (64,), (32,), (4,)), wl, RATES, MIXTRAL_8X22B, MISTRAL_7B_V3, int(20e9), int(10e9))
+
+
+def test_rounds_follow_one_verification_per_round():
+    wl = Workload(2 * 64, 503, 17, 1.0)  # E = n+1 = 5 at p = 1 → ceil(16/5) = 4 verifies per batch
+    bd = predict_throughput(Policy(64, 64, 64, 4), wl, RATES, MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9))
+    assert bd.rounds == 2 * 4
+
+
+def test_calibrate_recovers_link_rate():
+    wl = Workload(464, 503, 16, 0.8)
+    truth = dataclasses.replace(RATES, h2d_bytes_per_s=61e9)
+    pols = [Policy(64, b, 32, n) for b in (64, 128, 232) for n in (2, 4, 8)]
+    obs = [(p, predict_throughput(p, wl, truth, MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9),
+                                  include_prefill=False).throughput) for p in pols]
+    fit = calibrate(obs, wl, dataclasses.replace(RATES, h2d_bytes_per_s=40e9), MIXTRAL_8X22B, MISTRAL_7B_V3,
+                    int(190e9), int(191e9), free_params=("h2d_bytes_per_s",))
+    assert abs(fit.h2d_bytes_per_s / 61e9 - 1) < 0.02
+    with pytest.raises(Underdetermined):
+        calibrate(obs[:1], wl, RATES, MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(191e9))
+
+
+def test_roofline_definition():
+    # SURVEY.md §8d worked example: 270.58 GB streamed at 55 GB/s, 256·3.3616 tokens → 174.9 tok/s
+    S = 56 * ffn_offsets(MIXTRAL_8X22B)[2]
+    r = roofline_tokens_per_s(256 * 3.3616, S, 73e-3 * 1375.5e12, 55e9, 1375.5e12)
+    assert abs(r - 174.9) < 0.5
