@@ -244,8 +244,10 @@ def main():
     ev0.record(eng.tgt_stream)
     w0 = time.perf_counter()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects the timed rounds
+    eng.nvtx_range = "timed"             # ... on the draft-enqueue thread too
     for _ in range(steps):
         eng.round(s)  # public API: H2D inputs, verify+draft, barrier, D2H committed tokens
+    eng.nvtx_range = None
     torch.cuda.nvtx.range_pop()
     ev1.record(eng.tgt_stream)
     ev1.synchronize()

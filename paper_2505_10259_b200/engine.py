@@ -162,6 +162,7 @@ class Engine:
         self._cur = (None, None)  # (round, batch) being verified, for trace tags
         self._marks: dict = {}
         self._arenas: dict = {}   # stream handle -> _StagingArena (per-round H2D metadata)
+        self.nvtx_range: str | None = None  # mirrored onto the draft-enqueue thread when set
         self._join = native.Event()
         if trace:
             self.target.hooks = self._layer_hook
@@ -518,7 +519,13 @@ class Engine:
                 try:
                     torch.cuda.set_device(self.device)
                     native.set_device(self.device.index or 0)
-                    self._draft(s, 1 - bi, rnd)
+                    if self.nvtx_range:  # NVTX ranges are per thread (ncu --nvtx-include)
+                        torch.cuda.nvtx.range_push(self.nvtx_range)
+                    try:
+                        self._draft(s, 1 - bi, rnd)
+                    finally:
+                        if self.nvtx_range:
+                            torch.cuda.nvtx.range_pop()
                 except BaseException as exc:  # re-raised on the caller's thread
                     err.append(exc)
 
