@@ -30,6 +30,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// src_bytes = 0 → the 16 smem bytes are zero-filled (rows past the valid keys)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, bool valid) {
+  const uint32_t n = valid ? 16u : 0u;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -119,17 +124,23 @@ __global__ void __launch_bounds__(kThreads) attn_paged_kernel(
   float mA = -INFINITY, mB = -INFINITY, lA = 0.0f, lB = 0.0f;
 
   const int32_t* bt = block_table + (size_t)s * max_pages;
+  // Each key row resolves its own page, so any page size works (a 64-key tile
+  // may span several pages); rows at or past n_keys are zero-filled, keeping
+  // 0·V finite for masked keys whatever the unwritten cache holds.
   auto load_tile = [&](int kt, int buf) {
     const int key0 = kt * kKeys;
-    const int page = bt[key0 / page_size];
-    const size_t base = (((size_t)page * hkv + g_kv) * page_size + (key0 % page_size)) * DH;
     uint8_t* sk = smem + buf * 2 * TL::kBytes;
     uint8_t* sv = sk + TL::kBytes;
 #pragma unroll
     for (int i = threadIdx.x; i < kKeys * TL::kChunks; i += kThreads) {
       const int row = i / TL::kChunks, ch = i % TL::kChunks;
-      cp_async16(sk + TL::off(row, ch), kc + base + (size_t)row * DH + ch * 8);
-      cp_async16(sv + TL::off(row, ch), vc + base + (size_t)row * DH + ch * 8);
+      const int key = key0 + row;
+      const bool valid = key < n_keys;
+      const int kk = valid ? key : 0;
+      const int page = bt[kk / page_size];
+      const size_t src = (((size_t)page * hkv + g_kv) * page_size + (kk % page_size)) * DH + ch * 8;
+      cp_async16_zfill(sk + TL::off(row, ch), kc + src, valid);
+      cp_async16_zfill(sv + TL::off(row, ch), vc + src, valid);
     }
   };
 
@@ -274,7 +285,7 @@ extern "C" int so_attn_paged(const void* q, const void* k_cache, const void* v_c
                              int hq, int hkv, int dh, int page_size, float scale, void* out, void* stream) {
   SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
   SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
-  SO_REQUIRE(page_size % kKeys == 0, SO_E_SHAPE);
+  SO_REQUIRE(page_size >= 1, SO_E_SHAPE);
   SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (bs == 0) return SO_OK;
   cudaStream_t st = as_stream(stream);

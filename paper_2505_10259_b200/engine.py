@@ -146,7 +146,7 @@ class DecodeSession:
 
 
 class Engine:
-    def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 64,
+    def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 16,
                  trace: bool = True):
         self.target = target
         self.draft = draft

@@ -16,8 +16,11 @@ import torch
 from .config import ModelArch
 
 
+DEFAULT_PAGE = 16  # tokens per page: small pages waste ≤ 15 slots per sequence
+
+
 class PagedKVCache:
-    def __init__(self, arch: ModelArch, n_seq: int, max_len: int, device, page_size: int = 64):
+    def __init__(self, arch: ModelArch, n_seq: int, max_len: int, device, page_size: int = DEFAULT_PAGE):
         self.arch = arch
         self.page_size = page_size
         self.pages_per_seq = (max_len + page_size - 1) // page_size
@@ -33,7 +36,7 @@ class PagedKVCache:
         self.block_table = torch.from_numpy(bt).to(device)
 
     @staticmethod
-    def bytes_needed(arch: ModelArch, n_seq: int, max_len: int, page_size: int = 64) -> int:
+    def bytes_needed(arch: ModelArch, n_seq: int, max_len: int, page_size: int = DEFAULT_PAGE) -> int:
         pages = n_seq * ((max_len + page_size - 1) // page_size)
         return 2 * arch.n_layer * pages * arch.n_kv_head * page_size * arch.head_dim * 2
 

@@ -75,7 +75,7 @@ def resident_bytes(arch: ModelArch, include_ffn: bool) -> int:
     return b
 
 
-def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 64,
+def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 16,
              draft_seqs: int | None = None) -> int:
     """Target KV for every sequence; draft KV for ``draft_seqs`` (all of them when
     cached, one bs_draft chunk when the draft re-prefills: costmodel.py:132-137)."""
@@ -111,7 +111,7 @@ def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str)
 
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
-                 n_slots: int = 2, bs_candidates=None, page_size: int = 64, draft_kv_modes=("cached", "reprefill"),
+                 n_slots: int = 2, bs_candidates=None, page_size: int = 16, draft_kv_modes=("cached", "reprefill"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True)) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets."""
@@ -273,3 +273,34 @@ def calibrate(observations, workload, rates: B200Rates, target: ModelArch, draft
 
     sol = least_squares(resid, z0, method="lm", max_nfev=400)
     return with_z(sol.x)
+
+
+def predict_round_s(rates: B200Rates, target: ModelArch, draft: ModelArch, bs: int, n_cand: int, ctx: int,
+                    draft_kv: str, streamed_bytes: int) -> float:
+    """Round time of one measured configuration (fixed streamed split)."""
+    eff = rates.tensor_flops * rates.tensor_efficiency
+    comp = (verify_flops(target, bs, n_cand, ctx) + draft_flops(draft, bs, n_cand, ctx, draft_kv)) / eff
+    return max(streamed_bytes / rates.h2d_bytes_per_s, comp) + rates.round_overhead_s
+
+
+def calibrate_rounds(points, target: ModelArch, draft: ModelArch, rates: B200Rates, ctx: int,
+                     free_params=("h2d_bytes_per_s", "round_overhead_s")) -> B200Rates:
+    """Re-fit rates to measured rounds: points = [{policy: (bs_prefill, bs, bs_draft, n),
+    draft_kv, streamed_bytes, round_s}] (tools/sweep.py output); log-space LM on
+    relative round-time error with a weak pull to the prior (planner.py:251-274)."""
+    import numpy as np
+    from scipy.optimize import least_squares
+
+    meas = np.array([p["round_s"] for p in points])
+    z0 = np.log([getattr(rates, n) for n in free_params])
+
+    def with_z(z):
+        return dataclasses.replace(rates, **{n: float(np.exp(v)) for n, v in zip(free_params, z)})
+
+    def resid(z):
+        r = with_z(z)
+        pred = np.array([predict_round_s(r, target, draft, p["policy"][1], p["policy"][3], ctx, p["draft_kv"],
+                                         p["streamed_bytes"]) for p in points])
+        return np.concatenate([pred / meas - 1.0, 0.01 * (z - z0)])
+
+    return with_z(least_squares(resid, z0, method="lm", max_nfev=400).x)

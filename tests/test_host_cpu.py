@@ -31,7 +31,7 @@ def test_argument_validation_without_gpu(native_lib):
     # shape errors are reported before any CUDA call
     assert native_lib.so_gemm_bf16(None, None, 1, 1, 1, None, 1, 0, None, None) == -1
     assert native_lib.so_accept_greedy(1, 1, 1, None, 4, 0, 10, 1, 1, None) == -2
-    assert native_lib.so_attn_paged(1, 16, 16, 1, 1, 1, 1, 1, 1, 8, 2, 128, 48, 1.0, 1, None) == -2
+    assert native_lib.so_attn_paged(1, 16, 16, 1, 1, 1, 1, 1, 1, 8, 3, 128, 16, 1.0, 1, None) == -2  # hq % hkv
 
 
 def test_acceptance_matches_reference_golden():

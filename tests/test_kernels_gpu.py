@@ -299,14 +299,14 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
     return out
 
 
-@pytest.mark.parametrize("dh,hq,hkv,qlens,kvbs", [
-    (128, 48, 8, [5] * 6, [503, 0, 64, 1, 777, 130]),   # verify, 8x22B heads
-    (64, 4, 2, [5, 5, 5], [10, 100, 0]),                 # verify, tiny heads
-    (128, 32, 8, [17, 1, 64, 100], [0, 0, 0, 0]),        # prefill
-    (64, 4, 2, [33, 1], [3, 200]),                       # mixed
+@pytest.mark.parametrize("dh,hq,hkv,qlens,kvbs,ps", [
+    (128, 48, 8, [5] * 6, [503, 0, 64, 1, 777, 130], 64),   # verify, 8x22B heads
+    (128, 48, 8, [9] * 5, [503, 0, 17, 1, 130], 16),        # verify, n_cand 8, 16-token pages
+    (64, 4, 2, [5, 5, 5], [10, 100, 0], 32),                 # verify, tiny heads
+    (128, 32, 8, [17, 1, 64, 100], [0, 0, 0, 0], 16),        # prefill
+    (64, 4, 2, [33, 1], [3, 200], 64),                       # mixed
 ])
-def test_attn_paged(dh, hq, hkv, qlens, kvbs):
-    ps = 64
+def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps):
     bs = len(qlens)
     max_len = max(q + k for q, k in zip(qlens, kvbs))
     pps = (max_len + ps - 1) // ps + 1
@@ -314,8 +314,17 @@ def test_attn_paged(dh, hq, hkv, qlens, kvbs):
     g = torch.Generator(device=DEV).manual_seed(dh + bs)
     kc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
     vc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
+    # unwritten cache slots may hold anything: poison every slot past each
+    # sequence's keys with NaN — the kernel must never let them reach P·V
+    bt_host = None
     perm = torch.randperm(npages, device=DEV, generator=g).to(torch.int32)  # scattered pages
     bt = perm.view(bs, pps)
+    bt_host = bt.long().cpu().numpy()
+    for s in range(bs):
+        nk = qlens[s] + kvbs[s]
+        for key in range(nk, pps * ps):
+            kc[bt_host[s, key // ps], :, key % ps] = float("nan")
+            vc[bt_host[s, key // ps], :, key % ps] = float("nan")
     qs = torch.tensor(np.concatenate([[0], np.cumsum(qlens)]), dtype=torch.int32, device=DEV)
     kvb = torch.tensor(kvbs, dtype=torch.int32, device=DEV)
     T = sum(qlens)
