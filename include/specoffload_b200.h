@@ -137,6 +137,11 @@ int so_moe_combine(const void* y_perm, const int32_t* token_rows, const void* re
 int so_gemm_bf16(const void* A, const void* B, int M, int N, int K,
                  void* C, int ldc, int epilogue, const void* aux, void* stream);
 
+/* Tile variant of the GEMMs (process-wide; for tests and benchmarks):
+ * 0 = auto (CTA-pair 256×256 cta_group::2 tiles for M ≥ 1024 and N % 256 == 0,
+ * else 1-CTA 128×{128,256}), 1 = 1-CTA only, 2 = CTA-pair wherever legal. */
+int so_gemm_set_variant(int variant);
+
 /* Grouped (MoE) GEMM: rows [offs[e], offs[e+1]) of A use expert e's weight
  * B + e·N·K.  max_rows bounds offs[E] (no host sync: the tile schedule is
  * derived on device from offs). */

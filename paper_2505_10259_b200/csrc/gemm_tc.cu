@@ -135,6 +135,75 @@ struct Cfg {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+// TMEM → registers → global for one thread's accumulator row (32 columns per
+// tcgen05.ld), with the fused epilogue op.  `tbase` addresses lane window
+// (warp % 4)·32 of the CTA's accumulator.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(uint32_t tbase, bool valid, int grow, int n0, int N,
+                                              void* __restrict__ C, int ldc, const void* __restrict__ aux) {
+  if constexpr (EPI == SO_EPI_SWIGLU) {
+    // accumulator columns [128p, 128p+64) = gate, [128p+64, 128p+128) = up
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C);
+#pragma unroll 1
+    for (int p = 0; p < BN / 128; ++p) {
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t g[32], u[32];
+        tmem_ld32(tbase + p * 128 + h * 32, g);
+        tmem_ld32(tbase + p * 128 + 64 + h * 32, u);
+        tmem_ld_wait();
+        const int col = (n0 + p * 128) / 2 + h * 32;
+        if (valid && n0 + p * 128 < N) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
+          int4* dst = reinterpret_cast<int4*>(out + (size_t)grow * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + c, r);
+      tmem_ld_wait();
+      const int col = n0 + c;
+      if (!valid || col >= N) continue;
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
+      if constexpr (EPI == SO_EPI_F32) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (size_t)grow * ldc + col);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+      } else {
+        if constexpr (EPI == SO_EPI_BF16_RESID) {
+          const int4* res =
+              reinterpret_cast<const int4*>(reinterpret_cast<const __nv_bfloat16*>(aux) + (size_t)grow * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float rr[8];
+            unpack8(res[v], rr);
+            // round the GEMM result to bf16 first, then add (the bf16
+            // `residual + o_proj(x)` of the reference models)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[8 * v + j] = __bfloat162float(__float2bfloat16_rn(f[8 * v + j])) + rr[j];
+          }
+        } else if constexpr (EPI == SO_EPI_BF16_ROWSCALE) {
+          const float w = reinterpret_cast<const float*>(aux)[grow];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] *= w;
+        }
+        int4* dst = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(C) + (size_t)grow * ldc + col);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
+      }
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -241,67 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grow = row0 + row;
     const bool valid = grow < row_end && grow < M;
     const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16);
-    if constexpr (EPI == SO_EPI_SWIGLU) {
-      // accumulator columns [128p, 128p+64) = gate, [128p+64, 128p+128) = up
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C);
-#pragma unroll 1
-      for (int p = 0; p < BN / 128; ++p) {
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tbase + p * 128 + h * 32, g);
-          tmem_ld32(tbase + p * 128 + 64 + h * 32, u);
-          tmem_ld_wait();
-          const int col = (n0 + p * 128) / 2 + h * 32;
-          if (valid && n0 + p * 128 < N) {
-            float f[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = silu(__uint_as_float(g[j])) * __uint_as_float(u[j]);
-            int4* dst = reinterpret_cast<int4*>(out + (size_t)grow * ldc + col);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
-          }
-        }
-      }
-    } else {
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c, r);
-        tmem_ld_wait();
-        const int col = n0 + c;
-        if (!valid || col >= N) continue;
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(r[j]);
-        if constexpr (EPI == SO_EPI_F32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (size_t)grow * ldc + col);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
-        } else {
-          if constexpr (EPI == SO_EPI_BF16_RESID) {
-            const int4* res = reinterpret_cast<const int4*>(
-                reinterpret_cast<const __nv_bfloat16*>(aux) + (size_t)grow * ldc + col);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              float rr[8];
-              unpack8(res[v], rr);
-              // round the GEMM result to bf16 first, then add (matches the
-              // bf16 `residual + o_proj(x)` of the reference models)
-#pragma unroll
-              for (int j = 0; j < 8; ++j) f[8 * v + j] = __bfloat162float(__float2bfloat16_rn(f[8 * v + j])) + rr[j];
-            }
-          } else if constexpr (EPI == SO_EPI_BF16_ROWSCALE) {
-            const float w = reinterpret_cast<const float*>(aux)[grow];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] *= w;
-          }
-          int4* dst = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(C) + (size_t)grow * ldc + col);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) dst[v] = pack8(f + 8 * v);
-        }
-      }
-    }
+    epilogue_tile<BN, EPI>(tbase, valid, grow, n0, N, C, ldc, aux);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
@@ -309,6 +318,208 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(CF::kTmemCols));
+  }
+}
+
+// ---- 2-CTA variant: one 256×256 tile per CTA pair (cta_group::2) --------------
+//
+// The pair shares the operands of one M=256 × N=256 UMMA: CTA r of the pair
+// loads A rows [m0+128r, +128) and B rows [n0+128r, +128) into its own smem,
+// the leader (rank 0) issues tcgen05.mma.cta_group::2 that reads both CTAs'
+// halves, and each CTA's TMEM receives its 128 accumulator rows × 256 columns.
+// Per SM per k-block that is 32 KB of operand traffic instead of the 48 KB of
+// the 1-CTA 128×256 tile (whose L2 operand stream, not the tensor pipe, caps
+// it near 1 PFLOP/s).  Barrier protocol (as CUTLASS's PipelineTmaUmmaAsync):
+//   full[s]   leader's barrier only; armed once per phase by the leader with
+//             both halves' bytes; both CTAs' TMAs complete_tx on it (peer bit
+//             of the barrier address cleared);
+//   empty[s]  per CTA; the leader's tcgen05.commit multicasts to both;
+//   tmem_full per CTA; multicast commit after the last k-block.
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (++spins > (1u << 26)) __trap();
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+struct Cfg2 {
+  static constexpr int kStages = 6;
+  static constexpr int kABytes = 128 * BK * 2;  // this CTA's half of A
+  static constexpr int kBBytes = 128 * BK * 2;  // this CTA's half of B (N = 256 per pair)
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 256;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+};
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C, int ldc,
+                    const void* __restrict__ aux) {
+  using CF = Cfg2;
+  constexpr int BN = 256;
+  const uint32_t rank = cluster_rank();
+  const int pt = blockIdx.x >> 1;  // 256-row pair tile
+  const int nt = blockIdx.y;
+  int expert = 0, prow0 = pt * 256, row_end = M;
+  if (offs != nullptr) {
+    int before = 0;
+    expert = -1;
+    for (int e = 0; e < E; ++e) {
+      const int lo = offs[e], hi = offs[e + 1];
+      const int nt_e = (hi - lo + 255) / 256;
+      if (pt < before + nt_e) {
+        expert = e;
+        prow0 = lo + (pt - before) * 256;
+        row_end = hi;
+        break;
+      }
+      before += nt_e;
+    }
+    if (expert < 0) return;  // both CTAs of the pair see the same offsets → exit together
+  } else if (prow0 >= M) {
+    return;
+  }
+  const int row0 = prow0 + (int)rank * 128;
+  const int n0 = nt * BN;
+  const int num_kb = K / BK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::kStages * CF::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::kStages * CF::kStageBytes);
+  uint64_t* empty = full + CF::kStages;
+  uint64_t* tmem_full = empty + CF::kStages;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < CF::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs: each loads its halves) =====
+      const uint32_t leader_full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % CF::kStages;
+        const uint32_t ph = (kb / CF::kStages) & 1;
+        mbar_wait_guard(&empty[s], ph ^ 1);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * CF::kStageBytes);
+        const uint32_t bar = leader_full0 + s * 8;
+        tma_load_2d_pair(sA + s * CF::kABytes, &tmA, bar, kb * BK, row0);
+        tma_load_3d_pair(sB + s * CF::kBBytes, &tmB, bar, kb * BK, n0 + (int)rank * 128, expert);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (leader CTA only) =====
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(256 >> 4) << 24);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % CF::kStages;
+        const uint32_t ph = (kb / CF::kStages) & 1;
+        mbar_wait_guard(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + s * CF::kABytes);
+        const uint32_t b0 = smem_u32(sB + s * CF::kBBytes);
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          umma_bf16_pair(tmem_base, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
+                         (kb | kk) != 0);
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(tmem_full);
+    }
+  } else {
+    // ===== epilogue (both CTAs, own 128 rows) =====
+    mbar_wait_guard(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int grow = row0 + row;
+    const bool valid = grow < row_end && grow < M;
+    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    epilogue_tile<BN, EPI>(tbase, valid, grow, n0, N, C, ldc, aux);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  cluster_sync();  // the peer's TMEM is done with before the pair frees it
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::kTmemCols));
   }
 }
 
@@ -388,9 +599,38 @@ int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs,
   return SO_OK;
 }
 
+int g_variant = 0;  // 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where legal
+
+template <int EPI>
+int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
+                const void* aux, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, A, (uint64_t)M, (uint64_t)K, 128);
+  if (rc) return rc;
+  rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
+  if (rc) return rc;
+  auto kern = gemm_tc2_kernel<EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg2::kSmem);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  const int pair_tiles = offs ? (M + 255) / 256 + E : (M + 255) / 256;
+  dim3 grid(2 * pair_tiles, N / 256);
+  kern<<<grid, kThreads, Cfg2::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
 template <int EPI>
 int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
                const void* aux, cudaStream_t st) {
+  // CTA-pair 256×256 tiles halve the per-SM operand stream; 1-CTA tiles keep
+  // the waste of small M (decode steps, skinny experts) down.
+  const bool pair_ok = (N % 256) == 0;
+  if (pair_ok && (g_variant == 2 || (g_variant == 0 && M >= 1024)))
+    return launch_pair<EPI>(A, B, offs, E, M, N, K, C, ldc, aux, st);
   const int m_tiles = offs ? (M + BM - 1) / BM + E : (M + BM - 1) / BM;
   // prefer the wide tile unless it leaves most SMs idle
   bool wide = (long)m_tiles * ((N + 255) / 256) >= sm_count() || EPI == SO_EPI_SWIGLU && (N % 256) == 0;
@@ -444,3 +684,9 @@ extern "C" int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t*
 }
 
 extern "C" int so_device_sm_count(void) { return sm_count(); }
+
+extern "C" int so_gemm_set_variant(int variant) {
+  SO_REQUIRE(variant >= 0 && variant <= 2, SO_E_SHAPE);
+  g_variant = variant;
+  return SO_OK;
+}

@@ -33,6 +33,7 @@ _SIGNATURES = {
     "so_status_string": (ctypes.c_char_p, [c_int]),
     "so_device_sm_count": (c_int, []),
     "so_set_device": (c_int, [c_int]),
+    "so_gemm_set_variant": (c_int, [c_int]),
     "so_accept_greedy": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_accept_sample": (c_int, [_P, _P, _P, _P, _P, _P, c_float, c_int, c_int, c_int, _P, _P, _P]),
     "so_sample_tokens": (c_int, [_P, c_int64, _P, c_float, c_int, c_int, _P, c_int64, _P, c_int64, _P]),
@@ -101,6 +102,11 @@ def reset_launch_counter() -> None:
     with _count_lock:
         launches["kernels"] = 0
         launches["copies"] = 0
+
+
+def gemm_set_variant(variant: int) -> None:
+    """0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair (cta_group::2) tiles wherever legal."""
+    _check(lib().so_gemm_set_variant(variant), "so_set_device")
 
 
 def set_device(index: int) -> None:

@@ -173,6 +173,14 @@ def test_moe_combine():
 
 # ------------------------------------------------------------- K3/K4/K5 ---
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta_pair"])
+def gemm_variant(request):
+    """Run each GEMM test on the 1-CTA tiles and on the cta_group::2 pair tiles."""
+    native.gemm_set_variant(request.param)
+    yield request.param
+    native.gemm_set_variant(0)
+
+
 def _bf16_close(got, want, rel=1.5e-2):
     """bf16 output: |err| ≤ rel·(|want| + rms(want)) (fp32 accumulation-order + one rounding)."""
     got, want = got.float(), want.float()
@@ -183,7 +191,7 @@ def _bf16_close(got, want, rel=1.5e-2):
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 64), (128, 128, 128), (200, 384, 256), (1280, 8192, 6144),
                                    (77, 32768, 512), (4096, 4096, 4096), (3, 32, 64)])
-def test_gemm_dense(M, N, K):
+def test_gemm_dense(M, N, K, gemm_variant):
     g = torch.Generator(device=DEV).manual_seed(M + N + K)
     a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
     b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
@@ -201,7 +209,7 @@ def test_gemm_dense(M, N, K):
 
 
 @pytest.mark.parametrize("M,I,K", [(5, 128, 64), (300, 512, 256), (257, 16384 // 8, 6144 // 4)])
-def test_gemm_swiglu(M, I, K):
+def test_gemm_swiglu(M, I, K, gemm_variant):
     g = torch.Generator(device=DEV).manual_seed(M)
     a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
     wg = (torch.randn(I, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
@@ -218,7 +226,7 @@ def test_gemm_swiglu(M, I, K):
 
 @pytest.mark.parametrize("counts", [[0, 3, 130, 0, 1, 255, 256, 7], [320] * 8, [1, 0, 0, 0, 0, 0, 0, 0],
                                     [1000, 24, 0, 0, 513, 2, 2, 9]])
-def test_gemm_grouped(counts):
+def test_gemm_grouped(counts, gemm_variant):
     E, N, K = len(counts), 256, 384
     rows = sum(counts)
     g = torch.Generator(device=DEV).manual_seed(rows)

@@ -1,0 +1,84 @@
+#!/usr/bin/env python
+"""GEMM throughput on the path's real shapes, 1-CTA vs CTA-pair (cta_group::2) tiles.
+
+    python tools/gemm_bench.py > gpurun_out/gemm_bench.json
+
+CUDA-event timing, 3 warm-up + 10 timed launches per shape; TFLOP/s against
+the measured cuBLAS bf16 burst peak (MEASURED_PEAKS.json).  Weights are
+re-used across launches (L2-resident up to 126 MB; the MoE shapes exceed it).
+"""
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2505_10259_b200 import native  # noqa: E402
+
+DEV = "cuda:0"
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1590.0
+
+
+def timed(fn, reps=10):
+    for _ in range(3):
+        fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3
+
+
+def main():
+    g = torch.Generator(device=DEV).manual_seed(0)
+    rows = []
+    shapes = [
+        # name, M(rows), N, K, epilogue, grouped experts (0 = dense)
+        ("8x22B MoE gate_up (bs 248, n 8)", 4464, 32768, 6144, native.EPI_SWIGLU, 8),
+        ("8x22B MoE down (bs 248, n 8)", 4464, 6144, 16384, native.EPI_BF16_ROWSCALE, 8),
+        ("8x22B QKV (T 2232)", 2232, 8192, 6144, native.EPI_BF16, 0),
+        ("8x22B LM head (T 2232)", 2232, 32768, 6144, native.EPI_F32, 0),
+        ("Mistral-7B re-prefill gate_up (64 seqs x 520)", 33280, 28672, 4096, native.EPI_SWIGLU, 0),
+        ("Mistral-7B re-prefill down", 33280, 4096, 14336, native.EPI_BF16_RESID, 0),
+        ("square 8192^3", 8192, 8192, 8192, native.EPI_BF16, 0),
+    ]
+    for name, M, N, K, epi, E in shapes:
+        a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+        b = (torch.randn(max(E, 1) * N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+        out_cols = N // 2 if epi == native.EPI_SWIGLU else N
+        out = torch.empty(M, out_cols, dtype=torch.float32 if epi == native.EPI_F32 else torch.bfloat16, device=DEV)
+        aux = None
+        if epi == native.EPI_BF16_RESID:
+            aux = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
+        elif epi == native.EPI_BF16_ROWSCALE:
+            aux = torch.rand(M, device=DEV, generator=g)
+        if E:
+            cnt = np.full(E, M // E)
+            cnt[: M - cnt.sum()] += 1
+            offs = torch.tensor(np.concatenate([[0], np.cumsum(cnt)]), dtype=torch.int32, device=DEV)
+            fn = lambda: native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, epi, aux)  # noqa: E731
+        else:
+            fn = lambda: native.gemm(a, b, out, epi, aux)  # noqa: E731
+        flops = 2.0 * M * N * K
+        res = {"shape": name, "M": M, "N": N, "K": K}
+        for variant, label in ((1, "cta1"), (2, "cta_pair")):
+            native.gemm_set_variant(variant)
+            t = timed(fn)
+            res[label] = {"ms": t * 1e3, "tflops": flops / t / 1e12, "frac_of_peak": flops / t / 1e12 / PEAK}
+        native.gemm_set_variant(0)
+        rows.append(res)
+        print(json.dumps(res), flush=True)
+        del a, b, out, aux
+        torch.cuda.empty_cache()
+    print(json.dumps({"peak_tflops": PEAK, "rows": rows}))
+
+
+if __name__ == "__main__":
+    main()
