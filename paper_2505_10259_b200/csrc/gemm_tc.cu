@@ -626,10 +626,11 @@ int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M,
 template <int EPI>
 int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
                const void* aux, cudaStream_t st) {
-  // CTA-pair 256×256 tiles halve the per-SM operand stream; 1-CTA tiles keep
-  // the waste of small M (decode steps, skinny experts) down.
+  // CTA-pair 256×256 tiles cut the per-SM operand stream by a third; 1-CTA
+  // 128-row tiles pad less when M is small or split into experts (~560 rows
+  // each at bs 248: measured 0.58 vs 0.51 of peak, profiles/gemm_bench_r1.json).
   const bool pair_ok = (N % 256) == 0;
-  if (pair_ok && (g_variant == 2 || (g_variant == 0 && M >= 1024)))
+  if (pair_ok && (g_variant == 2 || (g_variant == 0 && offs == nullptr && M >= 1024)))
     return launch_pair<EPI>(A, B, offs, E, M, N, K, C, ldc, aux, st);
   const int m_tiles = offs ? (M + BM - 1) / BM + E : (M + BM - 1) / BM;
   // prefer the wide tile unless it leaves most SMs idle
