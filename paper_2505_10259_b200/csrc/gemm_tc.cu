@@ -135,6 +135,20 @@ struct Cfg {
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
 
+// Grouped raster of a 1-D tile index: bands of G m-tiles sweep every n-tile
+// before the next band starts, so a band's A rows stay L2-resident across the
+// n sweep (a 33k-row re-prefill activation would otherwise be re-read from HBM
+// once per n-tile) while each B tile is shared by the band's G m-tiles.
+__device__ __forceinline__ void raster_tile(int lin, int m_tiles, int n_tiles, int& mt, int& nt) {
+  constexpr int G = 16;
+  const int group = lin / (G * n_tiles);
+  const int first = group * G;
+  const int gm = min(G, m_tiles - first);
+  const int r = lin - group * G * n_tiles;
+  mt = first + r % gm;
+  nt = r / gm;
+}
+
 // TMEM → registers → global for one thread's accumulator row (32 columns per
 // tcgen05.ld), with the fused epilogue op.  `tbase` addresses lane window
 // (warp % 4)·32 of the CTA's accumulator.
@@ -208,11 +222,11 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C,
-                   int ldc, const void* __restrict__ aux) {
+                   int ldc, const void* __restrict__ aux, int m_tiles, int n_tiles) {
   using CF = Cfg<BN>;
   // ---- tile → (expert, row range) -------------------------------------------
-  const int mt = blockIdx.x;
-  const int nt = blockIdx.y;
+  int mt, nt;
+  raster_tile(blockIdx.x, m_tiles, n_tiles, mt, nt);
   int expert = 0, row0 = mt * BM, row_end = M;
   if (offs != nullptr) {
     int before = 0;
@@ -409,12 +423,12 @@ template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C, int ldc,
-                    const void* __restrict__ aux) {
+                    const void* __restrict__ aux, int m_tiles, int n_tiles) {
   using CF = Cfg2;
   constexpr int BN = 256;
   const uint32_t rank = cluster_rank();
-  const int pt = blockIdx.x >> 1;  // 256-row pair tile
-  const int nt = blockIdx.y;
+  int pt, nt;  // 256-row pair tile, n tile (both CTAs of the cluster decode the same pair)
+  raster_tile(blockIdx.x >> 1, m_tiles, n_tiles, pt, nt);
   int expert = 0, prow0 = pt * 256, row_end = M;
   if (offs != nullptr) {
     int before = 0;
@@ -593,8 +607,8 @@ int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs,
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  dim3 grid(m_tiles, (N + BN - 1) / BN);
-  kern<<<grid, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux);
+  const int n_tiles = (N + BN - 1) / BN;
+  kern<<<m_tiles * n_tiles, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
   SO_CHECK_LAUNCH();
   return SO_OK;
 }
@@ -617,8 +631,9 @@ int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M,
     attr_set = true;
   }
   const int pair_tiles = offs ? (M + 255) / 256 + E : (M + 255) / 256;
-  dim3 grid(2 * pair_tiles, N / 256);
-  kern<<<grid, kThreads, Cfg2::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux);
+  const int n_tiles = N / 256;
+  kern<<<2 * pair_tiles * n_tiles, kThreads, Cfg2::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, pair_tiles,
+                                                                 n_tiles);
   SO_CHECK_LAUNCH();
   return SO_OK;
 }
