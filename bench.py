@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--layers", type=int, default=0,
                     help="profiling only: override the target's layer count (same per-layer shapes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e-generate", action="store_true",
+                    help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
+    ap.add_argument("--e2e-seqs", type=int, default=256, help="sequences of the generate() leg")
+    ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
     ap.add_argument("--trace-out", default="")
     return ap.parse_args()
 
@@ -310,6 +314,28 @@ def main():
     except Exception as exc:  # the headline must still print
         kern = {"error": str(exc)}
 
+    # ---- generate(): the paper's end-to-end tokens/s (prefill included) ----
+    gen = None
+    if not args.no_e2e_generate:
+        del s
+        torch.cuda.empty_cache()
+        S_e = args.e2e_seqs
+        rng = np.random.default_rng(1234 + rank)
+        prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
+        pol = Policy(bs_prefill=S_e, bs_decoding=(S_e + 1) // 2, bs_draft=min(64, (S_e + 1) // 2),
+                     n_cand=args.n_cand)
+        torch.cuda.synchronize(device)
+        g0 = time.perf_counter()
+        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=plan.draft_kv)
+        g_wall = time.perf_counter() - g0
+        assert all(len(t) == args.e2e_new for t in toks)
+        gs = eng.last_session
+        gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
+               "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
+               "policy": list(pol.as_tuple()), "draft_kv": plan.draft_kv,
+               "note": "Engine.generate(): host token ids in, layer-major prefill (each streamed layer crosses "
+                       "the link once), dual-batch decode, host token lists out; paper's e2e definition"}
+
     if args.trace_out and rank == 0:
         from paper_2505_10259_b200.trace import SimResult, busy, export_chrome
 
@@ -352,6 +378,8 @@ def main():
                 "d2h_bytes_per_step": int(bs * (args.n_cand + 2) * 4)},
         "plan": plan.as_dict(),
     }
+    if gen is not None:
+        line["e2e_generate"] = gen
     if cpu is not None:
         line["cpu_baseline"] = {"value": cpu.tokens_per_s, "unit": "tokens/s", "cores": cpu.cores, "kind": "port",
                                 "sample": cpu.sample}

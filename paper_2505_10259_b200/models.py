@@ -112,8 +112,9 @@ class CausalLM:
         Ttot = sum(c.T for c in chunks)
         Tmax = max(c.T for c in chunks)
         H, dh, hq, hkv = a.hidden, a.head_dim, a.n_head, a.n_kv_head
+        # one hidden-state buffer for all chunks, updated in place: a layer reads
+        # x only until h = attn·Woᵀ + x exists, so its output can overwrite x
         xa = ws.get("x", (Ttot, H), torch.bfloat16)
-        xb = ws.get("x2", (Ttot, H), torch.bfloat16)
         xn = ws.get("xn", (Tmax, H), torch.bfloat16)
         h = ws.get("h", (Tmax, H), torch.bfloat16)
         qkv = ws.get("qkv", (Tmax, a.qkv_rows), torch.bfloat16)
@@ -138,7 +139,7 @@ class CausalLM:
             for ci, c in enumerate(chunks):
                 T = c.T
                 x = xa[c.row0:c.row0 + T]
-                out = xb[c.row0:c.row0 + T]
+                out = x  # in place (see above)
                 native.rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
                 native.gemm(xn[:T], wqkv, qkv[:T], native.EPI_BF16, None, stream)
                 native.rope_kv_append(qkv[:T], c.positions, c.slots, hq, hkv, dh, a.rope_theta, kv.page_size,
@@ -159,7 +160,6 @@ class CausalLM:
             self._ffn_release(li, stream)
             if hook:
                 hook(li, "ffn_end", stream)
-            xa, xb = xb, xa
         if not want_logits:
             return None
         rows_idx = [c.last_rows for c in chunks if c.last_rows is not None]
