@@ -76,7 +76,11 @@ struct Tile {
 };
 
 template <int DH>
-__global__ void __launch_bounds__(kThreads) attn_paged_kernel(
+#ifndef SO_ATTN_MINB
+#define SO_ATTN_MINB 3  // CTAs per SM the register budget must allow (3 × 128 threads ≤ 170 regs)
+#endif
+
+__global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
     const int32_t* __restrict__ block_table, int max_pages, const int32_t* __restrict__ q_start,
     const int32_t* __restrict__ kv_before, int hq, int hkv, int page_size, float scale_log2,
@@ -266,6 +270,8 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
+      e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }

@@ -1,0 +1,59 @@
+#!/usr/bin/env python
+"""Verify-attention (K6) bandwidth at the bench shape: 8x22B heads (48 q / 8 kv × 128),
+bs sequences × (n_cand+1) queries over ctx keys, 16-token pages.
+
+    python tools/attn_bench.py
+
+KV bytes read per launch = bs · (ctx + n + 1) · n_kv · dh · 2 (K,V) · 2 B; GB/s against
+the measured HBM copy peak (MEASURED_PEAKS.json).  Caches larger than L2 (126 MB), so
+every launch streams from HBM.
+"""
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2505_10259_b200 import native  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20):
+    dev = "cuda:0"
+    q_len = n + 1
+    max_len = ctx + q_len
+    pps = (max_len + ps - 1) // ps
+    npages = bs * pps
+    g = torch.Generator(device=dev).manual_seed(0)
+    kc = torch.randn(npages, hkv, ps, dh, device=dev, generator=g).to(torch.bfloat16)
+    vc = torch.randn(npages, hkv, ps, dh, device=dev, generator=g).to(torch.bfloat16)
+    bt = torch.arange(npages, dtype=torch.int32, device=dev).view(bs, pps)
+    qs = torch.arange(bs + 1, dtype=torch.int32, device=dev) * q_len
+    kvb = torch.full((bs,), ctx, dtype=torch.int32, device=dev)
+    q = torch.randn(bs * q_len, hq * dh, device=dev, generator=g).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    f = lambda: native.attn_paged(q, kc, vc, bt, qs, kvb, q_len, hq, hkv, dh, ps, 1 / math.sqrt(dh), out)  # noqa
+    for _ in range(3):
+        f()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        f()
+    b.record()
+    b.synchronize()
+    t = a.elapsed_time(b) / reps * 1e-3
+    kv_bytes = bs * (ctx + q_len) * hkv * dh * 2 * 2
+    return {"bs": bs, "n_cand": n, "ctx": ctx, "us": t * 1e6, "kv_MB": kv_bytes / 1e6,
+            "GBps": kv_bytes / t / 1e9, "frac_of_hbm_peak": kv_bytes / t / 1e9 / PEAK}
+
+
+if __name__ == "__main__":
+    res = [run(), run(bs=128, n=4), run(bs=248, n=8, ctx=2000)]
+    for r in res:
+        print(json.dumps(r))
