@@ -10,8 +10,8 @@
 // Work unit: one CTA (4 warps) per (sequence, kv-head, 64-row query tile).  The
 // rows of a (sequence, kv-head) pair are all q_len positions × the G = hq/hkv
 // query heads sharing that KV head (GQA), so each K/V tile read from HBM feeds
-// every query head of the group.  K/V tiles of 64 keys are staged with 16-B
-// cp.async into an XOR-swizzled, double-buffered smem ring (one page = one
+// every query head of the group.  K/V tiles of 32 keys are staged with 16-B
+// cp.async into an XOR-swizzled, 4-stage smem ring (one page = one
 // contiguous [page_size, dh] block per kv-head, so a tile is one coalesced
 // 8–16 KB run); S = QKᵀ and O += PV run on bf16 mma.sync with fp32 accumulate;
 // the softmax is the online (flash) form with quad-shuffle row reductions.
@@ -20,7 +20,8 @@
 namespace {
 
 constexpr int kRows = 64;   // query rows per CTA (4 warps × 16)
-constexpr int kKeys = 64;   // keys per smem tile
+constexpr int kKeys = 32;   // keys per smem tile
+constexpr int kStages = 4;  // cp.async ring depth (4 × 16 KB of K+V at dh = 128)
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -148,17 +149,24 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
     }
   };
 
-  load_tile(0, 0);
-  cp_commit();
-  for (int kt = 0; kt < n_tiles; ++kt) {
-    if (kt + 1 < n_tiles) load_tile(kt + 1, (kt + 1) & 1);
+  // kStages-deep cp.async ring: kStages−1 tiles stream from HBM while one is
+  // consumed (one commit group per tile, empty groups past the end keep the
+  // wait_group arithmetic uniform)
+#pragma unroll
+  for (int p = 0; p < kStages - 1; ++p) {
+    if (p < n_tiles) load_tile(p, p);
     cp_commit();
-    cp_wait<1>();
+  }
+  for (int kt = 0; kt < n_tiles; ++kt) {
+    const int nxt = kt + kStages - 1;
+    if (nxt < n_tiles) load_tile(nxt, nxt % kStages);
+    cp_commit();
+    cp_wait<kStages - 1>();
     __syncthreads();
     if (warp_live) {
-      const uint32_t sk = smem_u32(smem + (kt & 1) * 2 * TL::kBytes);
+      const uint32_t sk = smem_u32(smem + (kt % kStages) * 2 * TL::kBytes);
       const uint32_t sv = sk + TL::kBytes;
-      // ---- S = Q Kᵀ  (16 rows × 64 keys per warp) ----
+      // ---- S = Q Kᵀ  (16 rows × kKeys keys per warp) ----
       float sfr[kKeys / 8][4];
 #pragma unroll
       for (int nt = 0; nt < kKeys / 8; ++nt) sfr[nt][0] = sfr[nt][1] = sfr[nt][2] = sfr[nt][3] = 0.0f;
@@ -266,7 +274,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
            cudaStream_t st) {
   const int G = hq / hkv;
   const int tiles = (max_q * G + kRows - 1) / kRows;
-  const size_t smem = 2 * 2 * (size_t)Tile<DH>::kBytes;
+  const size_t smem = (size_t)kStages * 2 * Tile<DH>::kBytes;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
