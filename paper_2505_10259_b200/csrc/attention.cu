@@ -128,9 +128,18 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
   float mA = -INFINITY, mB = -INFINITY, lA = 0.0f, lB = 0.0f;
 
-  const int32_t* bt = block_table + (size_t)s * max_pages;
-  // Each key row resolves its own page, so any page size works (a 64-key tile
-  // may span several pages); rows at or past n_keys are zero-filled, keeping
+  // The sequence's page list is staged in smem once: every K/V row resolves its
+  // page from it, so issuing a tile's cp.asyncs never waits on a dependent
+  // global load (which had cost one memory latency per tile step).
+  int32_t* bt = reinterpret_cast<int32_t*>(smem + kStages * 2 * TL::kBytes);
+  {
+    const int32_t* gbt = block_table + (size_t)s * max_pages;
+    const int used = min(max_pages, (n_keys + page_size - 1) / page_size);
+    for (int i = threadIdx.x; i < used; i += kThreads) bt[i] = gbt[i];
+    __syncthreads();
+  }
+  // Each key row resolves its own page, so any page size works (a tile may
+  // span several pages); rows at or past n_keys are zero-filled, keeping
   // 0·V finite for masked keys whatever the unwritten cache holds.
   auto load_tile = [&](int kt, int buf) {
     const int key0 = kt * kKeys;
@@ -274,14 +283,14 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
            cudaStream_t st) {
   const int G = hq / hkv;
   const int tiles = (max_q * G + kRows - 1) / kRows;
-  const size_t smem = (size_t)kStages * 2 * Tile<DH>::kBytes;
-  static bool attr = false;
-  if (!attr) {
+  const size_t smem = (size_t)kStages * 2 * Tile<DH>::kBytes + (size_t)max_pages * sizeof(int32_t);
+  static size_t attr_bytes = 0;  // raised when a longer block table needs more smem
+  if (smem > attr_bytes) {
     cudaError_t e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
       e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr_bytes = smem;
   }
   dim3 grid(tiles, hkv, bs);
   attn_paged_kernel<DH><<<grid, kThreads, smem, st>>>(
