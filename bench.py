@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--e2e-seqs", type=int, default=256, help="sequences of the generate() leg")
     ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
     ap.add_argument("--trace-out", default="")
+    ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
+                    help="streamed units XC4-encoded in host DRAM (K9, lossless) or raw bf16")
     return ap.parse_args()
 
 
@@ -203,25 +205,41 @@ def main():
     max_new = verifies_per_batch * (args.n_cand + 1) + 1
     from paper_2505_10259_b200.planner_b200 import B200Rates
 
-    rates = B200Rates(h2d_bytes_per_s=link)
+    rates = B200Rates(h2d_bytes_per_s=link, hbm_bytes_per_s=peaks["hbm_gbs"] * 1e9)
     modes = ("cached", "reprefill") if args.draft_kv == "auto" else (args.draft_kv,)
+    ratio, ring = 1.0, 0
+    if args.codec == "xc4":
+        # encoded/raw ratio of this weight distribution, probed on one 64 Mi-weight sample
+        from paper_2505_10259_b200 import codec as C
+
+        g = torch.Generator(device=device).manual_seed(12345)
+        probe = torch.empty(1 << 26, dtype=torch.bfloat16, device=device).normal_(0.0, 0.02, generator=g)
+        enc = C.Encoder(device)
+        ratio = enc.encode(probe)[0].numel() / (2 * probe.numel()) * 1.002
+        ring = 4 * (64 << 20)  # LayerStreamer.RING_SLOTS encoded frames (≈50 MB each)
+        enc.release()
+        del probe
+        torch.cuda.empty_cache()
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
-                        bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes)
+                        bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
+                        ring_bytes=ring)
     t_setup = time.perf_counter()
     layer_bytes = ffn_offsets(tgt)[2]
     if world > 1:
         from paper_2505_10259_b200.streamer import SharedHostStore
 
+        cap = layer_bytes if args.codec == "none" else -(-int(layer_bytes * (ratio + 0.005)) // (2 << 20)) * (2 << 20)
         store = SharedHostStore(f"specoffload_{os.environ.get('MASTER_PORT', '0')}", list(plan.stream_layers),
-                                layer_bytes, rank, world, barrier=dist.barrier)
+                                cap, rank, world, barrier=dist.barrier, coded=args.codec != "none")
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
                            seed=1, trace=bool(args.trace_out), rank=rank, world=world, shared_store=store,
-                           stream_attn=plan.stream_attn)
+                           stream_attn=plan.stream_attn, codec=args.codec)
         dist.barrier()  # every slice of the shared store is written
     else:
         store = HostStore()
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
-                           seed=1, trace=bool(args.trace_out), host_store=store, stream_attn=plan.stream_attn)
+                           seed=1, trace=bool(args.trace_out), host_store=store, stream_attn=plan.stream_attn,
+                           codec=args.codec)
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
@@ -239,6 +257,7 @@ def main():
     committed0 = s.committed_decode
     st = eng.target.streamer
     bytes0 = st.bytes_issued if st else 0
+    raw0 = st.raw_bytes_issued if st else 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if eng.tracer.enabled:
@@ -262,7 +281,8 @@ def main():
     clk = clocks.stop()
     dev_s = ev0.elapsed_time(ev1) * 1e-3
     committed = s.committed_decode - committed0
-    streamed = (st.bytes_issued - bytes0) if st else 0
+    streamed = (st.bytes_issued - bytes0) if st else 0       # bytes over this rank's link
+    streamed_raw = (st.raw_bytes_issued - raw0) if st else 0  # layer bytes they delivered
     launches = dict(native.launches)
     if world > 1:
         t = torch.tensor([dev_s, wall], device=device, dtype=torch.float64)
@@ -279,8 +299,10 @@ def main():
     achieved_link = streamed / dev_s if dev_s > 0 else 0.0
     e_tok = expected_accepted(AcceptanceModel(args.p, args.n_cand))
     F = verify_flops(tgt, bs, args.n_cand, args.ctx)
-    roof = roofline_tokens_per_s(bs * e_tok * world, len(plan.stream_layers) * layer_bytes // world, F, link,
-                                 peaks["bf16_tflops_sustained"] * 1e12)
+    # north-star roofline: committed tokens over max(link bytes / B_h2d, compute at peak), per round
+    roof = roofline_tokens_per_s(bs * e_tok * world, streamed / steps, F, link, peaks["bf16_tflops_sustained"] * 1e12)
+    roof_raw = roofline_tokens_per_s(bs * e_tok * world, streamed_raw / steps, F, link,
+                                     peaks["bf16_tflops_sustained"] * 1e12)
 
     # ---- tensor-core kernel sample: MoE gate_up grouped GEMM at this round's shape ----
     kern = {}
@@ -313,6 +335,39 @@ def main():
         del a, act
     except Exception as exc:  # the headline must still print
         kern = {"error": str(exc)}
+
+    # ---- K9 decode kernel sample: ring-resident encoded frames → a window slot (HBM → HBM) ----
+    codec_k = None
+    if st is not None and st.coded:
+        try:
+            u = st.host[st.streamed[0]]
+            nf = min(st.RING_SLOTS, u.n_frames)
+            # frames [0, nf) copied contiguously into the staging ring; the decoder
+            # addresses frame f at base + frame_off[f], so base = ring − frame_off[0]
+            native.memcpy_async(st.ring.data_ptr(), u.data.data_ptr() + int(u.frame_off[0]), u.frame_bytes(0, nf),
+                                torch.cuda.current_stream(device))
+            base = st.ring.data_ptr() - int(u.frame_off[0])
+            out = st.slots[0].data_ptr()
+            for _ in range(2):
+                native.xc4_decode(u.data.data_ptr(), base, 0, nf, out)
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            x0.record()
+            for _ in range(reps):
+                native.xc4_decode(u.data.data_ptr(), base, 0, nf, out)
+            x1.record()
+            x1.synchronize()
+            t_d = x0.elapsed_time(x1) * 1e-3 / reps
+            raw_f = 2 * min(u.n_elems, nf * u.frame_elems)
+            algo = u.frame_bytes(0, nf) + raw_f
+            codec_k = {"kernel": "xc4_decode_kernel (K9)", "bound": "hbm", "achieved": algo / t_d / 1e9,
+                       "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": algo / t_d / 1e9 / peaks["hbm_gbs"],
+                       "ms_per_launch_group": t_d * 1e3, "frames": nf, "algorithmic_bytes": algo,
+                       "ms_per_layer_est": t_d * 1e3 * u.n_frames / nf, "ratio": u.ratio, "escapes": u.n_escapes,
+                       "frames_per_layer": u.n_frames,
+                       "note": "algorithmic bytes = encoded frames read + decoded bf16 written"}
+        except Exception as exc:
+            codec_k = {"error": str(exc)}
 
     # ---- generate(): the paper's end-to-end tokens/s (prefill included) ----
     gen = None
@@ -362,14 +417,20 @@ def main():
                    "draft_kv": plan.draft_kv, "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
-                   "streamed_bytes_per_round": len(plan.stream_layers) * layer_bytes,
+                   "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
+                   "streamed_bytes_per_round": int(streamed / steps * world),
+                   "streamed_layer_bytes_per_round": len(plan.stream_layers) * layer_bytes,
                    "host_pinned_bytes": store.bytes, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
                    "parallelism": f"dp{world} (independent prompt shards)", "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "h2d", "achieved": achieved_link / 1e9, "peak": link / 1e9, "unit": "GB/s",
                      "frac": achieved_link / link, "traffic": None,
-                     "note": "dominant 'kernel' = copy-engine stream of FFN layers; peak = pinned 1 GiB H2D "
-                             "measured in this run"},
+                     "note": "dominant 'kernel' = copy-engine stream of the streamed layer units (XC4-encoded "
+                             "bytes when codec=xc4); peak = pinned 1 GiB H2D measured in this run"},
         "roofline_tokens_per_s": roof, "frac_of_roofline": value / roof if roof else None,
+        "raw_roofline_tokens_per_s": roof_raw,
+        "note_roofline": "roofline_tokens_per_s uses the bytes that crossed the link; raw_roofline_tokens_per_s "
+                         "the same rounds if the layers crossed uncompressed (the reference's ffn_bytes)",
+        "codec_kernel": codec_k,
         "kernel_roofline": kern,
         "clocks": clk,
         "gpu_launches": launches["kernels"],

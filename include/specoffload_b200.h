@@ -177,6 +177,49 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
 int so_stream_layer(void* slot, const void* pinned_src, size_t bytes, size_t chunk,
                     void* stream, void* done_event);
 
+/* ---- K9: XC4 lossless exponent-coded weight units ------------------------
+ * Same streamed bytes' *meaning* as so_stream_layer (the modeled `ffn_load`,
+ * simulator.py:172-176; ffn_bytes / c2g_bandwidth, costmodel.py:74), fewer
+ * bytes on the link: sign+mantissa byte + 4-bit exponent code per bf16
+ * weight, escapes in a side stream (format: csrc/wcodec.cu).  Decoding is
+ * bit-exact.  A unit = this header | u64 frame_off[n_frames+1] | frames. */
+typedef struct so_xc4_header {
+  uint32_t magic;          /* "XC41" */
+  uint32_t version;        /* 1 */
+  uint64_t n_elems;        /* bf16 weights in the unit (multiple of 16) */
+  uint32_t frame_elems;    /* elements per frame (multiple of 4096) */
+  uint32_t n_frames;
+  uint8_t exp_of_code[16]; /* code → exponent byte; code 15 = escape */
+  uint64_t total_bytes;    /* encoded unit size */
+  uint64_t n_escapes;
+  uint8_t reserved[8];
+} so_xc4_header;
+
+/* Device scratch for so_xc4_encode, and an upper bound of the encoded size. */
+size_t so_xc4_scratch_bytes(uint64_t n_elems, uint32_t frame_elems);
+size_t so_xc4_bound(uint64_t n_elems, uint32_t frame_elems);
+/* Encode `n_elems` bf16 weights (device) into `dst` (device, 16-B aligned).
+ * dst == NULL → size query: *out_bytes = encoded size.  Synchronises
+ * `stream` (setup-time call, not a hot-path one). */
+int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, void* dst, size_t dst_cap,
+                  void* scratch, uint64_t* out_bytes, so_xc4_header* out_header, void* stream);
+/* Decode frames [frame_begin, frame_end) of a unit whose bytes sit at
+ * unit_dev (device) into dst (the unit's full bf16 output; frame f lands at
+ * element f·frame_elems).  unit_host = a host copy of at least the header and
+ * frame table (the streamed unit in pinned memory). */
+int so_xc4_decode(const void* unit_host, const void* unit_dev, uint32_t frame_begin, uint32_t frame_end,
+                  void* dst, void* stream);
+/* K1 over XC4: per frame, H2D copy of the encoded frame (pinned → ring slot,
+ * copy stream) then its decode into `slot` (decode stream).  ring_events =
+ * 2·ring_slots caller-created events (copied, consumed) per ring slot;
+ * *ring_cursor counts frames across calls.  The decode stream waits on
+ * slot_free_event (may be NULL) before writing the slot and records
+ * done_event after the last frame. */
+int so_xc4_stream(void* slot, const void* pinned_unit, uint32_t frame_begin, uint32_t frame_end,
+                  void* ring, size_t ring_slot_bytes, int ring_slots, void* const* ring_events,
+                  uint64_t* ring_cursor, void* copy_stream, void* decode_stream, void* slot_free_event,
+                  void* done_event);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,139 @@
+/* ORACLE — test infrastructure only.  Scalar C restatement of the XC4
+ * weight-unit format (paper_2505_10259_b200/csrc/wcodec.cu, declared in
+ * include/specoffload_b200.h) used to pin the GPU encoder byte for byte and
+ * the GPU decoder bit for bit.
+ *
+ * What the format must preserve is the reference's streamed payload: the
+ * bytes of one FFN layer moved host → GPU once per pass (placement.py:260-283
+ * prefetch ops, costmodel.py:74 ffn_bytes / c2g_bandwidth).  decode(encode(w))
+ * == w for every bf16 bit pattern (NaN, Inf, ±0, subnormals included) is the
+ * size-independent property the tests check at full size.
+ *
+ * Normative rules restated here:
+ *   code table  exponents sorted by (count desc, exponent asc); the first
+ *               min(15, distinct) get codes 0..; other table entries 0;
+ *               code 15 = escape (raw exponent byte in the side stream)
+ *   frame       sm u8[m] | ec u8[m/2] (element 2j → low nibble of byte j) |
+ *               pad to 16 | eo i32[nb+1] (escapes before each 4096-block) |
+ *               esc u8[frame escapes] | zero pad to 256
+ *   unit        64-B header | u64 frame_off[nf+1] | zero pad to 256 | frames
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define XC4_BLOCK 4096u
+#define XC4_MAGIC 0x31344358u
+
+typedef struct {
+  uint32_t magic, version;
+  uint64_t n_elems;
+  uint32_t frame_elems, n_frames;
+  uint8_t exp_of_code[16];
+  uint64_t total_bytes, n_escapes;
+  uint8_t reserved[8];
+} xc4_header;
+
+static uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+static void geom(uint64_t m, uint64_t* off_eo, uint64_t* off_esc) {
+  *off_eo = up(m + m / 2, 16);
+  *off_esc = *off_eo + 4 * ((m + XC4_BLOCK - 1) / XC4_BLOCK + 1);
+}
+
+static uint8_t expo(uint16_t v) { return (uint8_t)((v >> 7) & 0xff); }
+
+/* returns 0 on success, -2 on bad geometry, -3 if cap is too small (out_bytes
+ * still set); dst == NULL → size query */
+int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst, uint64_t cap, uint64_t* out_bytes) {
+  if (n == 0 || n % 16 || F < XC4_BLOCK || F % XC4_BLOCK) return -2;
+  uint64_t hist[256] = {0};
+  for (uint64_t i = 0; i < n; ++i) hist[expo(src[i])]++;
+  xc4_header h;
+  memset(&h, 0, sizeof h);
+  uint8_t code[256];
+  memset(code, 15, sizeof code);
+  int taken[256] = {0};
+  for (int c = 0; c < 15; ++c) {
+    int best = -1;
+    for (int x = 0; x < 256; ++x)
+      if (!taken[x] && hist[x] && (best < 0 || hist[x] > hist[best])) best = x;
+    if (best < 0) break;
+    taken[best] = 1;
+    h.exp_of_code[c] = (uint8_t)best;
+    code[best] = (uint8_t)c;
+  }
+  const uint64_t nf = (n + F - 1) / F;
+  uint64_t* off = (uint64_t*)calloc(nf + 1, 8);
+  uint64_t pos = up(sizeof(xc4_header) + 8 * (nf + 1), 256), esc_total = 0;
+  for (uint64_t f = 0; f < nf; ++f) {
+    const uint64_t e0 = f * F, m = (n - e0 < F) ? n - e0 : F;
+    uint64_t esc = 0, oe, os;
+    for (uint64_t i = 0; i < m; ++i) esc += code[expo(src[e0 + i])] == 15;
+    geom(m, &oe, &os);
+    off[f] = pos;
+    pos += up(os + esc, 256);
+    esc_total += esc;
+  }
+  off[nf] = pos;
+  *out_bytes = pos;
+  if (!dst) {
+    free(off);
+    return 0;
+  }
+  if (cap < pos) {
+    free(off);
+    return -3;
+  }
+  memset(dst, 0, pos);
+  h.magic = XC4_MAGIC;
+  h.version = 1;
+  h.n_elems = n;
+  h.frame_elems = F;
+  h.n_frames = (uint32_t)nf;
+  h.total_bytes = pos;
+  h.n_escapes = esc_total;
+  memcpy(dst, &h, sizeof h);
+  memcpy(dst + sizeof h, off, 8 * (nf + 1));
+  for (uint64_t f = 0; f < nf; ++f) {
+    const uint64_t e0 = f * F, m = (n - e0 < F) ? n - e0 : F;
+    uint64_t oe, os;
+    geom(m, &oe, &os);
+    uint8_t* fr = dst + off[f];
+    int32_t* eo = (int32_t*)(fr + oe);
+    int32_t k = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint16_t v = src[e0 + i];
+      if (i % XC4_BLOCK == 0) eo[i / XC4_BLOCK] = k;
+      fr[i] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
+      const uint8_t c = code[expo(v)];
+      fr[m + i / 2] |= (uint8_t)(c << (4 * (i & 1)));
+      if (c == 15) fr[os + k++] = expo(v);
+    }
+    eo[(m + XC4_BLOCK - 1) / XC4_BLOCK] = k;
+  }
+  free(off);
+  return 0;
+}
+
+/* decode a whole unit; returns 0, or -2 on a malformed header */
+int oracle_xc4_decode(const uint8_t* unit, uint16_t* dst) {
+  xc4_header h;
+  memcpy(&h, unit, sizeof h);
+  if (h.magic != XC4_MAGIC || h.version != 1) return -2;
+  const uint64_t* off = (const uint64_t*)(unit + sizeof h);
+  for (uint64_t f = 0; f < h.n_frames; ++f) {
+    const uint64_t e0 = f * h.frame_elems, m = (h.n_elems - e0 < h.frame_elems) ? h.n_elems - e0 : h.frame_elems;
+    uint64_t oe, os;
+    geom(m, &oe, &os);
+    const uint8_t* fr = unit + off[f];
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint8_t sm = fr[i];
+      const uint8_t c = (fr[m + i / 2] >> (4 * (i & 1))) & 0xf;
+      const uint8_t e = c == 15 ? fr[os + k++] : h.exp_of_code[c];
+      dst[e0 + i] = (uint16_t)(((sm & 0x80) << 8) | (e << 7) | (sm & 0x7f));
+    }
+  }
+  return 0;
+}

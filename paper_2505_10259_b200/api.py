@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import torch
 
+from . import codec as C
 from . import weights as W
 from .config import ModelArch
 from .engine import Engine
@@ -20,33 +21,43 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  draft_weights: dict | None = None, device="cuda:0", stream_layers=None, n_slots: int = 2,
                  seed: int = 0, trace: bool = True, page_size: int = 16, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
-                 shared_store: SharedHostStore | None = None, stream_attn: bool = False) -> Engine:
+                 shared_store: SharedHostStore | None = None, stream_attn: bool = False,
+                 codec: str = "none") -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
     all of them — the fully offloaded configuration).  With ``world > 1`` the
     streamed layers live once in ``shared_store`` and each rank pulls its
-    1/N slice, reassembled by an NCCL all-gather."""
+    1/N slice, reassembled by an NCCL all-gather.
+    ``codec="xc4"`` keeps the streamed units XC4-encoded in host DRAM (K9:
+    0.75 of the bytes cross the link, decoded bit-exactly on the GPU)."""
+    if codec not in ("none", "xc4"):
+        raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
     if stream_layers is None:
         stream_layers = set(range(target_arch.n_layer))
     stream_layers = set(stream_layers)
+    enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
     if target_weights is not None:
-        tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn)
+        tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc)
     elif shared_store is not None:
-        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=shared_store.write_slice,
-                         stream_attn=stream_attn)
+        sink = shared_store.write_coded if enc is not None else shared_store.write_slice
+        tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=sink,
+                         stream_attn=stream_attn, encoder=enc)
     else:
         store = host_store or HostStore()
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc,
-                         stream_attn=stream_attn)
+                         stream_attn=stream_attn, encoder=enc)
+    if enc is not None:
+        enc.release()
+        torch.cuda.empty_cache()  # hand the encoder's staging back before KV / workspaces are sized
     if draft_weights is not None:
         dw = W.from_logical(draft_arch, draft_weights, dev)
     else:
         dw = W.synthetic(draft_arch, dev, seed=seed + 1)
     _, ffn_bytes = W.unit_layout(target_arch, stream_attn)  # bytes of one streamed layer unit
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
-    host = {li: t.view(torch.uint8) for li, t in tw.host_ffn.items()}
+    host = {li: t if isinstance(t, C.XC4Unit) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
                              chunk_bytes=chunk_bytes, rank=rank, world=world, group=group) if host else None
     target = TargetModel(tw, dev, streamer)

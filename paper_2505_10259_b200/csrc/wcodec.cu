@@ -1,0 +1,526 @@
+// K9 — XC4: lossless exponent-coded transport of bf16 weight units.
+//
+// The offloaded decode round is bound by the host link: every streamed FFN
+// layer crosses PCIe once per verification pass (costmodel.py:74,
+// ffn_bytes / c2g_bandwidth).  A bf16 weight is sign(1) ·
+// exponent(8) · mantissa(7), and the exponents of a trained (or N(0, σ²)
+// initialised) matrix crowd into a few binades.  XC4 keeps sign+mantissa as
+// one raw byte and replaces the exponent by a 4-bit code: codes 0..14 name the
+// unit's 15 most frequent exponents, code 15 escapes to a raw exponent byte in
+// a side stream.  12 bits per weight instead of 16 (0.75 of the bytes on the
+// link) and the decoded bytes are bit-identical to the source, so every
+// kernel downstream sees exactly the reference's weights.
+//
+// Unit layout (all offsets from the unit start; so_xc4_header in the header):
+//   header (64 B) | frame_off u64[n_frames+1] | frames, each 256-B aligned.
+// Frame of m elements (nb = ceil(m/4096) blocks of 4096):
+//   sm  u8[m]       (sign << 7) | mantissa           byte i = element i
+//   ec  u8[m/2]     4-bit codes, element 2j in the low nibble of byte j
+//   eo  i32[nb+1]   frame-local escape prefix per block (16-B aligned start)
+//   esc u8[...]     raw exponents of escaped elements, in element order
+// Code table rule (normative; oracle/csrc/xc4_oracle.c restates it): the
+// exponents present in the unit sorted by (count desc, exponent asc); the
+// first ≤15 get codes 0.., unused table entries are 0.
+//
+// Decode (HBM-bound: 1.5 B read + 2 B written per weight): one CTA of 256
+// threads per 4096-element block, 16 weights per thread; the exponent lookup
+// is two PRMT byte permutes over the register-resident table plus a select,
+// and a block-wide scan runs only when the block holds an escape.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBlock = 4096;   // elements per decode CTA
+constexpr int kThreads = 256;  // 16 elements per thread
+constexpr uint32_t kMagic = 0x31344358u;  // "XC41"
+
+__host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct FrameGeom {
+  size_t off_eo, off_esc;  // byte offsets inside the frame
+};
+
+__host__ __device__ inline FrameGeom frame_geom(uint32_t m) {
+  FrameGeom g;
+  g.off_eo = align_up((size_t)m + m / 2, 16);
+  g.off_esc = g.off_eo + 4 * ((size_t)(m + kBlock - 1) / kBlock + 1);
+  return g;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// 4 exponents from 4 codes packed as nibbles of `s` (element k in nibble k)
+__device__ __forceinline__ uint32_t lookup4(uint32_t s, uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+  const uint32_t lo = prmt(t0, t1, s & 0x7777u);
+  const uint32_t hi = prmt(t2, t3, s & 0x7777u);
+  const uint32_t msk = prmt(0u, 0xffffffffu, (s >> 1) & 0x4444u);  // 0xff where code ≥ 8
+  return (hi & msk) | (lo & ~msk);
+}
+
+// two bf16 (elements k, k+1) from sign/mantissa bytes and exponent bytes
+// already spread into the 16-bit lanes of a u32
+__device__ __forceinline__ uint32_t assemble2(uint32_t s01, uint32_t e01) {
+  return ((s01 & 0x00800080u) << 8) | (e01 << 7) | (s01 & 0x007f007fu);
+}
+
+__device__ __forceinline__ int4 ld_nc16(const void* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// exclusive block scan of one int per thread (256 threads); returns the total
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kThreads / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kThreads / 32) s_warp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  total = s_warp[kThreads / 32 - 1];
+  const int before = warp ? s_warp[warp - 1] : 0;
+  return before + x - v;
+}
+
+__device__ __forceinline__ int count_escapes(uint64_t codes) {
+  // a nibble is 0xF iff all four of its bits are set
+  const uint64_t x = codes & (codes >> 1) & (codes >> 2) & (codes >> 3) & 0x1111111111111111ull;
+  return __popcll(x);
+}
+
+__global__ void __launch_bounds__(kThreads) xc4_decode_kernel(const uint8_t* __restrict__ frame, uint32_t m,
+                                                               uint32_t off_eo, uint32_t off_esc, uint32_t t0,
+                                                               uint32_t t1, uint32_t t2, uint32_t t3,
+                                                               uint16_t* __restrict__ dst) {
+  __shared__ int s_warp[kThreads / 32];
+  const uint32_t e0 = blockIdx.x * kBlock + threadIdx.x * 16;
+  const bool live = e0 < m;
+  int4 smv = make_int4(0, 0, 0, 0);
+  uint2 ecv = make_uint2(0xffffffffu, 0xffffffffu);  // dead lanes: treated as escapes, but counted as 0 below
+  if (live) {
+    smv = ld_nc16(frame + e0);
+    ecv = *reinterpret_cast<const uint2*>(frame + m + e0 / 2);
+  }
+  const uint64_t codes = ((uint64_t)ecv.y << 32) | ecv.x;
+  const int nesc = live ? count_escapes(codes) : 0;
+  const uint32_t sw[4] = {(uint32_t)smv.x, (uint32_t)smv.y, (uint32_t)smv.z, (uint32_t)smv.w};
+  uint32_t ex[4];
+  ex[0] = lookup4(ecv.x & 0xffffu, t0, t1, t2, t3);
+  ex[1] = lookup4(ecv.x >> 16, t0, t1, t2, t3);
+  ex[2] = lookup4(ecv.y & 0xffffu, t0, t1, t2, t3);
+  ex[3] = lookup4(ecv.y >> 16, t0, t1, t2, t3);
+  if (__syncthreads_or(nesc)) {  // rare: patch escaped exponents from the side stream
+    int total;
+    const int pre = block_exclusive_scan(nesc, s_warp, total);
+    if (nesc) {
+      const int32_t base = reinterpret_cast<const int32_t*>(frame + off_eo)[blockIdx.x];
+      const uint8_t* esc = frame + off_esc + base + pre;
+      int k = 0;
+#pragma unroll 1
+      for (int i = 0; i < 16; ++i) {
+        if (((codes >> (4 * i)) & 0xfu) == 0xfu) {
+          const uint32_t sh = 8 * (i & 3);
+          ex[i >> 2] = (ex[i >> 2] & ~(0xffu << sh)) | ((uint32_t)esc[k++] << sh);
+        }
+      }
+    }
+  }
+  if (!live) return;
+  uint32_t o[8];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    o[2 * w] = assemble2(prmt(sw[w], 0u, 0x5150u), prmt(ex[w], 0u, 0x5150u));
+    o[2 * w + 1] = assemble2(prmt(sw[w], 0u, 0x5352u), prmt(ex[w], 0u, 0x5352u));
+  }
+  int4* out = reinterpret_cast<int4*>(dst + e0);
+  out[0] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+  out[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
+}
+
+// ---------------------------------------------------------------- encoder ---
+
+__global__ void xc4_hist_kernel(const uint16_t* __restrict__ src, uint64_t n, unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t n8 = n / 8;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int4 v = ld_nc16(src + 8 * i);
+    const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      atomicAdd(&h[(w[k] >> 7) & 0xffu], 1u);
+      atomicAdd(&h[(w[k] >> 23) & 0xffu], 1u);
+    }
+  }
+  for (uint64_t i = n8 * 8 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[(src[i] >> 7) & 0xffu], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+// per 4096-block escape counts over the whole unit (frames hold whole blocks)
+__global__ void __launch_bounds__(kThreads) xc4_count_kernel(const uint16_t* __restrict__ src, uint64_t n,
+                                                              const uint8_t* __restrict__ code_of_exp,
+                                                              int32_t* __restrict__ cnt) {
+  __shared__ uint8_t cx[256];
+  cx[threadIdx.x] = code_of_exp[threadIdx.x];
+  __syncthreads();
+  const uint64_t e0 = (uint64_t)blockIdx.x * kBlock + threadIdx.x * 16;
+  int c = 0;
+  if (e0 < n) {
+    const int4 a = ld_nc16(src + e0), b = ld_nc16(src + e0 + 8);
+    const uint32_t w[8] = {(uint32_t)a.x, (uint32_t)a.y, (uint32_t)a.z, (uint32_t)a.w,
+                           (uint32_t)b.x, (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += (cx[(w[k] >> 7) & 0xffu] == 15) + (cx[(w[k] >> 23) & 0xffu] == 15);
+  }
+  __shared__ int s_warp[kThreads / 32];
+  int total;
+  block_exclusive_scan(c, s_warp, total);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = total;
+}
+
+// per frame: exclusive prefix of its blocks' escape counts → eo[f][0..nb], tot[f]
+__global__ void xc4_scan_kernel(const int32_t* __restrict__ cnt, uint64_t n_blocks, uint32_t blocks_per_frame,
+                                int32_t* __restrict__ eo, unsigned long long* __restrict__ tot) {
+  const uint32_t f = blockIdx.x;
+  const uint64_t b0 = (uint64_t)f * blocks_per_frame;
+  const uint32_t nb = (uint32_t)(n_blocks - b0 < blocks_per_frame ? n_blocks - b0 : blocks_per_frame);
+  int32_t* out = eo + (uint64_t)f * (blocks_per_frame + 1);
+  if (threadIdx.x == 0) {  // frames hold ≤ 16384 blocks; a serial pass costs microseconds at setup
+    int64_t run = 0;
+    for (uint32_t i = 0; i < nb; ++i) {
+      out[i] = (int32_t)run;
+      run += cnt[b0 + i];
+    }
+    out[nb] = (int32_t)run;
+    tot[f] = (unsigned long long)run;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __restrict__ src, uint64_t n,
+                                                              const uint8_t* __restrict__ code_of_exp,
+                                                              const int32_t* __restrict__ eo,
+                                                              const unsigned long long* __restrict__ frame_off,
+                                                              uint32_t frame_elems, uint8_t* __restrict__ dst) {
+  __shared__ uint8_t cx[256];
+  __shared__ int s_warp[kThreads / 32];
+  cx[threadIdx.x] = code_of_exp[threadIdx.x];
+  __syncthreads();
+  const uint32_t bpf = frame_elems / kBlock;
+  const uint64_t gb = blockIdx.x;
+  const uint32_t f = (uint32_t)(gb / bpf), bl = (uint32_t)(gb % bpf);
+  const uint64_t f_e0 = (uint64_t)f * frame_elems;
+  const uint32_t m = (uint32_t)(n - f_e0 < frame_elems ? n - f_e0 : frame_elems);
+  const FrameGeom g = frame_geom(m);
+  uint8_t* fr = dst + frame_off[f];
+  const int32_t* feo = eo + (uint64_t)f * (bpf + 1);
+  const uint32_t e0 = bl * kBlock + threadIdx.x * 16;  // frame-local
+  uint8_t sm[16], ex[16];
+  uint64_t codes = 0;
+  int nesc = 0;
+  if (e0 < m) {
+    const int4 a = ld_nc16(src + f_e0 + e0), b = ld_nc16(src + f_e0 + e0 + 8);
+    const uint32_t w[8] = {(uint32_t)a.x, (uint32_t)a.y, (uint32_t)a.z, (uint32_t)a.w,
+                           (uint32_t)b.x, (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint16_t v = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+      ex[i] = (uint8_t)((v >> 7) & 0xffu);
+      sm[i] = (uint8_t)(((v >> 8) & 0x80u) | (v & 0x7fu));
+      const uint64_t c = cx[ex[i]];
+      codes |= c << (4 * i);
+      nesc += c == 15;
+    }
+    int4 smv;
+    uint32_t* sw = reinterpret_cast<uint32_t*>(&smv);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      sw[w] = sm[4 * w] | (sm[4 * w + 1] << 8) | (sm[4 * w + 2] << 16) | ((uint32_t)sm[4 * w + 3] << 24);
+    *reinterpret_cast<int4*>(fr + e0) = smv;
+    *reinterpret_cast<uint2*>(fr + m + e0 / 2) = make_uint2((uint32_t)codes, (uint32_t)(codes >> 32));
+  }
+  int total;
+  const int pre = block_exclusive_scan(nesc, s_warp, total);
+  if (nesc) {
+    uint8_t* esc = fr + g.off_esc + feo[bl] + pre;
+    int k = 0;
+    for (int i = 0; i < 16; ++i)
+      if (((codes >> (4 * i)) & 0xfu) == 0xfu) esc[k++] = ex[i];
+  }
+  if (threadIdx.x == 0) {
+    int32_t* out_eo = reinterpret_cast<int32_t*>(fr + g.off_eo);
+    out_eo[bl] = feo[bl];
+    if ((uint64_t)(bl + 1) * kBlock >= m) out_eo[bl + 1] = feo[bl + 1];
+  }
+}
+
+struct ScratchLayout {
+  size_t hist, code, cnt, eo, tot, foff, bytes;
+};
+
+ScratchLayout scratch_layout(uint64_t n, uint32_t frame_elems) {
+  const uint64_t nb = (n + kBlock - 1) / kBlock;
+  const uint64_t nf = (n + frame_elems - 1) / frame_elems;
+  const uint64_t bpf = frame_elems / kBlock;
+  ScratchLayout s;
+  s.hist = 0;
+  s.code = 256 * 8;
+  s.cnt = align_up(s.code + 256, 256);
+  s.eo = align_up(s.cnt + 4 * nb, 256);
+  s.tot = align_up(s.eo + 4 * nf * (bpf + 1), 256);
+  s.foff = align_up(s.tot + 8 * nf, 256);
+  s.bytes = align_up(s.foff + 8 * (nf + 1), 256);
+  return s;
+}
+
+bool valid_geometry(uint64_t n, uint32_t frame_elems) {
+  return n > 0 && n % 16 == 0 && frame_elems >= (uint32_t)kBlock && frame_elems % kBlock == 0;
+}
+
+size_t header_bytes(uint64_t nf) { return align_up(sizeof(so_xc4_header) + 8 * (nf + 1), 256); }
+
+}  // namespace
+
+extern "C" size_t so_xc4_scratch_bytes(uint64_t n_elems, uint32_t frame_elems) {
+  if (!valid_geometry(n_elems, frame_elems)) return 0;
+  return scratch_layout(n_elems, frame_elems).bytes;
+}
+
+extern "C" size_t so_xc4_bound(uint64_t n_elems, uint32_t frame_elems) {
+  if (!valid_geometry(n_elems, frame_elems)) return 0;
+  const uint64_t nf = (n_elems + frame_elems - 1) / frame_elems;
+  size_t b = header_bytes(nf);
+  for (uint64_t f = 0; f < nf; ++f) {
+    const uint32_t m = (uint32_t)std::min<uint64_t>(frame_elems, n_elems - f * frame_elems);
+    b += align_up(frame_geom(m).off_esc + m, 256);
+  }
+  return b;
+}
+
+extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, void* dst, size_t dst_cap,
+                             void* scratch, uint64_t* out_bytes, so_xc4_header* out_header, void* stream) {
+  SO_REQUIRE(src && scratch && out_bytes, SO_E_NULLPTR);
+  SO_REQUIRE(valid_geometry(n_elems, frame_elems), SO_E_SHAPE);
+  SO_REQUIRE(aligned16(src), SO_E_ALIGN);
+  cudaStream_t st = as_stream(stream);
+  const ScratchLayout L = scratch_layout(n_elems, frame_elems);
+  uint8_t* sc = reinterpret_cast<uint8_t*>(scratch);
+  auto* hist = reinterpret_cast<unsigned long long*>(sc + L.hist);
+  auto* code = sc + L.code;
+  auto* cnt = reinterpret_cast<int32_t*>(sc + L.cnt);
+  auto* eo = reinterpret_cast<int32_t*>(sc + L.eo);
+  auto* tot = reinterpret_cast<unsigned long long*>(sc + L.tot);
+  auto* foff = reinterpret_cast<unsigned long long*>(sc + L.foff);
+  const uint64_t nb = (n_elems + kBlock - 1) / kBlock;
+  const uint64_t nf = (n_elems + frame_elems - 1) / frame_elems;
+  const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
+  cudaError_t e;
+
+  // 1. exponent histogram → code table (host; normative tie-break)
+  if ((e = cudaMemsetAsync(hist, 0, 256 * 8, st)) != cudaSuccess) return (int)e;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  xc4_hist_kernel<<<sms * 4, 512, 0, st>>>(s16, n_elems, hist);
+  SO_CHECK_LAUNCH();
+  unsigned long long h[256];
+  if ((e = cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return (int)e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return (int)e;
+  so_xc4_header hdr;
+  memset(&hdr, 0, sizeof(hdr));
+  uint8_t code_of_exp[256];
+  memset(code_of_exp, 15, sizeof(code_of_exp));
+  {
+    bool used[256] = {false};
+    for (int c = 0; c < 15; ++c) {
+      int best = -1;
+      for (int x = 0; x < 256; ++x)
+        if (!used[x] && h[x] > 0 && (best < 0 || h[x] > h[best])) best = x;  // ties → lower exponent
+      if (best < 0) break;
+      used[best] = true;
+      hdr.exp_of_code[c] = (uint8_t)best;
+      code_of_exp[best] = (uint8_t)c;
+    }
+  }
+  if ((e = cudaMemcpyAsync(code, code_of_exp, 256, cudaMemcpyHostToDevice, st)) != cudaSuccess) return (int)e;
+
+  // 2. escapes per block, per-frame prefixes, frame sizes
+  xc4_count_kernel<<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, cnt);
+  SO_CHECK_LAUNCH();
+  xc4_scan_kernel<<<(unsigned)nf, 32, 0, st>>>(cnt, nb, frame_elems / kBlock, eo, tot);
+  SO_CHECK_LAUNCH();
+  unsigned long long* t_host = (unsigned long long*)malloc(8 * nf);
+  unsigned long long* off_host = (unsigned long long*)malloc(8 * (nf + 1));
+  if (!t_host || !off_host) {
+    free(t_host);
+    free(off_host);
+    return SO_E_SHAPE;
+  }
+  if ((e = cudaMemcpyAsync(t_host, tot, 8 * nf, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+    free(t_host);
+    free(off_host);
+    return (int)e;
+  }
+  size_t pos = header_bytes(nf);
+  uint64_t n_esc = 0;
+  for (uint64_t f = 0; f < nf; ++f) {
+    const uint32_t m = (uint32_t)std::min<uint64_t>(frame_elems, n_elems - f * frame_elems);
+    off_host[f] = pos;
+    pos += align_up(frame_geom(m).off_esc + t_host[f], 256);
+    n_esc += t_host[f];
+  }
+  off_host[nf] = pos;
+  free(t_host);
+  hdr.magic = kMagic;
+  hdr.version = 1;
+  hdr.n_elems = n_elems;
+  hdr.frame_elems = frame_elems;
+  hdr.n_frames = (uint32_t)nf;
+  hdr.total_bytes = pos;
+  hdr.n_escapes = n_esc;
+  *out_bytes = pos;
+  if (out_header) *out_header = hdr;
+  if (dst == nullptr) {
+    free(off_host);
+    return SO_OK;  // size query
+  }
+  if (dst_cap < pos) {
+    free(off_host);
+    return SO_E_SHAPE;
+  }
+  SO_REQUIRE(aligned16(dst), SO_E_ALIGN);
+
+  // 3. planes + escapes, then header + frame table (padding bytes zeroed)
+  uint8_t* d = reinterpret_cast<uint8_t*>(dst);
+  const size_t hb = header_bytes(nf);
+  uint8_t* head = (uint8_t*)calloc(1, hb);
+  if (!head) {
+    free(off_host);
+    return SO_E_SHAPE;
+  }
+  memcpy(head, &hdr, sizeof(hdr));
+  memcpy(head + sizeof(hdr), off_host, 8 * (nf + 1));
+  if ((e = cudaMemsetAsync(d, 0, pos, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(foff, off_host, 8 * (nf + 1), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d, head, hb, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+    free(off_host);
+    free(head);
+    return (int)e;
+  }
+  xc4_write_kernel<<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, eo, foff, frame_elems, d);
+  cudaError_t le = cudaGetLastError();
+  e = cudaStreamSynchronize(st);  // host staging buffers must outlive the copies
+  free(off_host);
+  free(head);
+  if (le != cudaSuccess) return (int)le;
+  return (int)e;
+}
+
+namespace {
+inline bool header_ok(const so_xc4_header* h) {
+  return h->magic == kMagic && h->version == 1 && valid_geometry(h->n_elems, h->frame_elems) &&
+         h->n_frames == (h->n_elems + h->frame_elems - 1) / h->frame_elems;
+}
+inline const uint64_t* frame_table(const void* unit_host) {
+  return reinterpret_cast<const uint64_t*>(reinterpret_cast<const uint8_t*>(unit_host) + sizeof(so_xc4_header));
+}
+inline void table_words(const so_xc4_header* h, uint32_t t[4]) {
+  for (int w = 0; w < 4; ++w)
+    t[w] = h->exp_of_code[4 * w] | (h->exp_of_code[4 * w + 1] << 8) | (h->exp_of_code[4 * w + 2] << 16) |
+           ((uint32_t)h->exp_of_code[4 * w + 3] << 24);
+}
+inline int launch_decode(const so_xc4_header* h, uint32_t f, const uint8_t* frame_dev, void* dst_unit,
+                         cudaStream_t st) {
+  const uint64_t e_begin = (uint64_t)f * h->frame_elems;
+  const uint32_t m = (uint32_t)std::min<uint64_t>(h->frame_elems, h->n_elems - e_begin);
+  const FrameGeom g = frame_geom(m);
+  uint32_t t[4];
+  table_words(h, t);
+  xc4_decode_kernel<<<(m + kBlock - 1) / kBlock, kThreads, 0, st>>>(
+      frame_dev, m, (uint32_t)g.off_eo, (uint32_t)g.off_esc, t[0], t[1], t[2], t[3],
+      reinterpret_cast<uint16_t*>(dst_unit) + e_begin);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+}  // namespace
+
+extern "C" int so_xc4_decode(const void* unit_host, const void* unit_dev, uint32_t frame_begin, uint32_t frame_end,
+                             void* dst, void* stream) {
+  SO_REQUIRE(unit_host && unit_dev && dst, SO_E_NULLPTR);
+  const so_xc4_header* h = reinterpret_cast<const so_xc4_header*>(unit_host);
+  SO_REQUIRE(header_ok(h), SO_E_SHAPE);
+  SO_REQUIRE(frame_begin <= frame_end && frame_end <= h->n_frames, SO_E_SHAPE);
+  SO_REQUIRE(aligned16(unit_dev) && aligned16(dst), SO_E_ALIGN);
+  const uint64_t* off = frame_table(unit_host);
+  for (uint32_t f = frame_begin; f < frame_end; ++f) {
+    const int rc = launch_decode(h, f, reinterpret_cast<const uint8_t*>(unit_dev) + off[f], dst, as_stream(stream));
+    if (rc) return rc;
+  }
+  return SO_OK;
+}
+
+extern "C" int so_xc4_stream(void* slot, const void* pinned_unit, uint32_t frame_begin, uint32_t frame_end,
+                             void* ring, size_t ring_slot_bytes, int ring_slots, void* const* ring_events,
+                             uint64_t* ring_cursor, void* copy_stream, void* decode_stream, void* slot_free_event,
+                             void* done_event) {
+  SO_REQUIRE(slot && pinned_unit && ring && ring_events && ring_cursor && done_event, SO_E_NULLPTR);
+  SO_REQUIRE(ring_slots >= 1, SO_E_SHAPE);
+  const so_xc4_header* h = reinterpret_cast<const so_xc4_header*>(pinned_unit);
+  SO_REQUIRE(header_ok(h), SO_E_SHAPE);
+  SO_REQUIRE(frame_begin <= frame_end && frame_end <= h->n_frames, SO_E_SHAPE);
+  SO_REQUIRE(aligned16(slot) && aligned16(ring) && ring_slot_bytes % 256 == 0, SO_E_ALIGN);
+  const uint64_t* off = frame_table(pinned_unit);
+  cudaStream_t cs = as_stream(copy_stream), ds = as_stream(decode_stream);
+  cudaError_t e;
+  // the window slot is overwritten only after the compute released it; the
+  // link itself runs ahead, bounded by the ring
+  if (slot_free_event && (e = cudaStreamWaitEvent(ds, reinterpret_cast<cudaEvent_t>(slot_free_event), 0)) != cudaSuccess)
+    return (int)e;
+  for (uint32_t f = frame_begin; f < frame_end; ++f) {
+    const size_t bytes = off[f + 1] - off[f];
+    if (bytes > ring_slot_bytes) return SO_E_SHAPE;
+    const int r = (int)(*ring_cursor % (uint64_t)ring_slots);
+    cudaEvent_t copied = reinterpret_cast<cudaEvent_t>(ring_events[2 * r]);
+    cudaEvent_t consumed = reinterpret_cast<cudaEvent_t>(ring_events[2 * r + 1]);
+    uint8_t* rs = reinterpret_cast<uint8_t*>(ring) + (size_t)r * ring_slot_bytes;
+    if ((e = cudaStreamWaitEvent(cs, consumed, 0)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemcpyAsync(rs, reinterpret_cast<const uint8_t*>(pinned_unit) + off[f], bytes,
+                             cudaMemcpyHostToDevice, cs)) != cudaSuccess)
+      return (int)e;
+    if ((e = cudaEventRecord(copied, cs)) != cudaSuccess) return (int)e;
+    if ((e = cudaStreamWaitEvent(ds, copied, 0)) != cudaSuccess) return (int)e;
+    const int rc = launch_decode(h, f, rs, slot, ds);
+    if (rc) return rc;
+    if ((e = cudaEventRecord(consumed, ds)) != cudaSuccess) return (int)e;
+    ++*ring_cursor;
+  }
+  return (int)cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), ds);
+}

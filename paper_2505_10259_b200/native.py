@@ -60,6 +60,13 @@ _SIGNATURES = {
     "so_build_verify_tokens": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_gather_i32": (c_int, [_P, _P, c_int, _P, _P]),
     "so_scatter_i32": (c_int, [_P, _P, _P, c_int, _P]),
+    "so_xc4_scratch_bytes": (c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
+    "so_xc4_bound": (c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
+    "so_xc4_encode": (c_int, [_P, ctypes.c_uint64, ctypes.c_uint32, _P, c_size_t, _P,
+                              ctypes.POINTER(ctypes.c_uint64), _P, _P]),
+    "so_xc4_decode": (c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, _P, _P]),
+    "so_xc4_stream": (c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, _P, c_size_t, c_int, _P,
+                              ctypes.POINTER(ctypes.c_uint64), _P, _P, _P, _P]),
 }
 
 _PLUMBING = {"so_event_create", "so_event_destroy", "so_event_record", "so_stream_wait_event", "so_event_synchronize",
@@ -93,7 +100,7 @@ def exported_symbols() -> list[str]:
 
 # kernels (or copy-engine DMA batches) each entry point enqueues; summed into
 # ``launches`` so bench.py can report how many of our kernels ran
-_KERNELS_PER_CALL = {"so_router_top2": 3, "so_stream_layer": 0}
+_KERNELS_PER_CALL = {"so_router_top2": 3, "so_stream_layer": 0, "so_xc4_encode": 5}
 launches = {"kernels": 0, "copies": 0}
 _count_lock = threading.Lock()  # the verify and draft streams are enqueued from two threads
 
@@ -119,6 +126,8 @@ def _check(rc: int, what: str) -> None:
         with _count_lock:
             if what == "so_stream_layer":
                 launches["copies"] += 1
+            elif what in ("so_xc4_stream", "so_xc4_decode"):
+                pass  # counted per frame by the caller
             else:
                 launches["kernels"] += _KERNELS_PER_CALL.get(what, 1)
     if rc != 0:
@@ -327,3 +336,58 @@ def stream_layer(slot_ptr: int, host_ptr: int, nbytes: int, chunk: int, stream,
                  event: "Event | None" = None) -> None:
     ev = event.handle if event is not None else None
     _check(lib().so_stream_layer(slot_ptr, host_ptr, nbytes, chunk, _sp(stream), ev), "so_stream_layer")
+
+
+# ---------------------------------------------------------------- K9 ---
+
+class XC4Header(ctypes.Structure):
+    """so_xc4_header (include/specoffload_b200.h)."""
+
+    _fields_ = [("magic", ctypes.c_uint32), ("version", ctypes.c_uint32), ("n_elems", ctypes.c_uint64),
+                ("frame_elems", ctypes.c_uint32), ("n_frames", ctypes.c_uint32),
+                ("exp_of_code", ctypes.c_uint8 * 16), ("total_bytes", ctypes.c_uint64),
+                ("n_escapes", ctypes.c_uint64), ("reserved", ctypes.c_uint8 * 8)]
+
+
+assert ctypes.sizeof(XC4Header) == 64
+
+
+def xc4_scratch_bytes(n_elems: int, frame_elems: int) -> int:
+    return int(lib().so_xc4_scratch_bytes(n_elems, frame_elems))
+
+
+def xc4_bound(n_elems: int, frame_elems: int) -> int:
+    return int(lib().so_xc4_bound(n_elems, frame_elems))
+
+
+def xc4_encode(src, frame_elems: int, dst, scratch, stream=None) -> tuple[int, XC4Header]:
+    """Encode bf16 ``src`` (device) into ``dst`` (device uint8, or None for a
+    size query).  Returns (encoded bytes, header).  Synchronises the stream."""
+    assert src.dtype in (torch.bfloat16, torch.int16, torch.uint16) and src.is_cuda and src.is_contiguous()
+    n = ctypes.c_uint64()
+    h = XC4Header()
+    cap = dst.numel() if dst is not None else 0
+    _check(lib().so_xc4_encode(_ptr(src), src.numel(), frame_elems, _ptr(dst), cap, _ptr(scratch),
+                               ctypes.byref(n), ctypes.byref(h), _stream(stream)), "so_xc4_encode")
+    return int(n.value), h
+
+
+def xc4_decode(unit_host_ptr: int, unit_dev_ptr: int, frame_begin: int, frame_end: int, dst_ptr: int,
+               stream=None) -> None:
+    _check(lib().so_xc4_decode(unit_host_ptr, unit_dev_ptr, frame_begin, frame_end, dst_ptr,
+                               _sp(stream) if stream is not None else _stream(None)), "so_xc4_decode")
+    with _count_lock:
+        launches["kernels"] += frame_end - frame_begin
+
+
+def xc4_stream(slot_ptr: int, unit_ptr: int, frame_begin: int, frame_end: int, ring_ptr: int,
+               ring_slot_bytes: int, ring_events, cursor: "ctypes.c_uint64", copy_stream, decode_stream,
+               slot_free: "Event | None", done: "Event") -> None:
+    evs = (c_void_p * len(ring_events))(*[e.handle for e in ring_events])
+    _check(lib().so_xc4_stream(slot_ptr, unit_ptr, frame_begin, frame_end, ring_ptr, ring_slot_bytes,
+                               len(ring_events) // 2, evs, ctypes.byref(cursor), _sp(copy_stream),
+                               _sp(decode_stream), slot_free.handle if slot_free is not None else None,
+                               done.handle), "so_xc4_stream")
+    with _count_lock:
+        launches["kernels"] += frame_end - frame_begin
+        launches["copies"] += frame_end - frame_begin

@@ -57,6 +57,7 @@ class OffloadPlan:
     expected_tokens_per_round: float
     tokens_per_s: float
     stream_attn: bool = False  # attention projections streamed with each layer (H3)
+    stream_ratio: float = 1.0  # encoded / raw bytes of a streamed unit (K9 XC4 ≈ 0.75; 1 = raw)
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -112,9 +113,15 @@ def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str)
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
                  n_slots: int = 2, bs_candidates=None, page_size: int = 16, draft_kv_modes=("cached", "reprefill"),
-                 max_draft_chunk: int = 64, stream_attn_modes=(False, True)) -> OffloadPlan:
+                 max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
+                 ring_bytes: int = 0) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
-    maximise predicted decode tokens/s under both memory budgets."""
+    maximise predicted decode tokens/s under both memory budgets.
+
+    ``stream_ratio`` < 1: streamed units are kept XC4-encoded (K9) — host DRAM
+    and the link carry ratio × the layer bytes, HBM adds the ``ring_bytes``
+    staging ring and each pass pays the decode's HBM traffic (1.5 B read +
+    2 B written per weight)."""
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     best = None
@@ -125,7 +132,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
         # attention projections travel with the FFN and leave the resident set
         layer_bytes = unit_layout(target, stream_attn)[1]
         fixed = (resident_bytes(target, False) - (target.n_layer * attn_layer if stream_attn else 0)
-                 + resident_bytes(draft, True) + n_slots * layer_bytes)
+                 + resident_bytes(draft, True) + n_slots * layer_bytes + (ring_bytes if stream_ratio < 1 else 0))
+        host_unit = int(math.ceil(layer_bytes * stream_ratio))
         for bs in cands:
             bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
             kv = kv_bytes(target, draft, 2 * bs, max_len, page_size, None if mode == "cached" else bs_draft)
@@ -135,12 +143,14 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                 continue
             pinned = min(target.n_layer, int(free // layer_bytes))
             streamed = target.n_layer - pinned
-            if streamed * layer_bytes > host_budget:
+            if streamed * host_unit > host_budget:
                 continue
-            S = streamed * layer_bytes
+            S = streamed * host_unit
             t_stream = S / rates.h2d_bytes_per_s
             eff = rates.tensor_flops * rates.tensor_efficiency
             t_comp = (verify_flops(target, bs, n_cand, ctx_len) + draft_flops(draft, bs, n_cand, ctx_len, mode)) / eff
+            if stream_ratio < 1:
+                t_comp += streamed * layer_bytes * 1.75 / rates.hbm_bytes_per_s
             t_round = max(t_stream, t_comp) + rates.round_overhead_s
             tps = bs * e_tok / t_round
             if best is None or tps > best[0] * 1.001:
@@ -154,7 +164,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     stream_l = tuple(range(pinned, target.n_layer))
     return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if streamed else 0,
                        {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes},
-                       streamed * layer_bytes, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa)
+                       S, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

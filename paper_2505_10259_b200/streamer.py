@@ -22,6 +22,7 @@ import threading
 import torch
 
 from . import native
+from .codec import Cursor, XC4Unit
 from .errors import InsufficientTotalMemory
 
 
@@ -98,7 +99,8 @@ class SharedHostStore:
     link.  Layer ℓ lives at offset ℓ·layer_bytes.
     """
 
-    def __init__(self, name: str, layers: list[int], layer_bytes: int, rank: int, world: int, barrier=None):
+    def __init__(self, name: str, layers: list[int], layer_bytes: int, rank: int, world: int, barrier=None,
+                 coded: bool = False):
         self.layers = {li: i for i, li in enumerate(layers)}
         self.layer_bytes = layer_bytes
         self.rank, self.world = rank, world
@@ -116,8 +118,9 @@ class SharedHostStore:
         self._buf = (ctypes.c_uint8 * self.bytes).from_buffer(self._map)
         self.base = ctypes.addressof(self._buf)
         self._registered: list[int] = []
-        self.lo, self.hi = slice_bounds(layer_bytes, rank, world)
-        if torch.cuda.is_available():
+        self.coded = coded  # layer_bytes = capacity of one XC4 unit; slices are frame ranges
+        self.lo, self.hi = (0, 0) if coded else slice_bounds(layer_bytes, rank, world)
+        if torch.cuda.is_available() and not coded:
             for i in range(len(layers)):
                 addr = self.base + i * layer_bytes + self.lo
                 rc = torch.cuda.cudart().cudaHostRegister(addr, self.hi - self.lo, 0)
@@ -135,6 +138,31 @@ class SharedHostStore:
         flat = src.reshape(-1).view(torch.uint8)
         view[self.lo:self.hi].copy_(flat[self.lo:self.hi])
         return view
+
+    def write_coded(self, layer: int, enc: torch.Tensor) -> XC4Unit:
+        """Store an XC4-encoded unit (``enc``: its bytes, any device): every rank
+        writes the header and frame table, then only the frames it will move
+        over its own link, which it page-locks."""
+        nb = enc.numel()
+        if nb > self.layer_bytes:
+            raise InsufficientTotalMemory(f"XC4 unit of {nb} B exceeds the {self.layer_bytes} B store slot")
+        view = self.layer_view(layer)
+        h = native.XC4Header.from_buffer_copy(bytes(enc[:64].cpu().numpy()))
+        head = 64 + 8 * (int(h.n_frames) + 1)
+        view[:head].copy_(enc[:head])
+        u = XC4Unit.parse(view[:nb])
+        f0, f1 = u.frame_range(self.rank, self.world)
+        lo, hi = int(u.frame_off[f0]), int(u.frame_off[f1])
+        view[lo:hi].copy_(enc[lo:hi])
+        if torch.cuda.is_available():
+            base = self.base + self.layers[layer] * self.layer_bytes
+            a0, a1 = (base + lo) // 4096 * 4096, (base + hi + 4095) // 4096 * 4096
+            rc = torch.cuda.cudart().cudaHostRegister(a0, a1 - a0, 0)
+            if int(rc) != 0:
+                raise InsufficientTotalMemory(f"cudaHostRegister of {a1 - a0} B of frames failed ({int(rc)})")
+            self._registered.append(a0)
+        self.bytes_registered = getattr(self, "bytes_registered", 0) + (hi - lo)
+        return u
 
     def close(self, unlink: bool = False) -> None:
         for addr in self._registered:
@@ -168,10 +196,17 @@ class LayerStreamer:
     Resident layers return their HBM buffer and never touch the link.
     """
 
-    def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict[int, torch.Tensor],
+    RING_SLOTS = 4  # encoded frames in flight between the copy engine and the decoder (XC4 units)
+
+    def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict,
                  n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False,
                  rank: int = 0, world: int = 1, group=None):
         self.layer_bytes = layer_bytes
+        # host values are raw pinned uint8 tensors, or XC4Unit (K9: encoded
+        # frames cross the link and are decoded into the slot on the GPU)
+        self.coded = any(isinstance(v, XC4Unit) for v in host.values())
+        if self.coded and not all(isinstance(v, XC4Unit) for v in host.values()):
+            raise ValueError("streamed layers must be all raw or all XC4-encoded")
         self.resident = resident
         self.host = host
         self.streamed = [li for li in range(n_layer) if li in host]
@@ -190,25 +225,56 @@ class LayerStreamer:
         # event has handle 0, and record/wait on it silently no-op)
         self.loaded = [native.Event() for _ in range(self.n_slots)]
         self.free = [native.Event() for _ in range(self.n_slots)]
+        self.ring = None
+        if self.coded:
+            for u in host.values():
+                if u.raw_bytes != layer_bytes:
+                    raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
+            self.frames = {li: u.frame_range(rank, world) for li, u in host.items()}
+            self.ring_slot_bytes = (max(u.max_frame_bytes() for u in host.values()) + 255) // 256 * 256
+            self.ring = torch.empty(self.RING_SLOTS * self.ring_slot_bytes, dtype=torch.uint8, device=self.device)
+            self.ring_events = [native.Event() for _ in range(2 * self.RING_SLOTS)]
+            self.ring_cursor = Cursor(0)
+            # decode kernels jump ahead of the verify/draft kernels: they gate the next layer
+            self.decode_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.k_use = 0      # global index of the next streamed use
         self.k_issued = 0   # copies enqueued so far
-        self.bytes_issued = 0
+        self.bytes_issued = 0      # bytes moved over this rank's host link
+        self.raw_bytes_issued = 0  # decoded layer bytes those copies delivered
         self.trace = trace
         self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
 
     @property
     def window_bytes(self) -> int:
-        return self.n_slots * self.layer_bytes
+        return self.n_slots * self.layer_bytes + (self.ring.numel() if self.ring is not None else 0)
 
     def _issue(self, k: int) -> None:
         slot = k % self.n_slots
         layer = self.streamed[k % len(self.streamed)]
-        if k >= self.n_slots:
+        if k >= self.n_slots and not self.coded:  # coded: the decoder waits instead, the link runs ahead
             self.free[slot].wait(self.copy_stream)
         src = self.host[layer]
         start = None
         if self.trace:
             start = native.Event(timing=True).record(self.copy_stream)
+        if self.coded:
+            unit = src
+            f0, f1 = self.frames[layer]
+            done = self.loaded[slot] if self.world == 1 else self.copied[slot]
+            native.xc4_stream(self.slots[slot].data_ptr(), unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
+                              self.ring_slot_bytes, self.ring_events, self.ring_cursor, self.copy_stream,
+                              self.decode_stream, self.free[slot] if k >= self.n_slots else None, done)
+            if self.world > 1:
+                self.copied[slot].wait(self.comm_stream)
+                with torch.cuda.stream(self.comm_stream):
+                    gather_layer(self.slots[slot], self.rank, self.world, self.group)
+                self.loaded[slot].record(self.comm_stream)
+            self.bytes_issued += unit.frame_bytes(f0, f1)
+            self.raw_bytes_issued += self.hi - self.lo
+            if self.trace:
+                end_stream = self.decode_stream if self.world == 1 else self.comm_stream
+                self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream)))
+            return
         if self.world == 1:
             native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
                                 self.copy_stream, self.loaded[slot])
@@ -223,6 +289,7 @@ class LayerStreamer:
             end_stream = self.copy_stream if self.world == 1 else self.comm_stream
             self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream)))
         self.bytes_issued += self.hi - self.lo
+        self.raw_bytes_issued += self.hi - self.lo
 
     def _ensure_issued(self, upto: int) -> None:
         while self.k_issued <= upto:

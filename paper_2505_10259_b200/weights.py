@@ -19,6 +19,7 @@ import dataclasses
 import numpy as np
 import torch
 
+from . import codec
 from .config import ModelArch
 
 SWIGLU_BLOCK = 64
@@ -88,7 +89,7 @@ class ModelWeights:
     final_norm: torch.Tensor
     lm_head: torch.Tensor
     layers: list[LayerWeights]
-    host_ffn: dict[int, torch.Tensor]  # layer -> pinned host buffer (streamed layers)
+    host_ffn: dict  # layer -> pinned host buffer, or codec.XC4Unit (streamed layers)
 
     def resident_bytes(self) -> int:
         n = self.embed.numel() + self.final_norm.numel() + self.lm_head.numel()
@@ -100,8 +101,9 @@ class ModelWeights:
 
 
 def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset(),
-                 stream_attn: bool = False) -> ModelWeights:
-    """Build device weights from logical (HF-shaped) arrays — numpy or torch."""
+                 stream_attn: bool = False, encoder=None) -> ModelWeights:
+    """Build device weights from logical (HF-shaped) arrays — numpy or torch.
+    With ``encoder`` (codec.Encoder) the streamed units are kept XC4-encoded."""
     dev = torch.device(device)
     layers = []
     host = {}
@@ -113,7 +115,10 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
             if stream_attn:
                 packed = torch.cat([wqkv.reshape(-1), wo.reshape(-1), packed])
                 wqkv = wo = None
-            host[li] = packed.pin_memory() if dev.type == "cuda" else packed
+            if encoder is not None:
+                host[li] = codec.encode_to_host(packed.to(dev), encoder)
+            else:
+                host[li] = packed.pin_memory() if dev.type == "cuda" else packed
             ffn = None
         else:
             ffn = packed.to(dev)
@@ -130,14 +135,17 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 
 
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
-              host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False) -> ModelWeights:
+              host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False,
+              encoder=None) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
     time and copied into pinned host buffers from ``host_alloc(nbytes)`` — or
     handed to ``host_sink(layer, tensor) -> host view`` (multi-GPU: each rank
     writes only its slice of the shared store; every rank draws the same
-    weights from the same seed).
+    weights from the same seed).  With ``encoder`` (codec.Encoder) streamed
+    units are XC4-encoded on the GPU first and the host keeps the encoding
+    (the sink then receives the encoded device bytes).
     """
     dev = torch.device(device)
     g = torch.Generator(device=dev)
@@ -156,7 +164,12 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
         streamed = li in stream_layers
         with_attn = streamed and stream_attn
         unit = randn((ffn_bytes + (attn_elems(arch) * 2 if with_attn else 0)) // 2)
-        if streamed and host_sink is not None:
+        if streamed and encoder is not None:
+            if host_sink is not None:
+                host[li] = host_sink(li, encoder.encode(unit)[0])
+            else:
+                host[li] = codec.encode_to_host(unit, encoder, host_alloc)
+        elif streamed and host_sink is not None:
             host[li] = host_sink(li, unit).view(torch.bfloat16)
         elif streamed:
             buf = host_alloc(unit.numel() * 2) if host_alloc is not None else torch.empty(

@@ -183,3 +183,15 @@ def test_run_decoding_trace_contracts(pair):
             assert b.start >= a.end - 1e-6
     loads = [e for e in res.trace if e.label == "ffn_load"]
     assert loads, "streamed layers must show copy-engine events"
+
+
+def test_generate_identical_with_xc4_streamed_units(pair):
+    """K9 is lossless: the same prompts through XC4-encoded streamed layers give
+    exactly the tokens of the raw-byte streamer."""
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=5)
+    pol = Policy(8, 4, 4, 4)
+    raw = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3}).generate(prompts, 12, pol)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3}, codec="xc4")
+    assert eng.target.streamer.coded
+    assert eng.generate(prompts, 12, pol) == raw
