@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget (0 = MemAvailable − 14 GB)")
     ap.add_argument("--hbm-gb", type=float, default=0.0, help="HBM budget (0 = device; 8x7b config: 24 GiB cap)")
     ap.add_argument("--slots", type=int, default=2)
-    ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill"), default="auto",
+    ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill", "mixed"), default="auto",
                     help="draft KV policy (auto = planner)")
     ap.add_argument("--layers", type=int, default=0,
                     help="profiling only: override the target's layer count (same per-layer shapes)")
@@ -206,7 +206,7 @@ def main():
     from paper_2505_10259_b200.planner_b200 import B200Rates
 
     rates = B200Rates(h2d_bytes_per_s=link, hbm_bytes_per_s=peaks["hbm_gbs"] * 1e9)
-    modes = ("cached", "reprefill") if args.draft_kv == "auto" else (args.draft_kv,)
+    modes = ("cached", "reprefill", "mixed") if args.draft_kv == "auto" else (args.draft_kv,)
     ratio, ring = 1.0, 0
     if args.codec == "xc4":
         # encoded/raw ratio of this weight distribution, probed on one 64 Mi-weight sample
@@ -243,7 +243,7 @@ def main():
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
-                        bs_draft=plan.bs_draft, draft_kv=plan.draft_kv)
+                        bs_draft=plan.bs_draft, draft_kv=plan.draft_kv, draft_cached=plan.draft_cached)
     eng.synthetic_context(s, args.ctx, max_new, seed=rank)
     eng.first_draft(s)
     setup_s = time.perf_counter() - t_setup
@@ -381,7 +381,8 @@ def main():
                      n_cand=args.n_cand)
         torch.cuda.synchronize(device)
         g0 = time.perf_counter()
-        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=plan.draft_kv)
+        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=plan.draft_kv,
+                            draft_cached=min(plan.draft_cached, pol.bs_decoding) if plan.draft_kv == "mixed" else None)
         g_wall = time.perf_counter() - g0
         assert all(len(t) == args.e2e_new for t in toks)
         gs = eng.last_session
@@ -414,7 +415,8 @@ def main():
         "dtype": "bf16", "data": "synthetic (random-init weights, random prompt KV, forced acceptance p)",
         "config": {"workload": f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM",
                    "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
-                   "draft_kv": plan.draft_kv, "bs_draft": plan.bs_draft, "acceptance_p": args.p,
+                   "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
+                   "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,

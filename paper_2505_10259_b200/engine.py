@@ -103,7 +103,7 @@ class DecodeSession:
 
     def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
                  mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int,
-                 draft_kv: str = "cached"):
+                 draft_kv: str = "cached", draft_cached: int | None = None):
         self.e = engine
         self.n_seq = n_seq
         self.n_cand = n_cand
@@ -112,20 +112,40 @@ class DecodeSession:
         self.temperature = temperature
         self.forced_p = forced_p
         self.bs_draft = bs_draft
-        if draft_kv not in ("cached", "reprefill"):
-            raise ValueError(f"draft_kv must be 'cached' or 'reprefill', got {draft_kv!r}")
+        if draft_kv not in ("cached", "reprefill", "mixed"):
+            raise ValueError(f"draft_kv must be 'cached', 'reprefill' or 'mixed', got {draft_kv!r}")
+        if draft_kv == "mixed" and draft_cached is None:
+            raise ValueError("draft_kv='mixed' needs draft_cached (cached sequences per batch)")
         self.draft_kv = draft_kv
         self.batches = [_Batch(0, min(bs_decoding, n_seq)), _Batch(min(bs_decoding, n_seq), n_seq)]
         dev = engine.device
         self.tkv = PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size)
-        # cached: one persistent draft KV row per sequence.  reprefill (the
-        # paper's draft, PAPER.md:511-519 / costmodel.py:53-57,132-137): the
-        # draft re-reads the whole context each round into a scratch cache
-        # sized for one bs_draft chunk, so HBM goes to a larger batch instead.
-        self.dkv = PagedKVCache(engine.draft.arch, n_seq if draft_kv == "cached" else bs_draft, max_len, dev,
-                                engine.page_size)
+        # Draft KV policy (planner choice):
+        #   cached    one persistent draft KV row per sequence;
+        #   reprefill the paper's draft (costmodel.py:53-57,
+        #             132-137): the whole context is re-read each round into a
+        #             scratch cache sized for one bs_draft chunk, so HBM goes to
+        #             a larger batch instead;
+        #   mixed     the first ``draft_cached`` sequences of each batch keep a
+        #             row, the rest re-prefill — HBM and tensor time traded
+        #             sequence by sequence until both bind.
+        if draft_kv == "cached":
+            self.n_cached = [b.n for b in self.batches]
+        elif draft_kv == "reprefill":
+            self.n_cached = [0, 0]
+        else:
+            self.n_cached = [min(int(draft_cached), b.n) for b in self.batches]
+        self.drow = np.full(n_seq, -1, np.int64)   # sequence → persistent draft KV row
+        r = 0
+        for b, kc in zip(self.batches, self.n_cached):
+            self.drow[b.lo:b.lo + kc] = np.arange(r, r + kc)
+            r += kc
+        self.scratch_row0 = r
+        self.any_reprefill = any(kc < b.n for b, kc in zip(self.batches, self.n_cached))
+        self.dkv = PagedKVCache(engine.draft.arch, max(1, r + (bs_draft if self.any_reprefill else 0)), max_len,
+                                dev, engine.page_size)
         # token history (position-indexed) for the re-prefilling draft
-        self.hist = torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev) if draft_kv == "reprefill" else None
+        self.hist = torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev) if self.any_reprefill else None
         self.max_len = max_len
         self.ctx = np.zeros(n_seq, np.int64)
         self.t_last = np.zeros(n_seq, np.int32)
@@ -212,9 +232,10 @@ class Engine:
 
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
-                    bs_draft: int | None = None, draft_kv: str = "cached") -> DecodeSession:
+                    bs_draft: int | None = None, draft_kv: str = "cached",
+                    draft_cached: int | None = None) -> DecodeSession:
         return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
-                             bs_draft or bs_decoding, draft_kv)
+                             bs_draft or bs_decoding, draft_kv, draft_cached)
 
     def _hist_write(self, s: DecodeSession, seqs, positions, tokens, stream) -> None:
         """Record committed tokens in the device-side history (reprefill drafts)."""
@@ -241,30 +262,35 @@ class Engine:
             cur.append(i)
             cur_tok += int(L)
         groups.append(cur)
-        models = [(self.target, s.tkv, self.tgt_stream)]
-        if s.draft_kv == "cached":
-            models.append((self.draft, s.dkv, self.drf_stream))
-        else:  # the re-prefilling draft only needs the prompt tokens
+        models = [(self.target, s.tkv, self.tgt_stream, groups, np.arange(s.n_seq))]
+        if s.any_reprefill:  # the re-prefilling draft only needs the prompt tokens
             seqs = np.concatenate([np.full(L, i) for i, L in enumerate(lens)])
             pos = np.concatenate([np.arange(L) for L in lens])
             self._hist_write(s, seqs, pos, np.concatenate([np.asarray(p, np.int32) for p in prompts]),
                              self.drf_stream)
-        for model, kv, stream in models:
+        # sequences with a persistent draft KV row prefill the draft too (rows
+        # are consecutive in sequence order, so a group maps to a row range)
+        dgroups = [[i for i in g if s.drow[i] >= 0] for g in groups]
+        dgroups = [g for g in dgroups if g]
+        if dgroups:
+            models.append((self.draft, s.dkv, self.drf_stream, dgroups, s.drow))
+        for model, kv, stream, mgroups, rowmap in models:
             chunks = []
             row0 = 0
             last = []
-            for g in groups:
+            for g in mgroups:
                 toks = np.concatenate([np.asarray(prompts[i], np.int32) for i in g])
                 pos = np.concatenate([np.arange(lens[i]) for i in g])
-                seq = np.concatenate([np.full(lens[i], i) for i in g])
+                seq = np.concatenate([np.full(lens[i], rowmap[i]) for i in g])
                 qs = np.concatenate([[0], np.cumsum(lens[g])]).astype(np.int32)
                 meta = self._up(np.concatenate([toks, pos.astype(np.int32), kv.slots(seq, pos), qs,
                                                 np.zeros(len(g), np.int32)]), stream)
                 T = len(toks)
                 o = 0
+                r0, r1 = int(rowmap[g[0]]), int(rowmap[g[-1]])
                 fb = ForwardBatch(meta[o:o + T], meta[o + T:o + 2 * T], meta[o + 2 * T:o + 3 * T],
                                   meta[o + 3 * T:o + 3 * T + len(g) + 1], meta[o + 3 * T + len(g) + 1:],
-                                  kv.block_table[g[0]:g[-1] + 1], len(g), int(lens[g].max()), None, row0)
+                                  kv.block_table[r0:r1 + 1], len(g), int(lens[g].max()), None, row0)
                 last.extend(row0 + qs[1:] - 1)
                 chunks.append(fb)
                 row0 += T
@@ -326,16 +352,20 @@ class Engine:
         tr = self.tracer
         ev0 = tr.mark(st)
         u_all = input_uniforms(s.seed, rnd, bi, 0, (b.n, n)) if s.mode == "sample" else None
-        for c_lo in range(0, b.n, s.bs_draft):
-            c_hi = min(b.n, c_lo + s.bs_draft)
+        kc = s.n_cached[bi]
+        cstep = s.bs_draft if s.draft_kv == "cached" else max(kc, 1)
+        chunks = [(lo, min(kc, lo + cstep), True) for lo in range(0, kc, cstep)]
+        chunks += [(lo, min(b.n, lo + s.bs_draft), False) for lo in range(kc, b.n, s.bs_draft)]
+        for c_lo, c_hi, cached in chunks:
             cm = c_hi - c_lo
             seqs = np.arange(b.lo + c_lo, b.lo + c_hi)
             ctx = s.ctx[seqs]
-            if s.draft_kv == "reprefill":
+            if not cached:
                 self._draft_chunk_reprefill(s, bi, c_lo, c_hi, seqs, ctx, u_all)
                 continue
+            rows = s.drow[seqs]
             pos = ctx[None, :] + np.arange(n + 1)[:, None]                  # [n+1, cm]
-            slots = s.dkv.slots(np.broadcast_to(seqs, pos.shape), pos)
+            slots = s.dkv.slots(np.broadcast_to(rows, pos.shape), pos)
             qs = np.arange(cm + 1, dtype=np.int32)
             parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, pos.astype(np.int32).ravel()]
             if u_all is not None:
@@ -347,7 +377,7 @@ class Engine:
             qs_d = meta[o + 2 * P:o + 2 * P + cm + 1]
             kvb_d = meta[o + 2 * P + cm + 1:o + 3 * P + cm + 1]
             u_d = meta[o + 3 * P + cm + 1:].view(torch.float32) if u_all is not None else None
-            bt = s.dkv.block_table[seqs[0]:seqs[-1] + 1]
+            bt = s.dkv.block_table[rows[0]:rows[-1] + 1]
             for j in range(n + 1):
                 toks = meta[:cm] if j == 0 else s.drafts[bi][j - 1, c_lo:c_hi]
                 fb = ForwardBatch(toks, pos_d[j * cm:(j + 1) * cm], slot_d[j * cm:(j + 1) * cm], qs_d,
@@ -372,7 +402,7 @@ class Engine:
         st = self.drf_stream
         n = s.n_cand
         cm = c_hi - c_lo
-        local = np.arange(cm)
+        local = s.scratch_row0 + np.arange(cm)             # scratch draft KV rows
         lens = ctx + 1                                    # positions 0..ctx (t_last at ctx)
         T = int(lens.sum())
         flat = np.concatenate([seq * s.max_len + np.arange(L) for seq, L in zip(seqs, lens)])
@@ -401,7 +431,7 @@ class Engine:
         toks = self.draft.ws.get("rp_tokens", (T,), torch.int32)
         native.gather_i32(s.hist, idx, toks, st)
         last_rows = last_d
-        bt = s.dkv.block_table[:cm]
+        bt = s.dkv.block_table[s.scratch_row0:s.scratch_row0 + cm]
         for j in range(n):
             if j == 0:
                 fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_rows)
@@ -559,7 +589,7 @@ class Engine:
     # ------------------------------------------------------------ public API
     def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
                  mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None,
-                 draft_kv: str = "cached") -> list[list[int]]:
+                 draft_kv: str = "cached", draft_cached: int | None = None) -> list[list[int]]:
         """prompts (token id lists) → committed continuations, max_new_tokens each."""
         S = len(prompts)
         if policy is None:
@@ -567,7 +597,7 @@ class Engine:
                             bs_draft=(S + 1) // 2, n_cand=4)
         max_len = max(len(p) for p in prompts) + max_new_tokens + policy.n_cand + 2
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, temperature, forced_p,
-                             policy.bs_draft, draft_kv)
+                             policy.bs_draft, draft_kv, draft_cached)
         self.prefill(s, prompts, max_new_tokens, policy.bs_prefill)
         if (s.remaining > 0).any():
             self.first_draft(s)
@@ -576,7 +606,8 @@ class Engine:
         return [o[:max_new_tokens] for o in s.out]
 
     def run_decoding(self, policy, workload, plan=None, seed: int = 0, acceptance="greedy", prompts=None,
-                     max_rounds: int | None = None, draft_kv: str = "cached") -> SimResult:
+                     max_rounds: int | None = None, draft_kv: str = "cached",
+                     draft_cached: int | None = None) -> SimResult:
         """Measured counterpart of simulate_decoding (simulator.py:108-116).
 
         Runs workload.total_sequences sequences (two batches of
@@ -589,7 +620,7 @@ class Engine:
         S = workload.total_sequences
         max_len = workload.l_input + workload.max_new_tokens + policy.n_cand + 2
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, 1.0, forced_p,
-                             policy.bs_draft, draft_kv)
+                             policy.bs_draft, draft_kv, draft_cached)
         if prompts is not None:
             self.prefill(s, prompts, workload.max_new_tokens, policy.bs_prefill)
         else:

@@ -58,6 +58,7 @@ class OffloadPlan:
     tokens_per_s: float
     stream_attn: bool = False  # attention projections streamed with each layer (H3)
     stream_ratio: float = 1.0  # encoded / raw bytes of a streamed unit (K9 XC4 ≈ 0.75; 1 = raw)
+    draft_cached: int = 0      # draft_kv == "mixed": sequences per batch with a persistent draft KV row
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -103,16 +104,20 @@ def verify_flops(target: ModelArch, bs: int, n_cand: int, ctx: int) -> float:
     return bs * (n_cand + 1) * target.verify_flops_per_token(ctx)
 
 
-def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str) -> float:
-    """One batch's draft work per round: n+1 cached steps, or a context re-prefill + n−1 steps."""
-    if draft_kv == "cached":
-        return bs * (n_cand + 1) * draft.verify_flops_per_token(ctx)
-    return bs * (ctx * draft.verify_flops_per_token(ctx // 2) + (n_cand - 1) * draft.verify_flops_per_token(ctx))
+def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str, draft_cached: int = 0) -> float:
+    """One batch's draft work per round: n+1 cached steps per cached sequence, a
+    context re-prefill + n−1 steps per re-prefilled one ("mixed": the first
+    ``draft_cached`` sequences are cached)."""
+    kc = bs if draft_kv == "cached" else (0 if draft_kv == "reprefill" else min(draft_cached, bs))
+    cached = kc * (n_cand + 1) * draft.verify_flops_per_token(ctx)
+    rp = (bs - kc) * (ctx * draft.verify_flops_per_token(ctx // 2) + (n_cand - 1) * draft.verify_flops_per_token(ctx))
+    return cached + rp
 
 
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
-                 n_slots: int = 2, bs_candidates=None, page_size: int = 16, draft_kv_modes=("cached", "reprefill"),
+                 n_slots: int = 2, bs_candidates=None, page_size: int = 16,
+                 draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
@@ -135,36 +140,46 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  + resident_bytes(draft, True) + n_slots * layer_bytes + (ring_bytes if stream_ratio < 1 else 0))
         host_unit = int(math.ceil(layer_bytes * stream_ratio))
         for bs in cands:
-            bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
-            kv = kv_bytes(target, draft, 2 * bs, max_len, page_size, None if mode == "cached" else bs_draft)
-            ws = workspace_bytes(target, draft, bs, n_cand, None if mode == "cached" else bs_draft * max_len)
-            free = hbm_budget - fixed - kv - ws
-            if free < 0:
-                continue
-            pinned = min(target.n_layer, int(free // layer_bytes))
-            streamed = target.n_layer - pinned
-            if streamed * host_unit > host_budget:
-                continue
-            S = streamed * host_unit
-            t_stream = S / rates.h2d_bytes_per_s
-            eff = rates.tensor_flops * rates.tensor_efficiency
-            t_comp = (verify_flops(target, bs, n_cand, ctx_len) + draft_flops(draft, bs, n_cand, ctx_len, mode)) / eff
-            if stream_ratio < 1:
-                t_comp += streamed * layer_bytes * 1.75 / rates.hbm_bytes_per_s
-            t_round = max(t_stream, t_comp) + rates.round_overhead_s
-            tps = bs * e_tok / t_round
-            if best is None or tps > best[0] * 1.001:
-                best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
-                        stream_attn, fixed, layer_bytes)
+            if mode == "mixed":  # interior split points; the endpoints are the pure modes
+                step = max(8, bs // 32)
+                kcs = list(range(step, bs, step))
+            else:
+                kcs = [bs if mode == "cached" else 0]
+            for kc in kcs:
+                bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
+                draft_rows = 2 * kc + (bs_draft if kc < bs else 0)
+                kv = (PagedKVCache.bytes_needed(target, 2 * bs, max_len, page_size)
+                      + PagedKVCache.bytes_needed(draft, draft_rows, max_len, page_size))
+                ws = workspace_bytes(target, draft, bs, n_cand, None if kc == bs else max(bs_draft * max_len, kc))
+                free = hbm_budget - fixed - kv - ws
+                if free < 0:
+                    continue
+                pinned = min(target.n_layer, int(free // layer_bytes))
+                streamed = target.n_layer - pinned
+                if streamed * host_unit > host_budget:
+                    continue
+                S = streamed * host_unit
+                t_stream = S / rates.h2d_bytes_per_s
+                eff = rates.tensor_flops * rates.tensor_efficiency
+                t_comp = (verify_flops(target, bs, n_cand, ctx_len)
+                          + draft_flops(draft, bs, n_cand, ctx_len, "mixed", kc)) / eff
+                if stream_ratio < 1:
+                    t_comp += streamed * layer_bytes * 1.75 / rates.hbm_bytes_per_s
+                t_round = max(t_stream, t_comp) + rates.round_overhead_s
+                tps = bs * e_tok / t_round
+                if best is None or tps > best[0] * 1.001:
+                    best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
+                            stream_attn, fixed, layer_bytes, kc)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
-    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes = best
+    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes, kc = best
     # pin the first layers (ascending order, placement.py:220-231); stream the rest
     pinned_l = tuple(range(pinned))
     stream_l = tuple(range(pinned, target.n_layer))
     return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if streamed else 0,
                        {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes},
-                       S, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio)
+                       S, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
+                       kc if mode == "mixed" else 0)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,
@@ -286,10 +301,10 @@ def calibrate(observations, workload, rates: B200Rates, target: ModelArch, draft
 
 
 def predict_round_s(rates: B200Rates, target: ModelArch, draft: ModelArch, bs: int, n_cand: int, ctx: int,
-                    draft_kv: str, streamed_bytes: int) -> float:
+                    draft_kv: str, streamed_bytes: int, draft_cached: int = 0) -> float:
     """Round time of one measured configuration (fixed streamed split)."""
     eff = rates.tensor_flops * rates.tensor_efficiency
-    comp = (verify_flops(target, bs, n_cand, ctx) + draft_flops(draft, bs, n_cand, ctx, draft_kv)) / eff
+    comp = (verify_flops(target, bs, n_cand, ctx) + draft_flops(draft, bs, n_cand, ctx, draft_kv, draft_cached)) / eff
     return max(streamed_bytes / rates.h2d_bytes_per_s, comp) + rates.round_overhead_s
 
 

@@ -195,3 +195,22 @@ def test_generate_identical_with_xc4_streamed_units(pair):
     eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3}, codec="xc4")
     assert eng.target.streamer.coded
     assert eng.generate(prompts, 12, pol) == raw
+
+
+@pytest.mark.parametrize("draft_cached,bs_draft", [(2, 4), (1, 3), (3, 1)])
+def test_mixed_draft_kv_matches_oracle(pair, draft_cached, bs_draft):
+    """Mixed draft KV: the first draft_cached sequences of each batch keep a
+    draft KV row, the rest re-prefill into the scratch rows — same greedy
+    tokens as the all-cached engine and the oracle."""
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=19)
+    pol = Policy(8, 4, bs_draft, 4)
+    cached = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2}).generate(prompts, 14, pol)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2})
+    got = eng.generate(prompts, 14, pol, draft_kv="mixed", draft_cached=draft_cached)
+    s = eng.last_session
+    assert s.n_cached == [draft_cached, draft_cached] and s.dkv.n_seq == 2 * draft_cached + bs_draft
+    margins = []
+    want, _ = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts, 14, 4, 4, margins=margins)
+    assert_greedy_parity(got, want, margins)
+    assert got == cached
