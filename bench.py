@@ -54,6 +54,10 @@ def parse():
                     help="draft KV policy (auto = planner)")
     ap.add_argument("--layers", type=int, default=0,
                     help="profiling only: override the target's layer count (same per-layer shapes)")
+    ap.add_argument("--max-pinned", type=int, default=-1,
+                    help="profiling only: cap the planner's HBM-pinned layers (-1 = planner)")
+    ap.add_argument("--draft-cached", type=int, default=-1,
+                    help="mixed draft KV: cached sequences per batch (-1 = planner)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
@@ -222,7 +226,8 @@ def main():
         torch.cuda.empty_cache()
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
-                        ring_bytes=ring)
+                        ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
+                        draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached])
     t_setup = time.perf_counter()
     layer_bytes = ffn_offsets(tgt)[2]
     if world > 1:
@@ -268,6 +273,7 @@ def main():
     w0 = time.perf_counter()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects the timed rounds
     eng.nvtx_range = "timed"             # ... on the draft-enqueue thread too
+    eng.round_times.clear()
     for _ in range(steps):
         eng.round(s)  # public API: H2D inputs, verify+draft, barrier, D2H committed tokens
     eng.nvtx_range = None
@@ -435,6 +441,10 @@ def main():
         "codec_kernel": codec_k,
         "kernel_roofline": kern,
         "clocks": clk,
+        "stream_busy_ms": {"draft_stream_per_round": [round(a, 1) for a, _ in eng.round_times[:steps]],
+                           "verify_stream_per_round": [round(b, 1) for _, b in eng.round_times[:steps]],
+                           "note": "start→end of each stream's work in a round (the draft runs concurrently "
+                                   "with the verify; the verify waits on streamed layers)"},
         "gpu_launches": launches["kernels"],
         "copy_calls": launches["copies"],
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(streamed / steps + meta_bytes),

@@ -537,6 +537,226 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- persistent variants: double-buffered TMEM accumulator --------------------
+//
+// One CTA (cta_group::1) or CTA pair (cta_group::2) per SM (pair), looping over
+// a static round-robin tile schedule.  The accumulator is double-buffered in
+// TMEM (2 × BN columns), so the epilogue of tile i (TMEM → registers → global)
+// runs while the tensor pipe accumulates tile i+1, and the prologue (barrier
+// init, TMEM alloc, descriptor prefetch, pipeline fill) is paid once per CTA
+// instead of once per tile.  Pipelines:
+//   smem ring   full[s] / empty[s]        TMA producer  ↔ MMA issuer
+//   accumulator tmem_full[b] / tmem_empty[b]  MMA issuer ↔ epilogue warps
+// In pair mode tmem_empty lives in the leader and counts the epilogue warps
+// of both CTAs (the peer arrives remotely through its cluster address).
+
+template <int CG, int BN>
+struct CfgP {
+  static constexpr int kABytes = 128 * BK * 2;                          // this CTA's A rows per stage
+  static constexpr int kBBytes = (CG == 2 ? BN / 2 : BN) * BK * 2;      // this CTA's B rows per stage
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (196 * 1024) / kStageBytes;            // 6 × 32 KB or 4 × 48 KB
+  static constexpr int kTmemCols = 2 * BN;                              // two fp32 accumulators
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
+};
+
+struct TileInfo {
+  int expert, row0, row_end, n0;
+  bool valid;
+};
+
+// tile t → rows/expert/columns (tileM = output rows of one tile: 128, or 256 for a pair)
+__device__ __forceinline__ TileInfo tile_info(int t, const int32_t* __restrict__ offs, int E, int M, int m_tiles,
+                                              int n_tiles, int tileM, int BNc) {
+  int mt, nt;
+  raster_tile(t, m_tiles, n_tiles, mt, nt);
+  TileInfo ti;
+  ti.expert = 0;
+  ti.row0 = mt * tileM;
+  ti.row_end = M;
+  ti.n0 = nt * BNc;
+  ti.valid = ti.row0 < M;
+  if (offs != nullptr) {
+    int before = 0;
+    ti.valid = false;
+    for (int e = 0; e < E; ++e) {
+      const int lo = offs[e], hi = offs[e + 1];
+      const int nt_e = (hi - lo + tileM - 1) / tileM;
+      if (mt < before + nt_e) {
+        ti.expert = e;
+        ti.row0 = lo + (mt - before) * tileM;
+        ti.row_end = hi;
+        ti.valid = true;
+        break;
+      }
+      before += nt_e;
+    }
+  }
+  return ti;
+}
+
+template <int CG, int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C, int ldc,
+                    const void* __restrict__ aux, int m_tiles, int n_tiles) {
+  using CF = CfgP<CG, BN>;
+  constexpr int kTileM = 128 * CG;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int total = m_tiles * n_tiles;
+  const int num_kb = K / BK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + CF::kStages * CF::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::kStages * CF::kStageBytes);
+  uint64_t* empty = full + CF::kStages;
+  uint64_t* tmem_full = empty + CF::kStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < CF::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4 * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(CF::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(CF::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint32_t leader_full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;
+      uint32_t it = 0;
+      for (int t = unit; t < total; t += units) {
+        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+        if (!ti.valid) continue;
+        const int rowA = ti.row0 + (int)rank * 128;
+        const int rowB = ti.n0 + (CG == 2 ? (int)rank * (BN / 2) : 0);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % CF::kStages;
+          const uint32_t ph = (it / CF::kStages) & 1;
+          mbar_wait_guard(&empty[s], ph ^ 1);
+          if constexpr (CG == 2) {
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * CF::kStageBytes);
+            const uint32_t bar = leader_full0 + s * 8;
+            tma_load_2d_pair(sA + s * CF::kABytes, &tmA, bar, kb * BK, rowA);
+            tma_load_3d_pair(sB + s * CF::kBBytes, &tmB, bar, kb * BK, rowB, ti.expert);
+          } else {
+            mbar_expect_tx(&full[s], CF::kStageBytes);
+            tma_load_2d(sA + s * CF::kABytes, &tmA, &full[s], kb * BK, rowA);
+            tma_load_3d(sB + s * CF::kBBytes, &tmB, &full[s], kb * BK, rowB, ti.expert);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (single thread; the leader CTA in pair mode) =====
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(kTileM >> 4) << 24);
+      uint32_t it = 0, acc = 0;
+      for (int t = unit; t < total; t += units) {
+        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+        if (!ti.valid) continue;
+        const uint32_t buf = acc & 1, aph = (acc >> 1) & 1;
+        mbar_wait_guard(&tmem_empty[buf], aph ^ 1);  // the epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % CF::kStages;
+          const uint32_t ph = (it / CF::kStages) & 1;
+          mbar_wait_guard(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + s * CF::kABytes);
+          const uint32_t b0 = smem_u32(sB + s * CF::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            if constexpr (CG == 2)
+              umma_bf16_pair(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+            else
+              umma_bf16(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+          }
+          if constexpr (CG == 2) umma_commit_pair(&empty[s]);
+          else umma_commit(&empty[s]);
+        }
+        if constexpr (CG == 2) umma_commit_pair(&tmem_full[buf]);
+        else umma_commit(&tmem_full[buf]);
+        ++acc;
+      }
+    }
+  } else {
+    // ===== epilogue warps: TMEM → registers → global, then release the accumulator =====
+    const int quarter = warp & 3;  // tcgen05.ld lane window of this warp
+    const int row = quarter * 32 + lane;
+    uint32_t acc = 0;
+    uint32_t empty0 = smem_u32(&tmem_empty[0]), empty1 = smem_u32(&tmem_empty[1]);
+    if constexpr (CG == 2) {  // the leader's barriers
+      asm volatile("mapa.shared::cluster.u32 %0, %0, 0;" : "+r"(empty0));
+      asm volatile("mapa.shared::cluster.u32 %0, %0, 0;" : "+r"(empty1));
+    }
+    for (int t = unit; t < total; t += units) {
+      const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+      if (!ti.valid) continue;
+      const uint32_t buf = acc & 1, aph = (acc >> 1) & 1;
+      mbar_wait_guard(&tmem_full[buf], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int grow = ti.row0 + (int)rank * 128 + row;
+      const bool valid = grow < ti.row_end && grow < M;
+      const uint32_t tbase = tmem_base + buf * BN + ((uint32_t)(quarter * 32) << 16);
+      epilogue_tile<BN, EPI>(tbase, valid, grow, ti.n0, N, C, ldc, aux);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(buf ? empty1 : empty0)
+                       : "memory");
+        else
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(buf ? empty1 : empty0) : "memory");
+      }
+      ++acc;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (CG == 2) cluster_sync();  // the peer's TMEM is done with before the pair frees it
+  else __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::kTmemCols));
+  }
+}
+
 // ---- host side ---------------------------------------------------------------
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -613,7 +833,46 @@ int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs,
   return SO_OK;
 }
 
-int g_variant = 0;  // 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where legal
+int g_variant = 0;  // 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where legal, 3 = one tile per CTA
+
+// persistent launch: one CTA (pair) per SM (pair), never more than the tiles
+template <int CG, int BN, int EPI>
+int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs, int E, int m_tiles,
+                      int M, int N, int K, void* C, int ldc, const void* aux, cudaStream_t st) {
+  using CF = CfgP<CG, BN>;
+  auto kern = gemm_tcp_kernel<CG, BN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  const int n_tiles = (N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles;
+  int units = sm_count() / CG;
+  if (units > tiles) units = tiles;
+  if (units < 1) units = 1;
+  if constexpr (CG == 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * units);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = CF::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
+    if (e != cudaSuccess) return (int)e;
+  } else {
+    kern<<<units, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
+  }
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
 
 template <int EPI>
 int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
@@ -623,6 +882,8 @@ int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M,
   if (rc) return rc;
   rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
   if (rc) return rc;
+  const int pair_tiles = offs ? (M + 255) / 256 + E : (M + 255) / 256;
+  if (g_variant != 3) return launch_persistent<2, 256, EPI>(ma, mb, offs, E, pair_tiles, M, N, K, C, ldc, aux, st);
   auto kern = gemm_tc2_kernel<EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -630,7 +891,6 @@ int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M,
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  const int pair_tiles = offs ? (M + 255) / 256 + E : (M + 255) / 256;
   const int n_tiles = N / 256;
   kern<<<2 * pair_tiles * n_tiles, kThreads, Cfg2::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, pair_tiles,
                                                                  n_tiles);
@@ -645,7 +905,7 @@ int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, 
   // 128-row tiles pad less when M is small or split into experts (~560 rows
   // each at bs 248: measured 0.58 vs 0.51 of peak, profiles/gemm_bench_r1.json).
   const bool pair_ok = (N % 256) == 0;
-  if (pair_ok && (g_variant == 2 || (g_variant == 0 && offs == nullptr && M >= 1024)))
+  if (pair_ok && (g_variant == 2 || ((g_variant == 0 || g_variant == 3) && offs == nullptr && M >= 1024)))
     return launch_pair<EPI>(A, B, offs, E, M, N, K, C, ldc, aux, st);
   const int m_tiles = offs ? (M + BM - 1) / BM + E : (M + BM - 1) / BM;
   // prefer the wide tile unless it leaves most SMs idle
@@ -657,10 +917,12 @@ int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, 
   if (wide) {
     rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 256);
     if (rc) return rc;
+    if (g_variant != 3) return launch_persistent<1, 256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
     return launch_bn<256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
   }
   rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
   if (rc) return rc;
+  if (g_variant != 3) return launch_persistent<1, 128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
   return launch_bn<128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
 }
 
@@ -702,7 +964,7 @@ extern "C" int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t*
 extern "C" int so_device_sm_count(void) { return sm_count(); }
 
 extern "C" int so_gemm_set_variant(int variant) {
-  SO_REQUIRE(variant >= 0 && variant <= 2, SO_E_SHAPE);
+  SO_REQUIRE(variant >= 0 && variant <= 3, SO_E_SHAPE);
   g_variant = variant;
   return SO_OK;
 }

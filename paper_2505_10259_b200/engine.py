@@ -184,6 +184,9 @@ class Engine:
         self._arenas: dict = {}   # stream handle -> _StagingArena (per-round H2D metadata)
         self.nvtx_range: str | None = None  # mirrored onto the draft-enqueue thread when set
         self._join = native.Event()
+        # per-round stream busy times (draft stream start→end, verify start→end), ms
+        self._tev = [native.Event(timing=True) for _ in range(4)]
+        self.round_times: list[tuple[float, float]] = []
         if trace:
             self.target.hooks = self._layer_hook
             if self.target.streamer is not None:
@@ -559,21 +562,27 @@ class Engine:
                 except BaseException as exc:  # re-raised on the caller's thread
                     err.append(exc)
 
+            self._tev[0].record(self.drf_stream)
             worker = threading.Thread(target=run_draft, name="draft-enqueue")
             worker.start()
+        self._tev[2].record(self.tgt_stream)
         if verify:
             self._cur = (rnd, bi)
             self._verify(s, bi, rnd)
+        self._tev[3].record(self.tgt_stream)
         if worker is not None:
             worker.join()
             if err:
                 raise err[0]
+            self._tev[1].record(self.drf_stream)
         # barrier (simulator.py:209-211): device-side join, then the host reads counts
         self._join.record(self.drf_stream)
         self._join.wait(self.tgt_stream)
         bev = self.tracer.mark(self.tgt_stream)
         self.tracer.add("GPU_TARGET", "barrier", bev, bev, rnd=rnd)
         native.stream_synchronize(self.tgt_stream)
+        self.round_times.append((self._tev[0].elapsed_ms(self._tev[1]) if draft else 0.0,
+                                 self._tev[2].elapsed_ms(self._tev[3])))
         self._release_staging()
         c = self._commit(s, bi) if verify else 0
         s.rounds += 1

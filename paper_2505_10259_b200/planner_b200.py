@@ -35,7 +35,10 @@ class B200Rates:
     h2d_bytes_per_s: float = 55.5e9        # pinned H2D, measured 55.5 GB/s
     hbm_bytes_per_s: float = 6552e9        # MEASURED_PEAKS.json
     tensor_flops: float = 1375.5e12        # sustained bf16, MEASURED_PEAKS.json
-    tensor_efficiency: float = 0.5         # achieved fraction for skinny MoE tiles (re-fit by calibrate)
+    # achieved fraction of the sustained peak for a round's mixed compute (verify MoE + draft re-prefill,
+    # the two streams concurrent, power-capped): 0.68 measured with the persistent GEMMs
+    # (profiles/planner_sweep_r1.md, bs 440 / 48 cached: 3.3 PFLOP in 3.5 s); 0.65 keeps a margin
+    tensor_efficiency: float = 0.65
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
 
 
@@ -119,7 +122,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  n_slots: int = 2, bs_candidates=None, page_size: int = 16,
                  draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
-                 ring_bytes: int = 0) -> OffloadPlan:
+                 ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
@@ -142,7 +145,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
         for bs in cands:
             if mode == "mixed":  # interior split points; the endpoints are the pure modes
                 step = max(8, bs // 32)
-                kcs = list(range(step, bs, step))
+                kcs = list(range(step, bs, step)) if draft_cached_candidates is None else [
+                    k for k in draft_cached_candidates if 0 < k < bs]
             else:
                 kcs = [bs if mode == "cached" else 0]
             for kc in kcs:
@@ -154,7 +158,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                 free = hbm_budget - fixed - kv - ws
                 if free < 0:
                     continue
-                pinned = min(target.n_layer, int(free // layer_bytes))
+                pinned = min(target.n_layer, int(free // layer_bytes),
+                             target.n_layer if max_pinned is None else max_pinned)
                 streamed = target.n_layer - pinned
                 if streamed * host_unit > host_budget:
                     continue

@@ -173,9 +173,10 @@ def test_moe_combine():
 
 # ------------------------------------------------------------- K3/K4/K5 ---
 
-@pytest.fixture(params=[1, 2], ids=["cta1", "cta_pair"])
+@pytest.fixture(params=[1, 2, 3], ids=["cta1", "cta_pair", "one_tile_per_cta"])
 def gemm_variant(request):
-    """Run each GEMM test on the 1-CTA tiles and on the cta_group::2 pair tiles."""
+    """Run each GEMM test on the persistent 1-CTA tiles, the persistent cta_group::2
+    pair tiles, and the non-persistent one-tile-per-CTA kernels."""
     native.gemm_set_variant(request.param)
     yield request.param
     native.gemm_set_variant(0)
@@ -190,7 +191,7 @@ def _bf16_close(got, want, rel=1.5e-2):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 64), (128, 128, 128), (200, 384, 256), (1280, 8192, 6144),
-                                   (77, 32768, 512), (4096, 4096, 4096), (3, 32, 64)])
+                                   (77, 32768, 512), (4096, 4096, 4096), (3, 32, 64), (8192, 8192, 128)])
 def test_gemm_dense(M, N, K, gemm_variant):
     g = torch.Generator(device=DEV).manual_seed(M + N + K)
     a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
