@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
-    ap.add_argument("--e2e-seqs", type=int, default=256, help="sequences of the generate() leg")
+    ap.add_argument("--e2e-seqs", type=int, default=0,
+                    help="sequences of the generate() leg (0 = both batches of the decode plan, 2·bs_decoding)")
     ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
@@ -380,7 +381,7 @@ def main():
     if not args.no_e2e_generate:
         del s
         torch.cuda.empty_cache()
-        S_e = args.e2e_seqs
+        S_e = args.e2e_seqs or 2 * bs
         rng = np.random.default_rng(1234 + rank)
         prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
         pol = Policy(bs_prefill=S_e, bs_decoding=(S_e + 1) // 2, bs_draft=min(64, (S_e + 1) // 2),

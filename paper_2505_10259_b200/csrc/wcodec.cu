@@ -22,10 +22,11 @@
 // exponents present in the unit sorted by (count desc, exponent asc); the
 // first ≤15 get codes 0.., unused table entries are 0.
 //
-// Decode (HBM-bound: 1.5 B read + 2 B written per weight): one CTA of 256
-// threads per 4096-element block, 16 weights per thread; the exponent lookup
+// Decode (HBM-bound: 1.5 B read + 2 B written per weight): one warp per
+// 4096-element block (grid-stride), 8 weights per lane per step so every load
+// and store instruction of a warp is one contiguous run; the exponent lookup
 // is two PRMT byte permutes over the register-resident table plus a select,
-// and a block-wide scan runs only when the block holds an escape.
+// and escapes are consumed with a warp scan (no CTA barrier).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -111,53 +112,91 @@ __device__ __forceinline__ int count_escapes(uint64_t codes) {
   return __popcll(x);
 }
 
+__device__ __forceinline__ uint2 ld_nc8(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// One warp decodes one 4096-weight block: 8 steps of 512 weights, lane l
+// owning weights [512i + 16l, +16) of step i: a 16-B sign/mantissa load, an
+// 8-B code load and one 32-B (256-bit) store per lane, each a contiguous run
+// across the warp.  Escapes (stored in element order) are consumed step by
+// step with a warp-level scan — no CTA barrier anywhere.
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr int kStepsAhead = 4;  // steps whose loads are in flight together (96 B per lane)
+
+__device__ __forceinline__ void st_v8(void* p, const uint32_t* o) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+               "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads) xc4_decode_kernel(const uint8_t* __restrict__ frame, uint32_t m,
                                                                uint32_t off_eo, uint32_t off_esc, uint32_t t0,
                                                                uint32_t t1, uint32_t t2, uint32_t t3,
                                                                uint16_t* __restrict__ dst) {
-  __shared__ int s_warp[kThreads / 32];
-  const uint32_t e0 = blockIdx.x * kBlock + threadIdx.x * 16;
-  const bool live = e0 < m;
-  int4 smv = make_int4(0, 0, 0, 0);
-  uint2 ecv = make_uint2(0xffffffffu, 0xffffffffu);  // dead lanes: treated as escapes, but counted as 0 below
-  if (live) {
-    smv = ld_nc16(frame + e0);
-    ecv = *reinterpret_cast<const uint2*>(frame + m + e0 / 2);
-  }
-  const uint64_t codes = ((uint64_t)ecv.y << 32) | ecv.x;
-  const int nesc = live ? count_escapes(codes) : 0;
-  const uint32_t sw[4] = {(uint32_t)smv.x, (uint32_t)smv.y, (uint32_t)smv.z, (uint32_t)smv.w};
-  uint32_t ex[4];
-  ex[0] = lookup4(ecv.x & 0xffffu, t0, t1, t2, t3);
-  ex[1] = lookup4(ecv.x >> 16, t0, t1, t2, t3);
-  ex[2] = lookup4(ecv.y & 0xffffu, t0, t1, t2, t3);
-  ex[3] = lookup4(ecv.y >> 16, t0, t1, t2, t3);
-  if (__syncthreads_or(nesc)) {  // rare: patch escaped exponents from the side stream
-    int total;
-    const int pre = block_exclusive_scan(nesc, s_warp, total);
-    if (nesc) {
-      const int32_t base = reinterpret_cast<const int32_t*>(frame + off_eo)[blockIdx.x];
-      const uint8_t* esc = frame + off_esc + base + pre;
-      int k = 0;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nb = (m + kBlock - 1) / kBlock;
+  const uint32_t stride = gridDim.x * kWarpsPerCta;
+  for (uint32_t blk = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); blk < nb; blk += stride) {
+    const uint8_t* esc = frame + off_esc + reinterpret_cast<const int32_t*>(frame + off_eo)[blk];
+    int carry = 0;  // escapes consumed by earlier steps of this block
 #pragma unroll 1
-      for (int i = 0; i < 16; ++i) {
-        if (((codes >> (4 * i)) & 0xfu) == 0xfu) {
-          const uint32_t sh = 8 * (i & 3);
-          ex[i >> 2] = (ex[i >> 2] & ~(0xffu << sh)) | ((uint32_t)esc[k++] << sh);
+    for (int s0 = 0; s0 < kBlock / 512; s0 += kStepsAhead) {
+      int4 sm[kStepsAhead];
+      uint2 cd[kStepsAhead];
+      bool live[kStepsAhead];
+#pragma unroll
+      for (int j = 0; j < kStepsAhead; ++j) {
+        const uint32_t e = blk * kBlock + (s0 + j) * 512 + lane * 16;
+        live[j] = e < m;
+        sm[j] = make_int4(0, 0, 0, 0);
+        cd[j] = make_uint2(0u, 0u);
+        if (live[j]) {
+          sm[j] = ld_nc16(frame + e);
+          cd[j] = ld_nc8(frame + m + e / 2);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kStepsAhead; ++j) {
+        const uint64_t codes = ((uint64_t)cd[j].y << 32) | cd[j].x;
+        const int n = live[j] ? count_escapes(codes) : 0;
+        uint32_t ex[4] = {lookup4(cd[j].x & 0xffffu, t0, t1, t2, t3), lookup4(cd[j].x >> 16, t0, t1, t2, t3),
+                          lookup4(cd[j].y & 0xffffu, t0, t1, t2, t3), lookup4(cd[j].y >> 16, t0, t1, t2, t3)};
+        if (__any_sync(0xffffffffu, n)) {  // rare: patch escaped exponents from the side stream
+          int inc = n;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+          }
+          if (n) {
+            const uint8_t* q = esc + carry + inc - n;
+            int k = 0;
+#pragma unroll 1
+            for (int i = 0; i < 16; ++i) {
+              if (((codes >> (4 * i)) & 0xfu) == 0xfu) {
+                const uint32_t sh = 8 * (i & 3);
+                ex[i >> 2] = (ex[i >> 2] & ~(0xffu << sh)) | ((uint32_t)q[k++] << sh);
+              }
+            }
+          }
+          carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (live[j]) {
+          const uint32_t sw[4] = {(uint32_t)sm[j].x, (uint32_t)sm[j].y, (uint32_t)sm[j].z, (uint32_t)sm[j].w};
+          uint32_t o[8];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            o[2 * w] = assemble2(prmt(sw[w], 0u, 0x5150u), prmt(ex[w], 0u, 0x5150u));
+            o[2 * w + 1] = assemble2(prmt(sw[w], 0u, 0x5352u), prmt(ex[w], 0u, 0x5352u));
+          }
+          st_v8(dst + blk * kBlock + (s0 + j) * 512 + lane * 16, o);
         }
       }
     }
   }
-  if (!live) return;
-  uint32_t o[8];
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    o[2 * w] = assemble2(prmt(sw[w], 0u, 0x5150u), prmt(ex[w], 0u, 0x5150u));
-    o[2 * w + 1] = assemble2(prmt(sw[w], 0u, 0x5352u), prmt(ex[w], 0u, 0x5352u));
-  }
-  int4* out = reinterpret_cast<int4*>(dst + e0);
-  out[0] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
-  out[1] = make_int4((int)o[4], (int)o[5], (int)o[6], (int)o[7]);
 }
 
 // ---------------------------------------------------------------- encoder ---
@@ -464,7 +503,15 @@ inline int launch_decode(const so_xc4_header* h, uint32_t f, const uint8_t* fram
   const FrameGeom g = frame_geom(m);
   uint32_t t[4];
   table_words(h, t);
-  xc4_decode_kernel<<<(m + kBlock - 1) / kBlock, kThreads, 0, st>>>(
+  static int ctas = 0;  // 8 resident CTAs (64 warps) per SM, grid-stride over the rest
+  if (ctas == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = 8 * sms;
+  }
+  const uint32_t need = (m + kBlock * kWarpsPerCta - 1) / (kBlock * kWarpsPerCta);
+  xc4_decode_kernel<<<need < (uint32_t)ctas ? need : (uint32_t)ctas, kThreads, 0, st>>>(
       frame_dev, m, (uint32_t)g.off_eo, (uint32_t)g.off_esc, t[0], t[1], t[2], t[3],
       reinterpret_cast<uint16_t*>(dst_unit) + e_begin);
   SO_CHECK_LAUNCH();

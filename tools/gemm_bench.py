@@ -37,6 +37,7 @@ def timed(fn, reps=10):
 
 
 def main():
+    only = sys.argv[1] if len(sys.argv) > 1 else None  # substring filter on the shape name (profiling)
     g = torch.Generator(device=DEV).manual_seed(0)
     rows = []
     shapes = [
@@ -50,6 +51,8 @@ def main():
         ("square 8192^3", 8192, 8192, 8192, native.EPI_BF16, 0),
     ]
     for name, M, N, K, epi, E in shapes:
+        if only and only not in name:
+            continue
         a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
         b = (torch.randn(max(E, 1) * N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
         out_cols = N // 2 if epi == native.EPI_SWIGLU else N
