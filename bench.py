@@ -221,7 +221,7 @@ def main():
         probe = torch.empty(1 << 26, dtype=torch.bfloat16, device=device).normal_(0.0, 0.02, generator=g)
         enc = C.Encoder(device)
         ratio = enc.encode(probe)[0].numel() / (2 * probe.numel()) * 1.002
-        ring = 4 * (64 << 20)  # LayerStreamer.RING_SLOTS encoded frames (≈50 MB each)
+        ring = 4 * (192 << 20)  # LayerStreamer.RING_SLOTS encoded frames (≤ 180 MB each)
         enc.release()
         del probe
         torch.cuda.empty_cache()

@@ -138,8 +138,10 @@ int so_gemm_bf16(const void* A, const void* B, int M, int N, int K,
                  void* C, int ldc, int epilogue, const void* aux, void* stream);
 
 /* Tile variant of the GEMMs (process-wide; for tests and benchmarks):
- * 0 = auto (CTA-pair 256×256 cta_group::2 tiles for M ≥ 1024 and N % 256 == 0,
- * else 1-CTA 128×{128,256}), 1 = 1-CTA only, 2 = CTA-pair wherever legal. */
+ * 0 = auto (persistent kernels with double-buffered TMEM accumulators:
+ * CTA-pair 256×256 cta_group::2 tiles for M ≥ 1024 and N % 256 == 0, else
+ * 1-CTA 128×{128,256}), 1 = persistent 1-CTA only, 2 = persistent CTA-pair
+ * wherever legal, 3 = the auto choice with one tile per CTA (non-persistent). */
 int so_gemm_set_variant(int variant);
 
 /* Grouped (MoE) GEMM: rows [offs[e], offs[e+1]) of A use expert e's weight
@@ -180,12 +182,12 @@ int so_stream_layer(void* slot, const void* pinned_src, size_t bytes, size_t chu
 /* ---- K9: XC4 lossless exponent-coded weight units ------------------------
  * Same streamed bytes' *meaning* as so_stream_layer (the modeled `ffn_load`,
  * simulator.py:172-176; ffn_bytes / c2g_bandwidth, costmodel.py:74), fewer
- * bytes on the link: sign+mantissa byte + 4-bit exponent code per bf16
- * weight, escapes in a side stream (format: csrc/wcodec.cu).  Decoding is
- * bit-exact.  A unit = this header | u64 frame_off[n_frames+1] | frames. */
+ * bytes on the link: sign+mantissa byte + a 3- or 4-bit exponent code per
+ * bf16 weight, escapes in a side stream (format: csrc/wcodec.cu).  Decoding
+ * is bit-exact.  A unit = this header | u64 frame_off[n_frames+1] | frames. */
 typedef struct so_xc4_header {
   uint32_t magic;          /* "XC41" */
-  uint32_t version;        /* 1 */
+  uint32_t version;        /* 1: 4-bit codes (15 exponents + escape); 2: 3-bit codes (7 + escape) */
   uint64_t n_elems;        /* bf16 weights in the unit (multiple of 16) */
   uint32_t frame_elems;    /* elements per frame (multiple of 4096) */
   uint32_t n_frames;
@@ -199,10 +201,11 @@ typedef struct so_xc4_header {
 size_t so_xc4_scratch_bytes(uint64_t n_elems, uint32_t frame_elems);
 size_t so_xc4_bound(uint64_t n_elems, uint32_t frame_elems);
 /* Encode `n_elems` bf16 weights (device) into `dst` (device, 16-B aligned).
- * dst == NULL → size query: *out_bytes = encoded size.  Synchronises
- * `stream` (setup-time call, not a hot-path one). */
-int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, void* dst, size_t dst_cap,
-                  void* scratch, uint64_t* out_bytes, so_xc4_header* out_header, void* stream);
+ * code_bits: 0 = the smaller of 3- and 4-bit codes for this unit, 3 or 4 =
+ * forced (3 needs n_elems % 32 == 0).  dst == NULL → size query: *out_bytes =
+ * encoded size.  Synchronises `stream` (setup-time call, not a hot-path one). */
+int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, int code_bits, void* dst,
+                  size_t dst_cap, void* scratch, uint64_t* out_bytes, so_xc4_header* out_header, void* stream);
 /* Decode frames [frame_begin, frame_end) of a unit whose bytes sit at
  * unit_dev (device) into dst (the unit's full bf16 output; frame f lands at
  * element f·frame_elems).  unit_host = a host copy of at least the header and

@@ -10,12 +10,16 @@
  * size-independent property the tests check at full size.
  *
  * Normative rules restated here:
+ *   code width  b = 4 (header version 1: 15 exponents + escape) or b = 3
+ *               (version 2: 7 + escape); automatic choice: b = 3 iff n % 32 == 0
+ *               and 11·n + 8·esc7 < 12·n + 8·esc15 (esc_k = weights whose
+ *               exponent is not among the k most frequent)
  *   code table  exponents sorted by (count desc, exponent asc); the first
- *               min(15, distinct) get codes 0..; other table entries 0;
- *               code 15 = escape (raw exponent byte in the side stream)
- *   frame       sm u8[m] | ec u8[m/2] (element 2j → low nibble of byte j) |
- *               pad to 16 | eo i32[nb+1] (escapes before each 4096-block) |
- *               esc u8[frame escapes] | zero pad to 256
+ *               min(2^b − 1, distinct) get codes 0..; other table entries 0;
+ *               code 2^b − 1 = escape (raw exponent byte in the side stream)
+ *   frame       sm u8[m] | codes u8[m·b/8] (element i at bit b·i, little-endian
+ *               bytes) | pad to 16 | eo i32[nb+1] (escapes before each
+ *               4096-block) | esc u8[frame escapes] | zero pad to 256
  *   unit        64-B header | u64 frame_off[nf+1] | zero pad to 256 | frames
  */
 #include <stdint.h>
@@ -36,32 +40,47 @@ typedef struct {
 
 static uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
-static void geom(uint64_t m, uint64_t* off_eo, uint64_t* off_esc) {
-  *off_eo = up(m + m / 2, 16);
+static void geom(uint64_t m, int bits, uint64_t* off_eo, uint64_t* off_esc) {
+  *off_eo = up(m + m * bits / 8, 16);
   *off_esc = *off_eo + 4 * ((m + XC4_BLOCK - 1) / XC4_BLOCK + 1);
 }
 
 static uint8_t expo(uint16_t v) { return (uint8_t)((v >> 7) & 0xff); }
 
-/* returns 0 on success, -2 on bad geometry, -3 if cap is too small (out_bytes
- * still set); dst == NULL → size query */
-int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst, uint64_t cap, uint64_t* out_bytes) {
+/* bits: 0 = automatic, 3 or 4 = forced.  Returns 0 on success, -2 on bad
+ * geometry, -3 if cap is too small (out_bytes still set); dst == NULL → size
+ * query */
+int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, int bits, uint8_t* dst, uint64_t cap,
+                      uint64_t* out_bytes) {
   if (n == 0 || n % 16 || F < XC4_BLOCK || F % XC4_BLOCK) return -2;
+  if (!(bits == 0 || bits == 3 || bits == 4) || (bits == 3 && n % 32)) return -2;
   uint64_t hist[256] = {0};
   for (uint64_t i = 0; i < n; ++i) hist[expo(src[i])]++;
   xc4_header h;
   memset(&h, 0, sizeof h);
-  uint8_t code[256];
-  memset(code, 15, sizeof code);
-  int taken[256] = {0};
-  for (int c = 0; c < 15; ++c) {
+  int order[256], distinct = 0, taken[256] = {0};
+  for (;;) {
     int best = -1;
     for (int x = 0; x < 256; ++x)
       if (!taken[x] && hist[x] && (best < 0 || hist[x] > hist[best])) best = x;
     if (best < 0) break;
     taken[best] = 1;
-    h.exp_of_code[c] = (uint8_t)best;
-    code[best] = (uint8_t)c;
+    order[distinct++] = best;
+  }
+  if (bits == 0) {
+    uint64_t top7 = 0, top15 = 0;
+    for (int i = 0; i < distinct && i < 15; ++i) {
+      if (i < 7) top7 += hist[order[i]];
+      top15 += hist[order[i]];
+    }
+    bits = (n % 32 == 0 && 11 * n + 8 * (n - top7) < 12 * n + 8 * (n - top15)) ? 3 : 4;
+  }
+  const uint8_t esc_code = (uint8_t)((1u << bits) - 1);
+  uint8_t code[256];
+  memset(code, esc_code, sizeof code);
+  for (int c = 0; c < esc_code && c < distinct; ++c) {
+    h.exp_of_code[c] = (uint8_t)order[c];
+    code[order[c]] = (uint8_t)c;
   }
   const uint64_t nf = (n + F - 1) / F;
   uint64_t* off = (uint64_t*)calloc(nf + 1, 8);
@@ -69,8 +88,8 @@ int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst,
   for (uint64_t f = 0; f < nf; ++f) {
     const uint64_t e0 = f * F, m = (n - e0 < F) ? n - e0 : F;
     uint64_t esc = 0, oe, os;
-    for (uint64_t i = 0; i < m; ++i) esc += code[expo(src[e0 + i])] == 15;
-    geom(m, &oe, &os);
+    for (uint64_t i = 0; i < m; ++i) esc += code[expo(src[e0 + i])] == esc_code;
+    geom(m, bits, &oe, &os);
     off[f] = pos;
     pos += up(os + esc, 256);
     esc_total += esc;
@@ -87,7 +106,7 @@ int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst,
   }
   memset(dst, 0, pos);
   h.magic = XC4_MAGIC;
-  h.version = 1;
+  h.version = bits == 3 ? 2 : 1;
   h.n_elems = n;
   h.frame_elems = F;
   h.n_frames = (uint32_t)nf;
@@ -98,7 +117,7 @@ int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst,
   for (uint64_t f = 0; f < nf; ++f) {
     const uint64_t e0 = f * F, m = (n - e0 < F) ? n - e0 : F;
     uint64_t oe, os;
-    geom(m, &oe, &os);
+    geom(m, bits, &oe, &os);
     uint8_t* fr = dst + off[f];
     int32_t* eo = (int32_t*)(fr + oe);
     int32_t k = 0;
@@ -107,8 +126,9 @@ int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst,
       if (i % XC4_BLOCK == 0) eo[i / XC4_BLOCK] = k;
       fr[i] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
       const uint8_t c = code[expo(v)];
-      fr[m + i / 2] |= (uint8_t)(c << (4 * (i & 1)));
-      if (c == 15) fr[os + k++] = expo(v);
+      for (int b = 0; b < bits; ++b)  /* code bit b of element i → stream bit bits·i + b */
+        if ((c >> b) & 1) fr[m + (bits * i + b) / 8] |= (uint8_t)(1u << ((bits * i + b) % 8));
+      if (c == esc_code) fr[os + k++] = expo(v);
     }
     eo[(m + XC4_BLOCK - 1) / XC4_BLOCK] = k;
   }
@@ -120,18 +140,21 @@ int oracle_xc4_encode(const uint16_t* src, uint64_t n, uint32_t F, uint8_t* dst,
 int oracle_xc4_decode(const uint8_t* unit, uint16_t* dst) {
   xc4_header h;
   memcpy(&h, unit, sizeof h);
-  if (h.magic != XC4_MAGIC || h.version != 1) return -2;
+  if (h.magic != XC4_MAGIC || (h.version != 1 && h.version != 2)) return -2;
+  const int bits = h.version == 2 ? 3 : 4;
+  const uint8_t esc_code = (uint8_t)((1u << bits) - 1);
   const uint64_t* off = (const uint64_t*)(unit + sizeof h);
   for (uint64_t f = 0; f < h.n_frames; ++f) {
     const uint64_t e0 = f * h.frame_elems, m = (h.n_elems - e0 < h.frame_elems) ? h.n_elems - e0 : h.frame_elems;
     uint64_t oe, os;
-    geom(m, &oe, &os);
+    geom(m, bits, &oe, &os);
     const uint8_t* fr = unit + off[f];
     uint64_t k = 0;
     for (uint64_t i = 0; i < m; ++i) {
       const uint8_t sm = fr[i];
-      const uint8_t c = (fr[m + i / 2] >> (4 * (i & 1))) & 0xf;
-      const uint8_t e = c == 15 ? fr[os + k++] : h.exp_of_code[c];
+      uint8_t c = 0;
+      for (int b = 0; b < bits; ++b) c |= (uint8_t)(((fr[m + (bits * i + b) / 8] >> ((bits * i + b) % 8)) & 1) << b);
+      const uint8_t e = c == esc_code ? fr[os + k++] : h.exp_of_code[c];
       dst[e0 + i] = (uint16_t)(((sm & 0x80) << 8) | (e << 7) | (sm & 0x7f));
     }
   }

@@ -29,21 +29,23 @@ def _l():
             subprocess.run(["make", "-s", "-C", _HERE], check=True)
         _lib = ctypes.CDLL(_SO)
         P = ctypes.c_void_p
-        _lib.oracle_xc4_encode.argtypes = [P, ctypes.c_uint64, ctypes.c_uint32, P, ctypes.c_uint64,
+        _lib.oracle_xc4_encode.argtypes = [P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, P, ctypes.c_uint64,
                                            ctypes.POINTER(ctypes.c_uint64)]
         _lib.oracle_xc4_decode.argtypes = [P, P]
     return _lib
 
 
-def encode(w: np.ndarray, frame_elems: int) -> np.ndarray:
-    """bf16 bit patterns (uint16, 1-D) → encoded unit bytes (uint8)."""
+def encode(w: np.ndarray, frame_elems: int, bits: int = 0) -> np.ndarray:
+    """bf16 bit patterns (uint16, 1-D) → encoded unit bytes (uint8); bits 0 =
+    the smaller of 3- and 4-bit codes, else forced."""
     w = np.ascontiguousarray(w, dtype=np.uint16)
     n = ctypes.c_uint64()
-    rc = _l().oracle_xc4_encode(w.ctypes.data, w.size, frame_elems, None, 0, ctypes.byref(n))
+    rc = _l().oracle_xc4_encode(w.ctypes.data, w.size, frame_elems, bits, None, 0, ctypes.byref(n))
     if rc:
         raise ValueError(f"oracle_xc4_encode: bad geometry (rc {rc})")
     out = np.zeros(n.value, dtype=np.uint8)
-    rc = _l().oracle_xc4_encode(w.ctypes.data, w.size, frame_elems, out.ctypes.data, out.size, ctypes.byref(n))
+    rc = _l().oracle_xc4_encode(w.ctypes.data, w.size, frame_elems, bits, out.ctypes.data, out.size,
+                                ctypes.byref(n))
     assert rc == 0
     return out
 

@@ -21,7 +21,7 @@ import torch
 
 from . import native
 
-MAX_FRAME_ELEMS = 1 << 25   # 32 Mi weights → ≈48 MB encoded per frame
+MAX_FRAME_ELEMS = 1 << 27   # ≤ 128 Mi weights (≈180 MB encoded) per frame: few copy/decode launches per layer
 MIN_FRAME_ELEMS = 4096
 SLICE_WORLD = 8             # frames split evenly over 1, 2, 4 or 8 ranks when the unit allows it
 
@@ -56,16 +56,19 @@ class XC4Unit:
     n_frames: int
     frame_off: np.ndarray       # uint64 [n_frames + 1]
     n_escapes: int
+    code_bits: int = 4
+
 
     @classmethod
     def parse(cls, data: torch.Tensor) -> "XC4Unit":
         raw = bytes(data[:64].numpy()) if data.device.type == "cpu" else bytes(data[:64].cpu().numpy())
         h = native.XC4Header.from_buffer_copy(raw)
-        if h.magic != 0x31344358 or h.version != 1:
+        if h.magic != 0x31344358 or h.version not in (1, 2):
             raise ValueError("not an XC4 unit")
         tab = data[64:64 + 8 * (h.n_frames + 1)]
         off = np.frombuffer(bytes(tab.cpu().numpy()), dtype=np.uint64).copy()
-        return cls(data, int(h.n_elems), int(h.frame_elems), int(h.n_frames), off, int(h.n_escapes))
+        return cls(data, int(h.n_elems), int(h.frame_elems), int(h.n_frames), off, int(h.n_escapes),
+                   3 if h.version == 2 else 4)
 
     @property
     def nbytes(self) -> int:
@@ -95,9 +98,10 @@ class XC4Unit:
 class Encoder:
     """Device-side XC4 encoder with grow-only scratch (setup time only)."""
 
-    def __init__(self, device, world: int = SLICE_WORLD):
+    def __init__(self, device, world: int = SLICE_WORLD, code_bits: int = 0):
         self.device = torch.device(device)
         self.world = world
+        self.code_bits = code_bits  # 0 = per unit, the smaller of 3- and 4-bit codes
         self._scratch = None
         self._dst = None
 
@@ -118,9 +122,9 @@ class Encoder:
         n = flat.numel()
         fe = frame_elems_for(n, self.world)
         scratch = self._grow("_scratch", native.xc4_scratch_bytes(n, fe))
-        nbytes, _ = native.xc4_encode(flat, fe, None, scratch)
+        nbytes, _ = native.xc4_encode(flat, fe, None, scratch, code_bits=self.code_bits)
         dst = self._grow("_dst", nbytes)
-        nbytes, h = native.xc4_encode(flat, fe, dst, scratch)
+        nbytes, h = native.xc4_encode(flat, fe, dst, scratch, code_bits=self.code_bits)
         return dst[:nbytes], h
 
     def release(self) -> None:

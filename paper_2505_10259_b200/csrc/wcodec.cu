@@ -5,28 +5,31 @@
 // ffn_bytes / c2g_bandwidth).  A bf16 weight is sign(1) ·
 // exponent(8) · mantissa(7), and the exponents of a trained (or N(0, σ²)
 // initialised) matrix crowd into a few binades.  XC4 keeps sign+mantissa as
-// one raw byte and replaces the exponent by a 4-bit code: codes 0..14 name the
-// unit's 15 most frequent exponents, code 15 escapes to a raw exponent byte in
-// a side stream.  12 bits per weight instead of 16 (0.75 of the bytes on the
-// link) and the decoded bytes are bit-identical to the source, so every
-// kernel downstream sees exactly the reference's weights.
+// one raw byte and replaces the exponent by a fixed-width code naming one of
+// the unit's most frequent exponents; the all-ones code escapes to a raw
+// exponent byte in a side stream.  Two widths (header version):
+//   v1  4-bit codes: 15 exponents + escape   12 bits/weight (0.750 of bf16)
+//   v2  3-bit codes:  7 exponents + escape   11 bits/weight + 8 per escape
+//       (N(0, 0.02²): 2.1% escapes → 0.698 of bf16)
+// The encoder takes the smaller for the unit.  Decoded bytes are bit-identical
+// to the source, so every kernel downstream sees exactly the reference's weights.
 //
 // Unit layout (all offsets from the unit start; so_xc4_header in the header):
 //   header (64 B) | frame_off u64[n_frames+1] | frames, each 256-B aligned.
 // Frame of m elements (nb = ceil(m/4096) blocks of 4096):
-//   sm  u8[m]       (sign << 7) | mantissa           byte i = element i
-//   ec  u8[m/2]     4-bit codes, element 2j in the low nibble of byte j
-//   eo  i32[nb+1]   frame-local escape prefix per block (16-B aligned start)
-//   esc u8[...]     raw exponents of escaped elements, in element order
+//   sm  u8[m]        (sign << 7) | mantissa           byte i = element i
+//   ec  u8[m·b/8]    b-bit codes, element i at bit b·i (little-endian stream)
+//   eo  i32[nb+1]    frame-local escape prefix per block (16-B aligned start)
+//   esc u8[...]      raw exponents of escaped elements, in element order
 // Code table rule (normative; oracle/csrc/xc4_oracle.c restates it): the
 // exponents present in the unit sorted by (count desc, exponent asc); the
-// first ≤15 get codes 0.., unused table entries are 0.
+// first ≤ 2^b − 1 get codes 0.., unused table entries are 0.
 //
-// Decode (HBM-bound: 1.5 B read + 2 B written per weight): one warp per
-// 4096-element block (grid-stride), 8 weights per lane per step so every load
-// and store instruction of a warp is one contiguous run; the exponent lookup
-// is two PRMT byte permutes over the register-resident table plus a select,
-// and escapes are consumed with a warp scan (no CTA barrier).
+// Decode (HBM-bound: (1 + b/8) B read + 2 B written per weight): one warp per
+// 4096-element block (grid-stride), 16 (v1) or 32 (v2) weights per lane per
+// step so every load and store instruction of a warp is one contiguous run;
+// codes become 4 exponents per PRMT byte permute over the register-resident
+// table, and escapes are consumed with a warp scan (no CTA barrier).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -45,9 +48,9 @@ struct FrameGeom {
   size_t off_eo, off_esc;  // byte offsets inside the frame
 };
 
-__host__ __device__ inline FrameGeom frame_geom(uint32_t m) {
+__host__ __device__ inline FrameGeom frame_geom(uint32_t m, int bits) {
   FrameGeom g;
-  g.off_eo = align_up((size_t)m + m / 2, 16);
+  g.off_eo = align_up((size_t)m + (size_t)m * bits / 8, 16);
   g.off_esc = g.off_eo + 4 * ((size_t)(m + kBlock - 1) / kBlock + 1);
   return g;
 }
@@ -118,13 +121,13 @@ __device__ __forceinline__ uint2 ld_nc8(const void* p) {
   return v;
 }
 
-// One warp decodes one 4096-weight block: 8 steps of 512 weights, lane l
-// owning weights [512i + 16l, +16) of step i: a 16-B sign/mantissa load, an
-// 8-B code load and one 32-B (256-bit) store per lane, each a contiguous run
-// across the warp.  Escapes (stored in element order) are consumed step by
-// step with a warp-level scan — no CTA barrier anywhere.
+// One warp decodes one 4096-weight block.  v1: 8 steps of 512 weights, lane l
+// owning weights [512i + 16l, +16): a 16-B sign/mantissa load, an 8-B code
+// load, one 32-B (256-bit) store.  v2: 4 steps of 1024 weights, lane l owning
+// [1024i + 32l, +32): a 32-B load, three 4-B code loads, two 32-B stores.
+// Escapes (stored in element order) are consumed step by step with a
+// warp-level scan — no CTA barrier anywhere.
 constexpr int kWarpsPerCta = kThreads / 32;
-constexpr int kStepsAhead = 4;  // steps whose loads are in flight together (96 B per lane)
 
 __device__ __forceinline__ void st_v8(void* p, const uint32_t* o) {
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(o[0]), "r"(o[1]), "r"(o[2]),
@@ -132,10 +135,47 @@ __device__ __forceinline__ void st_v8(void* p, const uint32_t* o) {
                : "memory");
 }
 
+__device__ __forceinline__ void ld_nc32(const void* p, uint32_t* v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ uint32_t ld_nc4(const void* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// eight 3-bit fields (bits 0..23) → eight nibbles
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {
+  uint32_t y = (x & 0xfffu) | ((x & 0xfff000u) << 4);  // fields 0-3 at bit 0, 4-7 at bit 16
+  return (y & 0x00070007u) | ((y & 0x00380038u) << 1) | ((y & 0x01c001c0u) << 2) | ((y & 0x0e000e00u) << 3);
+}
+
+// nibble mask (bit 4k) of codes equal to `esc` (0xF for v1, 0x7 for v2)
+template <int BITS>
+__device__ __forceinline__ uint32_t escape_mask(uint32_t nib) {
+  if constexpr (BITS == 4) return nib & (nib >> 1) & (nib >> 2) & (nib >> 3) & 0x11111111u;
+  else return nib & (nib >> 1) & (nib >> 2) & ~(nib >> 3) & 0x11111111u;
+}
+
+// 4 codes (nibbles of s, low 16 bits) → 4 exponent bytes
+template <int BITS>
+__device__ __forceinline__ uint32_t lookup(uint32_t s, uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+  if constexpr (BITS == 4) return lookup4(s, t0, t1, t2, t3);
+  else return prmt(t0, t1, s & 0x7777u);
+}
+
+template <int BITS>
 __global__ void __launch_bounds__(kThreads) xc4_decode_kernel(const uint8_t* __restrict__ frame, uint32_t m,
                                                                uint32_t off_eo, uint32_t off_esc, uint32_t t0,
                                                                uint32_t t1, uint32_t t2, uint32_t t3,
                                                                uint16_t* __restrict__ dst) {
+  constexpr int kLaneElems = BITS == 4 ? 16 : 32;   // weights per lane per step
+  constexpr int kStep = 32 * kLaneElems;
+  constexpr int kAhead = BITS == 4 ? 4 : 2;         // steps whose loads are in flight together
+  constexpr int kNib = kLaneElems / 8;              // nibble words per lane per step
   const int lane = threadIdx.x & 31;
   const uint32_t nb = (m + kBlock - 1) / kBlock;
   const uint32_t stride = gridDim.x * kWarpsPerCta;
@@ -143,28 +183,46 @@ __global__ void __launch_bounds__(kThreads) xc4_decode_kernel(const uint8_t* __r
     const uint8_t* esc = frame + off_esc + reinterpret_cast<const int32_t*>(frame + off_eo)[blk];
     int carry = 0;  // escapes consumed by earlier steps of this block
 #pragma unroll 1
-    for (int s0 = 0; s0 < kBlock / 512; s0 += kStepsAhead) {
-      int4 sm[kStepsAhead];
-      uint2 cd[kStepsAhead];
-      bool live[kStepsAhead];
+    for (int s0 = 0; s0 < kBlock / kStep; s0 += kAhead) {
+      uint32_t sm[kAhead][kLaneElems / 4];
+      uint32_t nib[kAhead][kNib];
+      bool live[kAhead];
 #pragma unroll
-      for (int j = 0; j < kStepsAhead; ++j) {
-        const uint32_t e = blk * kBlock + (s0 + j) * 512 + lane * 16;
+      for (int j = 0; j < kAhead; ++j) {
+        const uint32_t e = blk * kBlock + (s0 + j) * kStep + lane * kLaneElems;
         live[j] = e < m;
-        sm[j] = make_int4(0, 0, 0, 0);
-        cd[j] = make_uint2(0u, 0u);
+#pragma unroll
+        for (int q = 0; q < kLaneElems / 4; ++q) sm[j][q] = 0u;
+#pragma unroll
+        for (int q = 0; q < kNib; ++q) nib[j][q] = 0u;
         if (live[j]) {
-          sm[j] = ld_nc16(frame + e);
-          cd[j] = ld_nc8(frame + m + e / 2);
+          if constexpr (BITS == 4) {
+            const int4 v = ld_nc16(frame + e);
+            sm[j][0] = v.x, sm[j][1] = v.y, sm[j][2] = v.z, sm[j][3] = v.w;
+            const uint2 c = ld_nc8(frame + m + e / 2);
+            nib[j][0] = c.x, nib[j][1] = c.y;
+          } else {
+            ld_nc32(frame + e, sm[j]);
+            const uint8_t* cp = frame + m + (size_t)e * 3 / 8;
+            const uint32_t w0 = ld_nc4(cp), w1 = ld_nc4(cp + 4), w2 = ld_nc4(cp + 8);
+            nib[j][0] = spread3(w0 & 0xffffffu);
+            nib[j][1] = spread3((w0 >> 24) | ((w1 & 0xffffu) << 8));
+            nib[j][2] = spread3((w1 >> 16) | ((w2 & 0xffu) << 16));
+            nib[j][3] = spread3(w2 >> 8);
+          }
         }
       }
 #pragma unroll
-      for (int j = 0; j < kStepsAhead; ++j) {
-        const uint64_t codes = ((uint64_t)cd[j].y << 32) | cd[j].x;
-        const int n = live[j] ? count_escapes(codes) : 0;
-        uint32_t ex[4] = {lookup4(cd[j].x & 0xffffu, t0, t1, t2, t3), lookup4(cd[j].x >> 16, t0, t1, t2, t3),
-                          lookup4(cd[j].y & 0xffffu, t0, t1, t2, t3), lookup4(cd[j].y >> 16, t0, t1, t2, t3)};
-        if (__any_sync(0xffffffffu, n)) {  // rare: patch escaped exponents from the side stream
+      for (int j = 0; j < kAhead; ++j) {
+        uint32_t ex[kLaneElems / 4];
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < kNib; ++q) {
+          ex[2 * q] = lookup<BITS>(nib[j][q] & 0xffffu, t0, t1, t2, t3);
+          ex[2 * q + 1] = lookup<BITS>(nib[j][q] >> 16, t0, t1, t2, t3);
+          n += live[j] ? __popc(escape_mask<BITS>(nib[j][q])) : 0;
+        }
+        if (__any_sync(0xffffffffu, n)) {  // patch escaped exponents from the side stream
           int inc = n;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -172,27 +230,32 @@ __global__ void __launch_bounds__(kThreads) xc4_decode_kernel(const uint8_t* __r
             if (lane >= o) inc += y;
           }
           if (n) {
-            const uint8_t* q = esc + carry + inc - n;
-            int k = 0;
-#pragma unroll 1
-            for (int i = 0; i < 16; ++i) {
-              if (((codes >> (4 * i)) & 0xfu) == 0xfu) {
-                const uint32_t sh = 8 * (i & 3);
-                ex[i >> 2] = (ex[i >> 2] & ~(0xffu << sh)) | ((uint32_t)q[k++] << sh);
+            const uint8_t* q8 = esc + carry + inc - n;
+#pragma unroll
+            for (int q = 0; q < kNib; ++q) {
+              uint32_t mk = escape_mask<BITS>(nib[j][q]);
+              while (mk) {  // set bit 4k ↔ weight 8q + k escaped
+                const int k = (__ffs(mk) - 1) >> 2;
+                const int w = 2 * q + (k >> 2), sh = 8 * (k & 3);
+                ex[w] = (ex[w] & ~(0xffu << sh)) | ((uint32_t)*q8++ << sh);
+                mk &= mk - 1;
               }
             }
           }
           carry += __shfl_sync(0xffffffffu, inc, 31);
         }
         if (live[j]) {
-          const uint32_t sw[4] = {(uint32_t)sm[j].x, (uint32_t)sm[j].y, (uint32_t)sm[j].z, (uint32_t)sm[j].w};
-          uint32_t o[8];
+          uint16_t* out = dst + blk * kBlock + (s0 + j) * kStep + lane * kLaneElems;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            o[2 * w] = assemble2(prmt(sw[w], 0u, 0x5150u), prmt(ex[w], 0u, 0x5150u));
-            o[2 * w + 1] = assemble2(prmt(sw[w], 0u, 0x5352u), prmt(ex[w], 0u, 0x5352u));
+          for (int h = 0; h < kLaneElems / 16; ++h) {
+            uint32_t o[8];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              o[2 * w] = assemble2(prmt(sm[j][4 * h + w], 0u, 0x5150u), prmt(ex[4 * h + w], 0u, 0x5150u));
+              o[2 * w + 1] = assemble2(prmt(sm[j][4 * h + w], 0u, 0x5352u), prmt(ex[4 * h + w], 0u, 0x5352u));
+            }
+            st_v8(out + 16 * h, o);
           }
-          st_v8(dst + blk * kBlock + (s0 + j) * 512 + lane * 16, o);
         }
       }
     }
@@ -225,7 +288,7 @@ __global__ void xc4_hist_kernel(const uint16_t* __restrict__ src, uint64_t n, un
 
 // per 4096-block escape counts over the whole unit (frames hold whole blocks)
 __global__ void __launch_bounds__(kThreads) xc4_count_kernel(const uint16_t* __restrict__ src, uint64_t n,
-                                                              const uint8_t* __restrict__ code_of_exp,
+                                                              const uint8_t* __restrict__ code_of_exp, uint32_t esc,
                                                               int32_t* __restrict__ cnt) {
   __shared__ uint8_t cx[256];
   cx[threadIdx.x] = code_of_exp[threadIdx.x];
@@ -237,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) xc4_count_kernel(const uint16_t* __r
     const uint32_t w[8] = {(uint32_t)a.x, (uint32_t)a.y, (uint32_t)a.z, (uint32_t)a.w,
                            (uint32_t)b.x, (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c += (cx[(w[k] >> 7) & 0xffu] == 15) + (cx[(w[k] >> 23) & 0xffu] == 15);
+    for (int k = 0; k < 8; ++k) c += (cx[(w[k] >> 7) & 0xffu] == esc) + (cx[(w[k] >> 23) & 0xffu] == esc);
   }
   __shared__ int s_warp[kThreads / 32];
   int total;
@@ -263,6 +326,7 @@ __global__ void xc4_scan_kernel(const int32_t* __restrict__ cnt, uint64_t n_bloc
   }
 }
 
+template <int BITS>
 __global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __restrict__ src, uint64_t n,
                                                               const uint8_t* __restrict__ code_of_exp,
                                                               const int32_t* __restrict__ eo,
@@ -277,7 +341,8 @@ __global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __r
   const uint32_t f = (uint32_t)(gb / bpf), bl = (uint32_t)(gb % bpf);
   const uint64_t f_e0 = (uint64_t)f * frame_elems;
   const uint32_t m = (uint32_t)(n - f_e0 < frame_elems ? n - f_e0 : frame_elems);
-  const FrameGeom g = frame_geom(m);
+  const FrameGeom g = frame_geom(m, BITS);
+  constexpr uint32_t kEsc = (1u << BITS) - 1;
   uint8_t* fr = dst + frame_off[f];
   const int32_t* feo = eo + (uint64_t)f * (bpf + 1);
   const uint32_t e0 = bl * kBlock + threadIdx.x * 16;  // frame-local
@@ -294,8 +359,8 @@ __global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __r
       ex[i] = (uint8_t)((v >> 7) & 0xffu);
       sm[i] = (uint8_t)(((v >> 8) & 0x80u) | (v & 0x7fu));
       const uint64_t c = cx[ex[i]];
-      codes |= c << (4 * i);
-      nesc += c == 15;
+      codes |= c << (BITS * i);
+      nesc += c == kEsc;
     }
     int4 smv;
     uint32_t* sw = reinterpret_cast<uint32_t*>(&smv);
@@ -303,7 +368,14 @@ __global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __r
     for (int w = 0; w < 4; ++w)
       sw[w] = sm[4 * w] | (sm[4 * w + 1] << 8) | (sm[4 * w + 2] << 16) | ((uint32_t)sm[4 * w + 3] << 24);
     *reinterpret_cast<int4*>(fr + e0) = smv;
-    *reinterpret_cast<uint2*>(fr + m + e0 / 2) = make_uint2((uint32_t)codes, (uint32_t)(codes >> 32));
+    if constexpr (BITS == 4) {
+      *reinterpret_cast<uint2*>(fr + m + e0 / 2) = make_uint2((uint32_t)codes, (uint32_t)(codes >> 32));
+    } else {  // 48 bits at byte 6·(e0/16): three 2-B stores
+      uint16_t* cp = reinterpret_cast<uint16_t*>(fr + m + (size_t)e0 * 3 / 8);
+      cp[0] = (uint16_t)codes;
+      cp[1] = (uint16_t)(codes >> 16);
+      cp[2] = (uint16_t)(codes >> 32);
+    }
   }
   int total;
   const int pre = block_exclusive_scan(nesc, s_warp, total);
@@ -311,7 +383,7 @@ __global__ void __launch_bounds__(kThreads) xc4_write_kernel(const uint16_t* __r
     uint8_t* esc = fr + g.off_esc + feo[bl] + pre;
     int k = 0;
     for (int i = 0; i < 16; ++i)
-      if (((codes >> (4 * i)) & 0xfu) == 0xfu) esc[k++] = ex[i];
+      if (((codes >> (BITS * i)) & kEsc) == kEsc) esc[k++] = ex[i];
   }
   if (threadIdx.x == 0) {
     int32_t* out_eo = reinterpret_cast<int32_t*>(fr + g.off_eo);
@@ -339,6 +411,8 @@ ScratchLayout scratch_layout(uint64_t n, uint32_t frame_elems) {
   return s;
 }
 
+int bits_of(const so_xc4_header* h) { return h->version == 2 ? 3 : 4; }
+
 bool valid_geometry(uint64_t n, uint32_t frame_elems) {
   return n > 0 && n % 16 == 0 && frame_elems >= (uint32_t)kBlock && frame_elems % kBlock == 0;
 }
@@ -358,15 +432,18 @@ extern "C" size_t so_xc4_bound(uint64_t n_elems, uint32_t frame_elems) {
   size_t b = header_bytes(nf);
   for (uint64_t f = 0; f < nf; ++f) {
     const uint32_t m = (uint32_t)std::min<uint64_t>(frame_elems, n_elems - f * frame_elems);
-    b += align_up(frame_geom(m).off_esc + m, 256);
+    b += align_up(frame_geom(m, 4).off_esc + m, 256);
   }
   return b;
 }
 
-extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, void* dst, size_t dst_cap,
-                             void* scratch, uint64_t* out_bytes, so_xc4_header* out_header, void* stream) {
+extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_elems, int code_bits, void* dst,
+                             size_t dst_cap, void* scratch, uint64_t* out_bytes, so_xc4_header* out_header,
+                             void* stream) {
   SO_REQUIRE(src && scratch && out_bytes, SO_E_NULLPTR);
   SO_REQUIRE(valid_geometry(n_elems, frame_elems), SO_E_SHAPE);
+  SO_REQUIRE(code_bits == 0 || code_bits == 3 || code_bits == 4, SO_E_SHAPE);
+  SO_REQUIRE(code_bits != 3 || n_elems % 32 == 0, SO_E_SHAPE);
   SO_REQUIRE(aligned16(src), SO_E_ALIGN);
   cudaStream_t st = as_stream(stream);
   const ScratchLayout L = scratch_layout(n_elems, frame_elems);
@@ -394,24 +471,39 @@ extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_e
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return (int)e;
   so_xc4_header hdr;
   memset(&hdr, 0, sizeof(hdr));
-  uint8_t code_of_exp[256];
-  memset(code_of_exp, 15, sizeof(code_of_exp));
+  // exponents by (count desc, exponent asc)
+  int order[256], n_present = 0;
   {
     bool used[256] = {false};
-    for (int c = 0; c < 15; ++c) {
+    for (;;) {
       int best = -1;
       for (int x = 0; x < 256; ++x)
         if (!used[x] && h[x] > 0 && (best < 0 || h[x] > h[best])) best = x;  // ties → lower exponent
       if (best < 0) break;
       used[best] = true;
-      hdr.exp_of_code[c] = (uint8_t)best;
-      code_of_exp[best] = (uint8_t)c;
+      order[n_present++] = best;
     }
+  }
+  // width: the smaller encoding (3-bit needs whole 32-weight lane groups)
+  int bits = code_bits;
+  if (bits == 0) {
+    unsigned long long top7 = 0, top15 = 0;
+    for (int i = 0; i < n_present && i < 15; ++i) (i < 7 ? top7 : top15) += h[order[i]];
+    top15 += top7;
+    const unsigned long long esc7 = n_elems - top7, esc15 = n_elems - top15;
+    bits = (n_elems % 32 == 0 && 11ull * n_elems + 8ull * esc7 < 12ull * n_elems + 8ull * esc15) ? 3 : 4;
+  }
+  const uint8_t esc_code = (uint8_t)((1u << bits) - 1);
+  uint8_t code_of_exp[256];
+  memset(code_of_exp, esc_code, sizeof(code_of_exp));
+  for (int c = 0; c < esc_code && c < n_present; ++c) {
+    hdr.exp_of_code[c] = (uint8_t)order[c];
+    code_of_exp[order[c]] = (uint8_t)c;
   }
   if ((e = cudaMemcpyAsync(code, code_of_exp, 256, cudaMemcpyHostToDevice, st)) != cudaSuccess) return (int)e;
 
   // 2. escapes per block, per-frame prefixes, frame sizes
-  xc4_count_kernel<<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, cnt);
+  xc4_count_kernel<<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, esc_code, cnt);
   SO_CHECK_LAUNCH();
   xc4_scan_kernel<<<(unsigned)nf, 32, 0, st>>>(cnt, nb, frame_elems / kBlock, eo, tot);
   SO_CHECK_LAUNCH();
@@ -433,13 +525,13 @@ extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_e
   for (uint64_t f = 0; f < nf; ++f) {
     const uint32_t m = (uint32_t)std::min<uint64_t>(frame_elems, n_elems - f * frame_elems);
     off_host[f] = pos;
-    pos += align_up(frame_geom(m).off_esc + t_host[f], 256);
+    pos += align_up(frame_geom(m, bits).off_esc + t_host[f], 256);
     n_esc += t_host[f];
   }
   off_host[nf] = pos;
   free(t_host);
   hdr.magic = kMagic;
-  hdr.version = 1;
+  hdr.version = bits == 3 ? 2 : 1;
   hdr.n_elems = n_elems;
   hdr.frame_elems = frame_elems;
   hdr.n_frames = (uint32_t)nf;
@@ -474,7 +566,10 @@ extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_e
     free(head);
     return (int)e;
   }
-  xc4_write_kernel<<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, eo, foff, frame_elems, d);
+  if (bits == 3)
+    xc4_write_kernel<3><<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, eo, foff, frame_elems, d);
+  else
+    xc4_write_kernel<4><<<(unsigned)nb, kThreads, 0, st>>>(s16, n_elems, code, eo, foff, frame_elems, d);
   cudaError_t le = cudaGetLastError();
   e = cudaStreamSynchronize(st);  // host staging buffers must outlive the copies
   free(off_host);
@@ -485,7 +580,8 @@ extern "C" int so_xc4_encode(const void* src, uint64_t n_elems, uint32_t frame_e
 
 namespace {
 inline bool header_ok(const so_xc4_header* h) {
-  return h->magic == kMagic && h->version == 1 && valid_geometry(h->n_elems, h->frame_elems) &&
+  return h->magic == kMagic && (h->version == 1 || (h->version == 2 && h->n_elems % 32 == 0)) &&
+         valid_geometry(h->n_elems, h->frame_elems) &&
          h->n_frames == (h->n_elems + h->frame_elems - 1) / h->frame_elems;
 }
 inline const uint64_t* frame_table(const void* unit_host) {
@@ -500,7 +596,7 @@ inline int launch_decode(const so_xc4_header* h, uint32_t f, const uint8_t* fram
                          cudaStream_t st) {
   const uint64_t e_begin = (uint64_t)f * h->frame_elems;
   const uint32_t m = (uint32_t)std::min<uint64_t>(h->frame_elems, h->n_elems - e_begin);
-  const FrameGeom g = frame_geom(m);
+  const FrameGeom g = frame_geom(m, bits_of(h));
   uint32_t t[4];
   table_words(h, t);
   static int ctas = 0;  // 8 resident CTAs (64 warps) per SM, grid-stride over the rest
@@ -511,9 +607,14 @@ inline int launch_decode(const so_xc4_header* h, uint32_t f, const uint8_t* fram
     ctas = 8 * sms;
   }
   const uint32_t need = (m + kBlock * kWarpsPerCta - 1) / (kBlock * kWarpsPerCta);
-  xc4_decode_kernel<<<need < (uint32_t)ctas ? need : (uint32_t)ctas, kThreads, 0, st>>>(
-      frame_dev, m, (uint32_t)g.off_eo, (uint32_t)g.off_esc, t[0], t[1], t[2], t[3],
-      reinterpret_cast<uint16_t*>(dst_unit) + e_begin);
+  const uint32_t grid = need < (uint32_t)ctas ? need : (uint32_t)ctas;
+  uint16_t* out = reinterpret_cast<uint16_t*>(dst_unit) + e_begin;
+  if (h->version == 2)
+    xc4_decode_kernel<3><<<grid, kThreads, 0, st>>>(frame_dev, m, (uint32_t)g.off_eo, (uint32_t)g.off_esc, t[0], t[1],
+                                                    t[2], t[3], out);
+  else
+    xc4_decode_kernel<4><<<grid, kThreads, 0, st>>>(frame_dev, m, (uint32_t)g.off_eo, (uint32_t)g.off_esc, t[0], t[1],
+                                                    t[2], t[3], out);
   SO_CHECK_LAUNCH();
   return SO_OK;
 }

@@ -62,7 +62,7 @@ _SIGNATURES = {
     "so_scatter_i32": (c_int, [_P, _P, _P, c_int, _P]),
     "so_xc4_scratch_bytes": (c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
     "so_xc4_bound": (c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
-    "so_xc4_encode": (c_int, [_P, ctypes.c_uint64, ctypes.c_uint32, _P, c_size_t, _P,
+    "so_xc4_encode": (c_int, [_P, ctypes.c_uint64, ctypes.c_uint32, c_int, _P, c_size_t, _P,
                               ctypes.POINTER(ctypes.c_uint64), _P, _P]),
     "so_xc4_decode": (c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, _P, _P]),
     "so_xc4_stream": (c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, _P, c_size_t, c_int, _P,
@@ -360,14 +360,15 @@ def xc4_bound(n_elems: int, frame_elems: int) -> int:
     return int(lib().so_xc4_bound(n_elems, frame_elems))
 
 
-def xc4_encode(src, frame_elems: int, dst, scratch, stream=None) -> tuple[int, XC4Header]:
+def xc4_encode(src, frame_elems: int, dst, scratch, stream=None, code_bits: int = 0) -> tuple[int, XC4Header]:
     """Encode bf16 ``src`` (device) into ``dst`` (device uint8, or None for a
-    size query).  Returns (encoded bytes, header).  Synchronises the stream."""
+    size query).  ``code_bits`` 0 = smaller of 3/4-bit codes, else forced.
+    Returns (encoded bytes, header).  Synchronises the stream."""
     assert src.dtype in (torch.bfloat16, torch.int16, torch.uint16) and src.is_cuda and src.is_contiguous()
     n = ctypes.c_uint64()
     h = XC4Header()
     cap = dst.numel() if dst is not None else 0
-    _check(lib().so_xc4_encode(_ptr(src), src.numel(), frame_elems, _ptr(dst), cap, _ptr(scratch),
+    _check(lib().so_xc4_encode(_ptr(src), src.numel(), frame_elems, code_bits, _ptr(dst), cap, _ptr(scratch),
                                ctypes.byref(n), ctypes.byref(h), _stream(stream)), "so_xc4_encode")
     return int(n.value), h
 
