@@ -58,6 +58,8 @@ def parse():
                     help="profiling only: cap the planner's HBM-pinned layers (-1 = planner)")
     ap.add_argument("--draft-cached", type=int, default=-1,
                     help="mixed draft KV: cached sequences per batch (-1 = planner)")
+    ap.add_argument("--no-shards", action="store_true",
+                    help="N > 1: stream every non-pinned layer over the host links (no HBM-sharded layers, §8 f3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
@@ -68,6 +70,9 @@ def parse():
     ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
                     help="streamed units XC4-encoded in host DRAM (K9, lossless) or raw bf16")
     return ap.parse_args()
+
+
+NVLINK_PEER_BPS = 770e9  # B200_PROFILING.md: measured NVLink 5 peer copy per direction
 
 
 def mem_available() -> int:
@@ -187,7 +192,7 @@ def main():
     from paper_2505_10259_b200.api import build_engine
     from paper_2505_10259_b200.planner_b200 import plan_offload, roofline_tokens_per_s, verify_flops
     from paper_2505_10259_b200.streamer import HostStore
-    from paper_2505_10259_b200.weights import ffn_offsets
+    from paper_2505_10259_b200.weights import ffn_offsets, unit_layout
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
@@ -228,18 +233,21 @@ def main():
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
-                        draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached])
+                        draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
+                        world=world, allow_shards=not args.no_shards)
     t_setup = time.perf_counter()
     layer_bytes = ffn_offsets(tgt)[2]
     if world > 1:
         from paper_2505_10259_b200.streamer import SharedHostStore
 
-        cap = layer_bytes if args.codec == "none" else -(-int(layer_bytes * (ratio + 0.005)) // (2 << 20)) * (2 << 20)
+        unit_bytes = unit_layout(tgt, plan.stream_attn)[1]
+        cap = unit_bytes if args.codec == "none" else -(-int(unit_bytes * (ratio + 0.005)) // (2 << 20)) * (2 << 20)
         store = SharedHostStore(f"specoffload_{os.environ.get('MASTER_PORT', '0')}", list(plan.stream_layers),
-                                cap, rank, world, barrier=dist.barrier, coded=args.codec != "none")
+                                cap, rank, world, barrier=dist.barrier,
+                                coded=args.codec != "none") if plan.stream_layers else None
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
                            seed=1, trace=bool(args.trace_out), rank=rank, world=world, shared_store=store,
-                           stream_attn=plan.stream_attn, codec=args.codec)
+                           stream_attn=plan.stream_attn, codec=args.codec, shard_layers=set(plan.shard_layers))
         dist.barrier()  # every slice of the shared store is written
     else:
         store = HostStore()
@@ -264,6 +272,7 @@ def main():
     st = eng.target.streamer
     bytes0 = st.bytes_issued if st else 0
     raw0 = st.raw_bytes_issued if st else 0
+    nvl0 = st.nvlink_bytes_issued if st else 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if eng.tracer.enabled:
@@ -290,6 +299,7 @@ def main():
     committed = s.committed_decode - committed0
     streamed = (st.bytes_issued - bytes0) if st else 0       # bytes over this rank's link
     streamed_raw = (st.raw_bytes_issued - raw0) if st else 0  # layer bytes they delivered
+    nvl = (st.nvlink_bytes_issued - nvl0) if st else 0       # bytes this rank received from HBM shards
     launches = dict(native.launches)
     if world > 1:
         t = torch.tensor([dev_s, wall], device=device, dtype=torch.float64)
@@ -308,6 +318,11 @@ def main():
     F = verify_flops(tgt, bs, args.n_cand, args.ctx)
     # north-star roofline: committed tokens over max(link bytes / B_h2d, compute at peak), per round
     roof = roofline_tokens_per_s(bs * e_tok * world, streamed / steps, F, link, peaks["bf16_tflops_sustained"] * 1e12)
+    if world > 1:  # the NVLink all-gathers are a third bound
+        gathered = nvl + (streamed_raw * (world - 1))  # host-streamed slices are all-gathered too
+        t_nvl = gathered / steps / NVLINK_PEER_BPS
+        t_roof = max(streamed / steps / link, t_nvl, F / (peaks["bf16_tflops_sustained"] * 1e12))
+        roof = bs * e_tok * world / t_roof
     roof_raw = roofline_tokens_per_s(bs * e_tok * world, streamed_raw / steps, F, link,
                                      peaks["bf16_tflops_sustained"] * 1e12)
 
@@ -411,7 +426,8 @@ def main():
 
     if world > 1:
         dist.barrier()
-        store.close(unlink=rank == 0)
+        if store is not None:
+            store.close(unlink=rank == 0)
     if rank != 0:
         return
     meta_bytes = bs * (args.n_cand + 1) * 4 * 2 + bs * 4 * 4
@@ -425,17 +441,22 @@ def main():
                    "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
+                   "hbm_sharded_layers": len(plan.shard_layers),
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
                    "streamed_bytes_per_round": int(streamed / steps * world),
                    "streamed_layer_bytes_per_round": len(plan.stream_layers) * layer_bytes,
-                   "host_pinned_bytes": store.bytes, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
+                   "host_pinned_bytes": store.bytes if store is not None else 0, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
                    "parallelism": f"dp{world} (independent prompt shards)", "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "h2d", "achieved": achieved_link / 1e9, "peak": link / 1e9, "unit": "GB/s",
                      "frac": achieved_link / link, "traffic": None,
                      "note": "dominant 'kernel' = copy-engine stream of the streamed layer units (XC4-encoded "
                              "bytes when codec=xc4); peak = pinned 1 GiB H2D measured in this run"},
         "roofline_tokens_per_s": roof, "frac_of_roofline": value / roof if roof else None,
+        "nvlink": ({"received_bytes_per_round": int((nvl + streamed_raw * (world - 1)) / steps),
+                    "achieved_GBps": (nvl + streamed_raw * (world - 1)) / dev_s / 1e9,
+                    "peak_GBps": NVLINK_PEER_BPS / 1e9, "peak_kind": "measured peer copy (B200_PROFILING.md)"}
+                   if world > 1 else None),
         "raw_roofline_tokens_per_s": roof_raw,
         "note_roofline": "roofline_tokens_per_s uses the bytes that crossed the link; raw_roofline_tokens_per_s "
                          "the same rounds if the layers crossed uncompressed (the reference's ffn_bytes)",

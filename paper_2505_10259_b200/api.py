@@ -22,7 +22,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  seed: int = 0, trace: bool = True, page_size: int = 16, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
                  shared_store: SharedHostStore | None = None, stream_attn: bool = False,
-                 codec: str = "none") -> Engine:
+                 codec: str = "none", shard_layers=None) -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
@@ -30,24 +30,30 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     streamed layers live once in ``shared_store`` and each rank pulls its
     1/N slice, reassembled by an NCCL all-gather.
     ``codec="xc4"`` keeps the streamed units XC4-encoded in host DRAM (K9:
-    0.75 of the bytes cross the link, decoded bit-exactly on the GPU)."""
+    0.70–0.75 of the bytes cross the link, decoded bit-exactly on the GPU).
+    ``shard_layers`` (world > 1): layers kept 1/N per GPU in
+    HBM and rebuilt each pass by an NVLink all-gather instead of the host link."""
     if codec not in ("none", "xc4"):
         raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
     if stream_layers is None:
         stream_layers = set(range(target_arch.n_layer))
     stream_layers = set(stream_layers)
+    shard_layers = set(shard_layers or ())
+    if shard_layers and world < 2:
+        raise ValueError("shard_layers needs world > 1")
+    stream_layers -= shard_layers
     enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
     if target_weights is not None:
         tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc)
     elif shared_store is not None:
         sink = shared_store.write_coded if enc is not None else shared_store.write_slice
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=sink,
-                         stream_attn=stream_attn, encoder=enc)
+                         stream_attn=stream_attn, encoder=enc, shard_layers=shard_layers, shard=(rank, world))
     else:
         store = host_store or HostStore()
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc,
-                         stream_attn=stream_attn, encoder=enc)
+                         stream_attn=stream_attn, encoder=enc, shard_layers=shard_layers, shard=(rank, world))
     if enc is not None:
         enc.release()
         torch.cuda.empty_cache()  # hand the encoder's staging back before KV / workspaces are sized
@@ -59,7 +65,8 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
     host = {li: t if isinstance(t, C.XC4Unit) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
-                             chunk_bytes=chunk_bytes, rank=rank, world=world, group=group) if host else None
+                             chunk_bytes=chunk_bytes, rank=rank, world=world, group=group,
+                             shards=tw.shard_ffn) if (host or tw.shard_ffn) else None
     target = TargetModel(tw, dev, streamer)
     draft = DraftModel(dw, dev)
     return Engine(target, draft, device=dev, page_size=page_size, trace=trace)

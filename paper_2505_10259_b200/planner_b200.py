@@ -40,6 +40,9 @@ class B200Rates:
     # (profiles/planner_sweep_r1.md, bs 440 / 48 cached: 3.3 PFLOP in 3.5 s); 0.65 keeps a margin
     tensor_efficiency: float = 0.65
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
+    # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
+    # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin
+    nvlink_bytes_per_s: float = 650e9
 
 
 @dataclasses.dataclass(frozen=True)
@@ -62,11 +65,15 @@ class OffloadPlan:
     stream_attn: bool = False  # attention projections streamed with each layer (H3)
     stream_ratio: float = 1.0  # encoded / raw bytes of a streamed unit (K9 XC4 ≈ 0.75; 1 = raw)
     draft_cached: int = 0      # draft_kv == "mixed": sequences per batch with a persistent draft KV row
+    shard_layers: tuple[int, ...] = ()  # f3 (world > 1): 1/N per GPU in HBM, NVLink all-gather each pass
+    world: int = 1
+    t_nvlink_s: float = 0.0
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
         d["stream_layers"] = len(self.stream_layers)
         d["pinned_layers"] = len(self.pinned_layers)
+        d["shard_layers"] = len(self.shard_layers)
         return d
 
 
@@ -122,14 +129,22 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  n_slots: int = 2, bs_candidates=None, page_size: int = 16,
                  draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
-                 ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None) -> OffloadPlan:
+                 ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,
+                 world: int = 1, allow_shards: bool = True) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
     ``stream_ratio`` < 1: streamed units are kept XC4-encoded (K9) — host DRAM
     and the link carry ratio × the layer bytes, HBM adds the ``ring_bytes``
     staging ring and each pass pays the decode's HBM traffic (1.5 B read +
-    2 B written per weight)."""
+    2 B written per weight).
+
+    ``world`` = N > 1 (per-GPU plan; every GPU runs its own batches, SURVEY.md
+    §8e): host-streamed layers cost each rank 1/N of their bytes on its own
+    link plus an NVLink all-gather; with ``allow_shards`` (§8 f3) layers may
+    instead live 1/N per GPU in HBM and cross only NVLink — the aggregate HBM
+    of N GPUs holds what one GPU's cannot.  Per layer and pass each rank
+    receives (N−1)/N of the layer over NVLink either way."""
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     best = None
@@ -158,33 +173,48 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                 free = hbm_budget - fixed - kv - ws
                 if free < 0:
                     continue
-                pinned = min(target.n_layer, int(free // layer_bytes),
-                             target.n_layer if max_pinned is None else max_pinned)
-                streamed = target.n_layer - pinned
-                if streamed * host_unit > host_budget:
-                    continue
-                S = streamed * host_unit
-                t_stream = S / rates.h2d_bytes_per_s
+                L = target.n_layer
+                cap = L if max_pinned is None else max_pinned
                 eff = rates.tensor_flops * rates.tensor_efficiency
-                t_comp = (verify_flops(target, bs, n_cand, ctx_len)
+                t_base = (verify_flops(target, bs, n_cand, ctx_len)
                           + draft_flops(draft, bs, n_cand, ctx_len, "mixed", kc)) / eff
-                if stream_ratio < 1:
-                    t_comp += streamed * layer_bytes * 1.75 / rates.hbm_bytes_per_s
-                t_round = max(t_stream, t_comp) + rates.round_overhead_s
-                tps = bs * e_tok / t_round
-                if best is None or tps > best[0] * 1.001:
-                    best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
-                            stream_attn, fixed, layer_bytes, kc)
+                p0 = min(L, int(free // layer_bytes), cap)
+                for n_sh in (range(0, L - p0 + 1) if (world > 1 and allow_shards) else (0,)):
+                    room = free - n_sh * layer_bytes / world
+                    if room < 0:
+                        break
+                    pinned = min(L - n_sh, int(room // layer_bytes), cap)
+                    streamed = L - pinned - n_sh
+                    if streamed * host_unit > host_budget:
+                        continue
+                    S = streamed * host_unit // world         # this rank's link bytes per pass
+                    t_stream = S / rates.h2d_bytes_per_s
+                    t_nvl = ((streamed + n_sh) * layer_bytes * (world - 1) / world / rates.nvlink_bytes_per_s
+                             if world > 1 else 0.0)
+                    t_comp = t_base + (streamed * layer_bytes / world * 1.75 / rates.hbm_bytes_per_s
+                                       if stream_ratio < 1 else 0.0)
+                    t_round = max(t_stream, t_nvl, t_comp) + rates.round_overhead_s
+                    tps = bs * e_tok / t_round
+                    if best is None or tps > best[0] * 1.001:
+                        best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
+                                stream_attn, fixed, layer_bytes, kc, n_sh, t_nvl, host_unit)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
-    tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes, kc = best
-    # pin the first layers (ascending order, placement.py:220-231); stream the rest
+    (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes, kc,
+     n_sh, t_nvl, host_unit) = best
+    # pin the first layers (ascending order, placement.py:220-231); among the
+    # rest, host-streamed layers are spread evenly between the sharded ones so
+    # the PCIe link keeps a layer in flight while NVLink gathers the others
     pinned_l = tuple(range(pinned))
-    stream_l = tuple(range(pinned, target.n_layer))
-    return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if streamed else 0,
-                       {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes},
-                       S, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
-                       kc if mode == "mixed" else 0)
+    rest = list(range(pinned, target.n_layer))
+    host_pos = {int((i + 0.5) * len(rest) / streamed) for i in range(streamed)} if streamed else set()
+    stream_l = tuple(li for j, li in enumerate(rest) if j in host_pos)
+    shard_l = tuple(li for j, li in enumerate(rest) if j not in host_pos)
+    return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if rest else 0,
+                       {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes,
+                        "shards": int(n_sh * layer_bytes / world)},
+                       streamed * host_unit, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
+                       kc if mode == "mixed" else 0, shard_l, world, t_nvl)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

@@ -186,6 +186,19 @@ def gather_layer(slot: torch.Tensor, rank: int, world: int, group=None) -> None:
         dist.all_gather(parts, slot[lo:hi].clone(), group=group)
 
 
+def gather_shards(slot: torch.Tensor, shard: torch.Tensor, group=None) -> None:
+    """Rebuild a layer in ``slot`` from every rank's resident 1/N shard (f3).
+    NCCL moves the (N−1)/N foreign bytes over NVLink; gloo (CPU tests) takes
+    the list form."""
+    import torch.distributed as dist
+
+    if slot.is_cuda:
+        dist.all_gather_into_tensor(slot, shard, group=group)
+    else:
+        world = dist.get_world_size(group)
+        dist.all_gather(list(slot.view(world, -1).unbind(0)), shard, group=group)
+
+
 class LayerStreamer:
     """Moves host-resident FFN layers through ``n_slots`` HBM slots.
 
@@ -200,8 +213,16 @@ class LayerStreamer:
 
     def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict,
                  n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False,
-                 rank: int = 0, world: int = 1, group=None):
+                 rank: int = 0, world: int = 1, group=None, shards: dict[int, torch.Tensor] | None = None):
         self.layer_bytes = layer_bytes
+        # layers sharded across the N GPUs' HBM: rank r keeps
+        # bytes slice_bounds(r) of the layer resident, and every pass rebuilds
+        # the layer in a window slot with an NVLink all-gather (no host link)
+        self.shards = shards or {}
+        if self.shards and world < 2:
+            raise ValueError("HBM-sharded layers need world > 1")
+        if set(self.shards) & set(host):
+            raise ValueError("a layer is either host-streamed or HBM-sharded")
         # host values are raw pinned uint8 tensors, or XC4Unit (K9: encoded
         # frames cross the link and are decoded into the slot on the GPU)
         self.coded = any(isinstance(v, XC4Unit) for v in host.values())
@@ -209,17 +230,17 @@ class LayerStreamer:
             raise ValueError("streamed layers must be all raw or all XC4-encoded")
         self.resident = resident
         self.host = host
-        self.streamed = [li for li in range(n_layer) if li in host]
+        self.streamed = [li for li in range(n_layer) if li in host or li in self.shards]
         self.n_slots = n_slots if self.streamed else 0
         self.chunk = chunk_bytes
         self.device = torch.device(device)
-        self.copy_stream = torch.cuda.Stream(device=self.device) if self.streamed else None
+        self.copy_stream = torch.cuda.Stream(device=self.device) if host else None
         # N > 1: each rank pushes its 1/N slice over its own PCIe link, then an
         # in-place NCCL all-gather on the comm stream rebuilds the layer
         self.rank, self.world, self.group = rank, world, group
         self.lo, self.hi = slice_bounds(layer_bytes, rank, world) if world > 1 else (0, layer_bytes)
         self.comm_stream = torch.cuda.Stream(device=self.device) if (self.streamed and world > 1) else None
-        self.copied = [native.Event() for _ in range(self.n_slots)] if world > 1 else []
+        self.copied = [native.Event() for _ in range(self.n_slots)] if (world > 1 and host) else []
         self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
         # events are created eagerly through the C ABI (a lazily created torch
         # event has handle 0, and record/wait on it silently no-op)
@@ -228,7 +249,7 @@ class LayerStreamer:
         self.ring = None
         if self.coded:
             for u in host.values():
-                if u.raw_bytes != layer_bytes:
+                if u.raw_bytes != layer_bytes:  # noqa: SIM102
                     raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
             self.frames = {li: u.frame_range(rank, world) for li, u in host.items()}
             self.ring_slot_bytes = (max(u.max_frame_bytes() for u in host.values()) + 255) // 256 * 256
@@ -240,7 +261,8 @@ class LayerStreamer:
         self.k_use = 0      # global index of the next streamed use
         self.k_issued = 0   # copies enqueued so far
         self.bytes_issued = 0      # bytes moved over this rank's host link
-        self.raw_bytes_issued = 0  # decoded layer bytes those copies delivered
+        self.raw_bytes_issued = 0  # layer bytes this rank's copies / shards delivered
+        self.nvlink_bytes_issued = 0  # bytes this rank receives in the all-gathers
         self.trace = trace
         self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
 
@@ -251,6 +273,18 @@ class LayerStreamer:
     def _issue(self, k: int) -> None:
         slot = k % self.n_slots
         layer = self.streamed[k % len(self.streamed)]
+        if layer in self.shards:  # f3: NVLink all-gather of the resident 1/N shards
+            start = native.Event(timing=True).record(self.comm_stream) if self.trace else None
+            if k >= self.n_slots:
+                self.free[slot].wait(self.comm_stream)
+            with torch.cuda.stream(self.comm_stream):
+                gather_shards(self.slots[slot], self.shards[layer], self.group)
+            self.loaded[slot].record(self.comm_stream)
+            self.nvlink_bytes_issued += (self.world - 1) * (self.hi - self.lo)
+            self.raw_bytes_issued += self.hi - self.lo
+            if self.trace:
+                self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.comm_stream)))
+            return
         if k >= self.n_slots and not self.coded:  # coded: the decoder waits instead, the link runs ahead
             self.free[slot].wait(self.copy_stream)
         src = self.host[layer]

@@ -90,6 +90,7 @@ class ModelWeights:
     lm_head: torch.Tensor
     layers: list[LayerWeights]
     host_ffn: dict  # layer -> pinned host buffer, or codec.XC4Unit (streamed layers)
+    shard_ffn: dict = dataclasses.field(default_factory=dict)  # layer -> this rank's HBM shard (f3)
 
     def resident_bytes(self) -> int:
         n = self.embed.numel() + self.final_norm.numel() + self.lm_head.numel()
@@ -136,7 +137,7 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
               host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False,
-              encoder=None) -> ModelWeights:
+              encoder=None, shard_layers: set[int] = frozenset(), shard: tuple[int, int] = (0, 1)) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
@@ -145,8 +146,11 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
     writes only its slice of the shared store; every rank draws the same
     weights from the same seed).  With ``encoder`` (codec.Encoder) streamed
     units are XC4-encoded on the GPU first and the host keeps the encoding
-    (the sink then receives the encoded device bytes).
+    (the sink then receives the encoded device bytes).  ``shard_layers`` (f3,
+    N > 1): this rank keeps only its ``slice_bounds`` share of the layer unit in
+    HBM; the streamer all-gathers the shards every pass.
     """
+    from .streamer import slice_bounds
     dev = torch.device(device)
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
@@ -160,11 +164,16 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
     _, _, ffn_bytes = ffn_offsets(arch)
     layers = []
     host = {}
+    shards = {}
     for li in range(arch.n_layer):
-        streamed = li in stream_layers
+        sharded = li in shard_layers
+        streamed = li in stream_layers or sharded
         with_attn = streamed and stream_attn
         unit = randn((ffn_bytes + (attn_elems(arch) * 2 if with_attn else 0)) // 2)
-        if streamed and encoder is not None:
+        if sharded:
+            lo, hi = slice_bounds(unit.numel() * 2, *shard)
+            shards[li] = unit.view(torch.uint8)[lo:hi].clone()
+        elif streamed and encoder is not None:
             if host_sink is not None:
                 host[li] = host_sink(li, encoder.encode(unit)[0])
             else:
@@ -189,4 +198,4 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
         ))
     torch.cuda.synchronize(dev) if dev.type == "cuda" else None
     return ModelWeights(arch, randn(arch.vocab, arch.hidden), ones(arch.hidden), randn(arch.vocab, arch.hidden),
-                        layers, host)
+                        layers, host, shards)

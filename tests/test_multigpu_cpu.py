@@ -129,3 +129,41 @@ def test_shared_store_xc4_frames_and_allgather():
     # each rank's share of the link bytes is about half of the encoded layers
     assert abs(results[0][1] - results[1][1]) < 0.01 * results[0][1]
     assert not os.path.exists(f"/dev/shm/{name}")
+
+
+def _shard_worker(rank: int, world: int, port: int, q):
+    from paper_2505_10259_b200 import TINY_TARGET
+    from paper_2505_10259_b200 import weights as W
+    from paper_2505_10259_b200.streamer import gather_shards
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = W.synthetic(TINY_TARGET, "cpu", seed=3)                        # every layer resident
+        sh = W.synthetic(TINY_TARGET, "cpu", seed=3, shard_layers={1, 2}, shard=(rank, world))
+        ok = set(sh.shard_ffn) == {1, 2} and sh.layers[1].ffn is None and sh.layers[0].ffn is not None
+        for li in (1, 2):
+            unit = full.layers[li].ffn.view(torch.uint8)
+            lo, hi = slice_bounds(unit.numel(), rank, world)
+            ok &= torch.equal(sh.shard_ffn[li], unit[lo:hi])                  # this rank keeps its 1/N
+            slot = torch.zeros_like(unit)
+            gather_shards(slot, sh.shard_ffn[li])                             # f3: the per-pass all-gather
+            ok &= torch.equal(slot, unit)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hbm_sharded_layers_allgather():
+    """layers kept 1/N per rank (same seed → same weights on
+    every rank) rebuild bit-exactly from the ranks' shards."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 33500 + (os.getpid() % 2000)
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert dict(q.get(timeout=5) for _ in range(world)) == {0: True, 1: True}

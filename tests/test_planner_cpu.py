@@ -98,3 +98,26 @@ def test_roofline_definition():
     S = 56 * ffn_offsets(MIXTRAL_8X22B)[2]
     r = roofline_tokens_per_s(256 * 3.3616, S, 73e-3 * 1375.5e12, 55e9, 1375.5e12)
     assert abs(r - 174.9) < 0.5
+
+
+def test_multi_gpu_plan_uses_hbm_shards():
+    """§8 e/f3: at N GPUs each rank pulls 1/N of the host-streamed bytes and the
+    planner moves layers into the N GPUs' aggregate HBM (1/N each) when that
+    beats the host link; every layer is pinned, sharded or host-streamed."""
+    one = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(193e9), 8, 0.8, 503, 45, RATES,
+                       stream_ratio=0.7, ring_bytes=800 << 20, bs_candidates=list(range(64, 1025, 32)))
+    prev = one.tokens_per_s
+    for world in (2, 8):
+        p = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(193e9), 8, 0.8, 503, 45, RATES,
+                         stream_ratio=0.7, ring_bytes=800 << 20, world=world, bs_candidates=list(range(64, 1025, 32)))
+        assert len(p.pinned_layers) + len(p.stream_layers) + len(p.shard_layers) == 56
+        assert set(p.pinned_layers).isdisjoint(p.shard_layers) and set(p.stream_layers).isdisjoint(p.shard_layers)
+        assert p.shard_layers and p.world == world
+        assert sum(p.hbm_bytes.values()) <= 190e9
+        assert p.t_round_s >= max(p.t_stream_s, p.t_nvlink_s, p.t_compute_s)
+        assert p.tokens_per_s > prev  # per-GPU tokens/s grows: the host link stops binding alone
+        prev = p.tokens_per_s
+    no = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(193e9), 8, 0.8, 503, 45, RATES,
+                      stream_ratio=0.7, ring_bytes=800 << 20, world=8, allow_shards=False,
+                      bs_candidates=list(range(64, 1025, 32)))
+    assert not no.shard_layers and no.tokens_per_s < prev
