@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
     ap.add_argument("--e2e-seqs", type=int, default=0,
-                    help="sequences of the generate() leg (0 = both batches of the decode plan, 2·bs_decoding)")
+                    help="prompts of the generate() leg (0 = twice the decode plan's 2·bs_decoding slots, "
+                         "run with slot refill)")
     ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
@@ -396,10 +397,13 @@ def main():
     if not args.no_e2e_generate:
         del s
         torch.cuda.empty_cache()
-        S_e = args.e2e_seqs or 2 * bs
+        S_e = args.e2e_seqs or 4 * bs
         rng = np.random.default_rng(1234 + rank)
         prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
-        pol = Policy(bs_prefill=S_e, bs_decoding=(S_e + 1) // 2, bs_draft=min(64, (S_e + 1) // 2),
+        # the decode plan's two batches are the slot pool; prompts beyond them are
+        # admitted as slots free up (slot refill, prefill inside the verify passes)
+        pol = Policy(bs_prefill=min(S_e, 2 * bs), bs_decoding=min(bs, (S_e + 1) // 2),
+                     bs_draft=min(64, (S_e + 1) // 2) if plan.draft_kv != "cached" else min(bs, (S_e + 1) // 2),
                      n_cand=args.n_cand)
         torch.cuda.synchronize(device)
         g0 = time.perf_counter()
@@ -411,8 +415,11 @@ def main():
         gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
                "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
                "policy": list(pol.as_tuple()), "draft_kv": plan.draft_kv,
-               "note": "Engine.generate(): host token ids in, layer-major prefill (each streamed layer crosses "
-                       "the link once), dual-batch decode, host token lists out; paper's e2e definition"}
+               "refill": gs.refill, "slots": gs.n_seq,
+               "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
+                       "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "
+                       "verify pass), so every round streams the layers once for prefill and decode alike; "
+                       "paper's e2e definition (prefill included)"}
 
     if args.trace_out and rank == 0:
         from paper_2505_10259_b200.trace import SimResult, busy, export_chrome

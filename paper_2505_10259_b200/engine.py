@@ -103,7 +103,8 @@ class DecodeSession:
 
     def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
                  mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int,
-                 draft_kv: str = "cached", draft_cached: int | None = None):
+                 draft_kv: str = "cached", draft_cached: int | None = None, prompts: list | None = None,
+                 max_new: int = 0):
         self.e = engine
         self.n_seq = n_seq
         self.n_cand = n_cand
@@ -144,13 +145,29 @@ class DecodeSession:
         self.any_reprefill = any(kc < b.n for b, kc in zip(self.batches, self.n_cached))
         self.dkv = PagedKVCache(engine.draft.arch, max(1, r + (bs_draft if self.any_reprefill else 0)), max_len,
                                 dev, engine.page_size)
-        # token history (position-indexed) for the re-prefilling draft
-        self.hist = torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev) if self.any_reprefill else None
+        # Slot refill: with ``prompts`` the n_seq slots are a
+        # pool; a prompt is admitted into a free slot of the batch about to be
+        # verified, prefilled inside that verify pass (the streamed layers are
+        # crossing the link anyway), drafted from its context in the next round
+        # ("fresh"), and its slot is freed as soon as it has max_new tokens.
+        self.refill = prompts is not None
+        self.prompts = prompts
+        self.max_new = max_new
+        self.queue = list(range(len(prompts))) if self.refill else []
+        self.queue.reverse()  # pop() from the end = admission in prompt order
+        # token history (position-indexed) for every draft that re-reads its context
+        self.hist = (torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev)
+                     if (self.any_reprefill or self.refill) else None)
         self.max_len = max_len
         self.ctx = np.zeros(n_seq, np.int64)
         self.t_last = np.zeros(n_seq, np.int32)
         self.remaining = np.zeros(n_seq, np.int32)
-        self.out: list[list[int]] = [[] for _ in range(n_seq)]
+        self.slot_prompt = np.full(n_seq, -1, np.int64) if self.refill else np.arange(n_seq)
+        self.active = np.zeros(n_seq, bool)     # the slot holds a decoding sequence
+        self.fresh = np.zeros(n_seq, bool)      # ... whose draft state must be built from its context
+        self.dlist = [np.zeros(0, np.int64), np.zeros(0, np.int64)]  # slots drafted for each batch's next verify
+        self.pending_new = [np.zeros(0, np.int64), np.zeros(0, np.int64)]  # slots prefilled in the next verify
+        self.out: list[list[int]] = [[] for _ in range(len(prompts) if self.refill else n_seq)]
         V = engine.target.arch.vocab
         self.drafts = []
         self.qprobs = []
@@ -161,6 +178,7 @@ class DecodeSession:
         self.res_tok = [torch.empty((max(b.n, 1), n_cand + 1), dtype=torch.int32, pin_memory=True)
                         for b in self.batches]
         self.res_cnt = [torch.empty(max(b.n, 1), dtype=torch.int32, pin_memory=True) for b in self.batches]
+        self.res_first = [torch.empty(max(b.n, 1), dtype=torch.int32, pin_memory=True) for b in self.batches]
         self.rounds = 0
         self.committed_decode = 0
 
@@ -236,9 +254,14 @@ class Engine:
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
                     bs_draft: int | None = None, draft_kv: str = "cached",
-                    draft_cached: int | None = None) -> DecodeSession:
+                    draft_cached: int | None = None, prompts: list | None = None,
+                    max_new: int = 0) -> DecodeSession:
         return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
-                             bs_draft or bs_decoding, draft_kv, draft_cached)
+                             bs_draft or bs_decoding, draft_kv, draft_cached, prompts, max_new)
+
+    def _bt(self, kv: PagedKVCache, rows, stream) -> torch.Tensor:
+        """Block-table rows of an arbitrary slot list, staged to the device."""
+        return self._up(kv._bt_host[np.asarray(rows, np.int64)], stream)
 
     def _hist_write(self, s: DecodeSession, seqs, positions, tokens, stream) -> None:
         """Record committed tokens in the device-side history (reprefill drafts)."""
@@ -322,6 +345,7 @@ class Engine:
         s.t_last[:] = first_np
         s.ctx[:] = lens
         s.remaining[:] = max_new - 1
+        s.active[:] = True
         self._hist_write(s, np.arange(s.n_seq), lens, first_np, self.drf_stream)
         self.drf_stream.synchronize()
         self._release_staging()
@@ -339,6 +363,7 @@ class Engine:
         s.t_last[:] = rng.integers(0, self.target.arch.vocab, s.n_seq)
         s.ctx[:] = ctx_len
         s.remaining[:] = max_new
+        s.active[:] = True
         if s.hist is not None:
             s.hist.random_(0, self.target.arch.vocab, generator=g)
             self._hist_write(s, np.arange(s.n_seq), s.ctx, s.t_last, self.drf_stream)
@@ -347,77 +372,106 @@ class Engine:
 
     # ------------------------------------------------------------------ draft
     def _draft(self, s: DecodeSession, bi: int, rnd: int) -> None:
+        """Draft n_cand tokens for every active slot of batch ``bi``.
+
+        Slots are ordered [cached rows | fresh rows | re-prefilled] and that
+        order (``s.dlist[bi]``) indexes the draft buffers and the next verify
+        of the batch.  Cached rows run n+1 decode steps; fresh rows (a prompt
+        just prefilled by the target) and slots without a row re-read their
+        whole context (the paper's re-prefill, into their own row or the
+        scratch rows)."""
         b = s.batches[bi]
-        if b.n == 0:
+        slots = np.arange(b.lo, b.hi)
+        act = slots[s.active[slots]]
+        has_row = s.drow[act] >= 0
+        fresh = s.fresh[act]
+        cached, fresh_rows, rp = act[has_row & ~fresh], act[has_row & fresh], act[~has_row]
+        order = np.concatenate([cached, fresh_rows, rp])
+        s.dlist[bi] = order
+        if order.size == 0:
             return
         st = self.drf_stream
         n = s.n_cand
         tr = self.tracer
         ev0 = tr.mark(st)
-        u_all = input_uniforms(s.seed, rnd, bi, 0, (b.n, n)) if s.mode == "sample" else None
-        kc = s.n_cached[bi]
-        cstep = s.bs_draft if s.draft_kv == "cached" else max(kc, 1)
-        chunks = [(lo, min(kc, lo + cstep), True) for lo in range(0, kc, cstep)]
-        chunks += [(lo, min(b.n, lo + s.bs_draft), False) for lo in range(kc, b.n, s.bs_draft)]
-        for c_lo, c_hi, cached in chunks:
-            cm = c_hi - c_lo
-            seqs = np.arange(b.lo + c_lo, b.lo + c_hi)
-            ctx = s.ctx[seqs]
-            if not cached:
-                self._draft_chunk_reprefill(s, bi, c_lo, c_hi, seqs, ctx, u_all)
-                continue
-            rows = s.drow[seqs]
-            pos = ctx[None, :] + np.arange(n + 1)[:, None]                  # [n+1, cm]
-            slots = s.dkv.slots(np.broadcast_to(rows, pos.shape), pos)
-            qs = np.arange(cm + 1, dtype=np.int32)
-            parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, pos.astype(np.int32).ravel()]
-            if u_all is not None:
-                parts.append(u_all[c_lo:c_hi].T.ravel().view(np.int32))
-            meta = self._up(np.concatenate(parts), st)
-            o = cm
-            P = (n + 1) * cm
-            pos_d, slot_d = meta[o:o + P], meta[o + P:o + 2 * P]
-            qs_d = meta[o + 2 * P:o + 2 * P + cm + 1]
-            kvb_d = meta[o + 2 * P + cm + 1:o + 3 * P + cm + 1]
-            u_d = meta[o + 3 * P + cm + 1:].view(torch.float32) if u_all is not None else None
-            bt = s.dkv.block_table[rows[0]:rows[-1] + 1]
-            for j in range(n + 1):
-                toks = meta[:cm] if j == 0 else s.drafts[bi][j - 1, c_lo:c_hi]
-                fb = ForwardBatch(toks, pos_d[j * cm:(j + 1) * cm], slot_d[j * cm:(j + 1) * cm], qs_d,
-                                  kvb_d[j * cm:(j + 1) * cm], bt, cm, 1)
-                if j == n:
-                    self.draft.forward(fb, s.dkv, st, want_logits=False)  # KV of d_n only
-                    break
-                logits = self.draft.forward(fb, s.dkv, st)
-                out_tok = s.drafts[bi][j, c_lo:c_hi]
-                if s.mode == "sample":
-                    qp = s.qprobs[bi][c_lo:c_hi, j, :]
-                    native.sample_tokens(logits, out_tok, uniforms=u_d[j * cm:(j + 1) * cm], out_probs=qp,
-                                         temperature=s.temperature, stream=st)
-                else:
-                    native.sample_tokens(logits, out_tok, stream=st)
+        u_all = input_uniforms(s.seed, rnd, bi, 0, (order.size, n)) if s.mode == "sample" else None
+        cstep = s.bs_draft if s.draft_kv == "cached" else max(cached.size, 1)
+        for c_lo in range(0, cached.size, cstep):
+            c_hi = min(cached.size, c_lo + cstep)
+            self._draft_chunk_cached(s, bi, c_lo, order[c_lo:c_hi], u_all)
+        base = cached.size
+        for c_lo in range(0, fresh_rows.size, s.bs_draft):
+            seqs = fresh_rows[c_lo:c_lo + s.bs_draft]
+            self._draft_chunk_reprefill(s, bi, base + c_lo, seqs, u_all, rows=s.drow[seqs], kv_dn=True)
+        base += fresh_rows.size
+        for c_lo in range(0, rp.size, s.bs_draft):
+            seqs = rp[c_lo:c_lo + s.bs_draft]
+            self._draft_chunk_reprefill(s, bi, base + c_lo, seqs, u_all,
+                                        rows=s.scratch_row0 + np.arange(seqs.size), kv_dn=False)
+        s.fresh[act] = False
         tr.add("GPU_DRAFT", "draft_decode", ev0, tr.mark(st), batch=bi, rnd=rnd)
 
-    def _draft_chunk_reprefill(self, s: DecodeSession, bi: int, c_lo: int, c_hi: int, seqs, ctx, u_all) -> None:
-        """One bs_draft chunk of the paper's draft: prefill the whole context
-        (prompt + committed tokens + t_last) into the scratch cache, take d_1
-        from its last row, then n_cand−1 cached decode steps."""
+    def _draft_chunk_cached(self, s: DecodeSession, bi: int, p0: int, seqs, u_all) -> None:
+        """n+1 cached-KV decode steps for slots ``seqs`` (draft positions p0..)."""
         st = self.drf_stream
         n = s.n_cand
-        cm = c_hi - c_lo
-        local = s.scratch_row0 + np.arange(cm)             # scratch draft KV rows
+        cm = seqs.size
+        ctx = s.ctx[seqs]
+        rows = s.drow[seqs]
+        pos = ctx[None, :] + np.arange(n + 1)[:, None]                  # [n+1, cm]
+        slots = s.dkv.slots(np.broadcast_to(rows, pos.shape), pos)
+        qs = np.arange(cm + 1, dtype=np.int32)
+        parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, pos.astype(np.int32).ravel()]
+        if u_all is not None:
+            parts.append(u_all[p0:p0 + cm].T.ravel().view(np.int32))
+        meta = self._up(np.concatenate(parts), st)
+        o = cm
+        P = (n + 1) * cm
+        pos_d, slot_d = meta[o:o + P], meta[o + P:o + 2 * P]
+        qs_d = meta[o + 2 * P:o + 2 * P + cm + 1]
+        kvb_d = meta[o + 2 * P + cm + 1:o + 3 * P + cm + 1]
+        u_d = meta[o + 3 * P + cm + 1:].view(torch.float32) if u_all is not None else None
+        bt = self._bt(s.dkv, rows, st)
+        for j in range(n + 1):
+            toks = meta[:cm] if j == 0 else s.drafts[bi][j - 1, p0:p0 + cm]
+            fb = ForwardBatch(toks, pos_d[j * cm:(j + 1) * cm], slot_d[j * cm:(j + 1) * cm], qs_d,
+                              kvb_d[j * cm:(j + 1) * cm], bt, cm, 1)
+            if j == n:
+                self.draft.forward(fb, s.dkv, st, want_logits=False)  # KV of d_n only
+                break
+            logits = self.draft.forward(fb, s.dkv, st)
+            out_tok = s.drafts[bi][j, p0:p0 + cm]
+            if s.mode == "sample":
+                qp = s.qprobs[bi][p0:p0 + cm, j, :]
+                native.sample_tokens(logits, out_tok, uniforms=u_d[j * cm:(j + 1) * cm], out_probs=qp,
+                                     temperature=s.temperature, stream=st)
+            else:
+                native.sample_tokens(logits, out_tok, stream=st)
+
+    def _draft_chunk_reprefill(self, s: DecodeSession, bi: int, p0: int, seqs, u_all, rows, kv_dn: bool) -> None:
+        """The paper's draft for slots ``seqs``: prefill the whole context
+        (prompt + committed tokens + t_last) into draft KV rows ``rows``, take
+        d_1 from its last row, then n_cand−1 cached decode steps.  ``kv_dn``
+        (a fresh slot with a persistent row) adds the step that writes d_n's
+        KV, after which the row follows the cached invariant."""
+        st = self.drf_stream
+        n = s.n_cand
+        cm = seqs.size
+        ctx = s.ctx[seqs]
+        rows = np.asarray(rows, np.int64)
         lens = ctx + 1                                    # positions 0..ctx (t_last at ctx)
         T = int(lens.sum())
         flat = np.concatenate([seq * s.max_len + np.arange(L) for seq, L in zip(seqs, lens)])
         pos = np.concatenate([np.arange(L) for L in lens])
-        slots = s.dkv.slots(np.repeat(local, lens), pos)
+        slots = s.dkv.slots(np.repeat(rows, lens), pos)
         qs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
-        dpos = ctx[None, :] + np.arange(1, n)[:, None]    # decode steps j = 1..n-1: [n-1, cm]
-        dslots = s.dkv.slots(np.broadcast_to(local, dpos.shape), dpos)
+        steps = n if kv_dn else n - 1                     # decode steps j = 1..steps
+        dpos = ctx[None, :] + np.arange(1, steps + 1)[:, None]
+        dslots = s.dkv.slots(np.broadcast_to(rows, dpos.shape), dpos)
         parts = [pos.astype(np.int32), slots, qs, np.zeros(cm, np.int32), (qs[1:] - 1).astype(np.int32),
                  dpos.astype(np.int32).ravel(), dslots.ravel(), np.arange(cm + 1, dtype=np.int32)]
         if u_all is not None:
-            parts.append(u_all[c_lo:c_hi].T.ravel().view(np.int32))
+            parts.append(u_all[p0:p0 + cm].T.ravel().view(np.int32))
         meta = self._up(np.concatenate(parts), st)
         idx = self._up(flat, st, torch.int64)
         o = 0
@@ -426,108 +480,191 @@ class Engine:
         qs_d = meta[o:o + cm + 1]; o += cm + 1
         zero_d = meta[o:o + cm]; o += cm
         last_d = meta[o:o + cm]; o += cm
-        D = (n - 1) * cm
+        D = steps * cm
         dpos_d = meta[o:o + D]; o += D
         dslot_d = meta[o:o + D]; o += D
         dqs_d = meta[o:o + cm + 1]; o += cm + 1
         u_d = meta[o:].view(torch.float32) if u_all is not None else None
         toks = self.draft.ws.get("rp_tokens", (T,), torch.int32)
         native.gather_i32(s.hist, idx, toks, st)
-        last_rows = last_d
-        bt = s.dkv.block_table[s.scratch_row0:s.scratch_row0 + cm]
-        for j in range(n):
+        bt = self._bt(s.dkv, rows, st)
+        for j in range(steps + 1):
             if j == 0:
-                fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_rows)
+                fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_d)
             else:
                 sl = slice((j - 1) * cm, j * cm)
-                fb = ForwardBatch(s.drafts[bi][j - 1, c_lo:c_hi], dpos_d[sl], dslot_d[sl], dqs_d, dpos_d[sl], bt,
+                fb = ForwardBatch(s.drafts[bi][j - 1, p0:p0 + cm], dpos_d[sl], dslot_d[sl], dqs_d, dpos_d[sl], bt,
                                   cm, 1)
+            if j == n:
+                self.draft.forward(fb, s.dkv, st, want_logits=False)  # KV of d_n only
+                break
             logits = self.draft.forward(fb, s.dkv, st)
-            out_tok = s.drafts[bi][j, c_lo:c_hi]
+            out_tok = s.drafts[bi][j, p0:p0 + cm]
             if s.mode == "sample":
                 native.sample_tokens(logits, out_tok, uniforms=u_d[j * cm:(j + 1) * cm],
-                                     out_probs=s.qprobs[bi][c_lo:c_hi, j, :], temperature=s.temperature, stream=st)
+                                     out_probs=s.qprobs[bi][p0:p0 + cm, j, :], temperature=s.temperature, stream=st)
             else:
                 native.sample_tokens(logits, out_tok, stream=st)
 
     # ----------------------------------------------------------------- verify
-    def _verify(self, s: DecodeSession, bi: int, rnd: int) -> None:
-        b = s.batches[bi]
+    def _verify(self, s: DecodeSession, bi: int, rnd: int, chunk_tokens: int = 16384) -> None:
+        """Verify batch ``bi``: the drafted slots (``s.dlist[bi]``, n_cand+1
+        query tokens each) and, with slot refill, prefill the prompts admitted
+        into its free slots (``s.pending_new[bi]``) in the same layer pass —
+        layer-major over token-bounded chunks, so each streamed layer still
+        crosses the link once.  LM-head rows: every verify row, then the last
+        prompt row of each admitted slot (its first token)."""
         st = self.tgt_stream
         n = s.n_cand
         tr = self.tracer
-        seqs = b.ids
-        ctx = s.ctx[seqs]
-        T = b.n * (n + 1)
+        act = s.dlist[bi]
+        new = s.pending_new[bi]
+        na, nn = act.size, new.size
+        T = na * (n + 1)
+        ctx = s.ctx[act]
         pos = ctx[:, None] + np.arange(n + 1)[None, :]
-        slots = s.tkv.slots(np.broadcast_to(seqs[:, None], pos.shape), pos)
-        qs = (np.arange(b.n + 1) * (n + 1)).astype(np.int32)
+        slots = s.tkv.slots(np.broadcast_to(act[:, None], pos.shape), pos)
+        qs = (np.arange(na + 1) * (n + 1)).astype(np.int32)
         forced = None
         if s.forced_p is not None and s.mode == "greedy":
-            forced = forced_counts(s.seed, rnd, bi, s.forced_p, n, b.n)
-        parts = [s.t_last[seqs], pos.astype(np.int32).ravel(), slots.ravel(), qs, ctx.astype(np.int32),
-                 s.remaining[seqs]]
+            forced = forced_counts(s.seed, rnd, bi, s.forced_p, n, na)
+        parts = [s.t_last[act], pos.astype(np.int32).ravel(), slots.ravel(), qs, ctx.astype(np.int32),
+                 s.remaining[act]]
         if forced is not None:
             parts.append(forced)
         if s.mode == "sample":
-            parts.append(input_uniforms(s.seed, rnd, bi, 1, (b.n, n)).ravel().view(np.int32))
-            parts.append(input_uniforms(s.seed, rnd, bi, 2, b.n).view(np.int32))
+            parts.append(input_uniforms(s.seed, rnd, bi, 1, (na, n)).ravel().view(np.int32))
+            parts.append(input_uniforms(s.seed, rnd, bi, 2, na).view(np.int32))
         meta = self._up(np.concatenate(parts), st)
         o = 0
-        t_last_d = meta[o:o + b.n]; o += b.n
+        t_last_d = meta[o:o + na]; o += na
         pos_d = meta[o:o + T]; o += T
         slot_d = meta[o:o + T]; o += T
-        qs_d = meta[o:o + b.n + 1]; o += b.n + 1
-        kvb_d = meta[o:o + b.n]; o += b.n
-        rem_d = meta[o:o + b.n]; o += b.n
+        qs_d = meta[o:o + na + 1]; o += na + 1
+        kvb_d = meta[o:o + na]; o += na
+        rem_d = meta[o:o + na]; o += na
         forced_d = None
         if forced is not None:
-            forced_d = meta[o:o + b.n]; o += b.n
+            forced_d = meta[o:o + na]; o += na
         ev0 = tr.mark(st)
-        toks = self.target.ws.get("vtok", (b.n, n + 1), torch.int32)
-        draft_rows = self.target.ws.get("vdraft", (b.n, n), torch.int32)
-        native.build_verify_tokens(t_last_d, s.drafts[bi], b.n, n, toks, draft_rows, st)
-        fb = ForwardBatch(toks.view(-1), pos_d, slot_d, qs_d, kvb_d, s.tkv.block_table[b.lo:b.hi], b.n, n + 1)
-        logits = self.target.forward(fb, s.tkv, st)
+        chunks, last = [], []
+        if na:
+            toks = self.target.ws.get("vtok", (na, n + 1), torch.int32)
+            draft_rows = self.target.ws.get("vdraft", (na, n), torch.int32)
+            native.build_verify_tokens(t_last_d, s.drafts[bi], na, n, toks, draft_rows, st)
+            chunks.append(ForwardBatch(toks.view(-1), pos_d, slot_d, qs_d, kvb_d, self._bt(s.tkv, act, st), na,
+                                       n + 1, None, 0))
+            last.append(np.arange(T, dtype=np.int32))
+        row0 = T
+        lo = 0
+        while lo < nn:  # admitted prompts, ≤ chunk_tokens per chunk
+            hi, tok = lo, 0
+            while hi < nn and (hi == lo or tok + len(s.prompts[s.slot_prompt[new[hi]]]) <= chunk_tokens):
+                tok += len(s.prompts[s.slot_prompt[new[hi]]])
+                hi += 1
+            g = new[lo:hi]
+            lens = np.array([len(s.prompts[s.slot_prompt[i]]) for i in g], np.int64)
+            ptok = np.concatenate([np.asarray(s.prompts[s.slot_prompt[i]], np.int32) for i in g])
+            ppos = np.concatenate([np.arange(L) for L in lens])
+            pq = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+            pm = self._up(np.concatenate([ptok, ppos.astype(np.int32), s.tkv.slots(np.repeat(g, lens), ppos), pq,
+                                          np.zeros(g.size, np.int32)]), st)
+            Tg = int(lens.sum())
+            chunks.append(ForwardBatch(pm[:Tg], pm[Tg:2 * Tg], pm[2 * Tg:3 * Tg], pm[3 * Tg:3 * Tg + g.size + 1],
+                                       pm[3 * Tg + g.size + 1:], self._bt(s.tkv, g, st), g.size, int(lens.max()),
+                                       None, row0))
+            last.append((row0 + pq[1:] - 1).astype(np.int32))
+            row0 += Tg
+            lo = hi
+        if len(chunks) > 1 or nn:
+            chunks[0].last_rows = self._up(np.concatenate(last), st)
+        logits = self.target.forward(chunks, s.tkv, st)
         ev1 = tr.mark(st)
-        out_tok = self.target.ws.get("acc_tok", (b.n, n + 1), torch.int32)
-        out_cnt = self.target.ws.get("acc_cnt", (b.n,), torch.int32)
-        if s.mode == "sample":
-            u_acc = meta[o:o + b.n * n].view(torch.float32); o += b.n * n
-            u_res = meta[o:o + b.n].view(torch.float32); o += b.n
-            native.accept_sample(draft_rows, logits, s.qprobs[bi][:b.n], u_acc, u_res, rem_d, out_tok, out_cnt,
-                                 s.temperature, st)
-        else:
-            native.accept_greedy(draft_rows, logits, rem_d, out_tok, out_cnt, forced_d, st)
-        # device → host: the round's result (committed tokens and counts)
-        native.copy_sm(s.res_tok[bi].data_ptr(), out_tok.data_ptr(), out_tok.numel() * 4, st)
-        native.copy_sm(s.res_cnt[bi].data_ptr(), out_cnt.data_ptr(), out_cnt.numel() * 4, st)
+        if na:
+            out_tok = self.target.ws.get("acc_tok", (na, n + 1), torch.int32)
+            out_cnt = self.target.ws.get("acc_cnt", (na,), torch.int32)
+            vlog = logits[:T]
+            if s.mode == "sample":
+                u_acc = meta[o:o + na * n].view(torch.float32); o += na * n
+                u_res = meta[o:o + na].view(torch.float32); o += na
+                native.accept_sample(draft_rows, vlog, s.qprobs[bi][:na], u_acc, u_res, rem_d, out_tok, out_cnt,
+                                     s.temperature, st)
+            else:
+                native.accept_greedy(draft_rows, vlog, rem_d, out_tok, out_cnt, forced_d, st)
+            # device → host: the round's result (committed tokens and counts)
+            native.copy_sm(s.res_tok[bi].data_ptr(), out_tok.data_ptr(), out_tok.numel() * 4, st)
+            native.copy_sm(s.res_cnt[bi].data_ptr(), out_cnt.data_ptr(), out_cnt.numel() * 4, st)
+        if nn:  # first tokens of the admitted prompts
+            first = self.target.ws.get("first_tok", (nn,), torch.int32)
+            u = (self._up(input_uniforms(s.seed, rnd, bi, 3, nn), st, torch.float32)
+                 if s.mode == "sample" else None)
+            native.sample_tokens(logits[T:T + nn], first, uniforms=u, temperature=s.temperature, stream=st)
+            native.copy_sm(s.res_first[bi].data_ptr(), first.data_ptr(), nn * 4, st)
         ev2 = tr.mark(st)
         tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
         tr.add("GPU_TARGET", "accept", ev1, ev2, batch=bi, rnd=rnd)
 
     def _commit(self, s: DecodeSession, bi: int) -> int:
-        b = s.batches[bi]
-        cnt = s.res_cnt[bi][:b.n].numpy()
-        tok = s.res_tok[bi][:b.n].numpy()
+        act, new = s.dlist[bi], s.pending_new[bi]
+        cnt = s.res_cnt[bi][:act.size].numpy()
+        tok = s.res_tok[bi][:act.size].numpy()
         total = 0
         hs, hp, hv = [], [], []
-        for j, i in enumerate(b.ids):
+        for j, i in enumerate(act):
             c = int(cnt[j])
-            if c <= 0:
-                continue
-            s.out[i].extend(int(x) for x in tok[j, :c])
-            if s.hist is not None:  # committed tokens land at positions ctx+1 .. ctx+c
-                hs.append(np.full(c, i))
-                hp.append(s.ctx[i] + 1 + np.arange(c))
-                hv.append(tok[j, :c])
-            s.remaining[i] -= c
-            s.t_last[i] = tok[j, c - 1]
-            s.ctx[i] += c
-            total += c
-        if hs:
+            if c > 0:
+                s.out[s.slot_prompt[i]].extend(int(x) for x in tok[j, :c])
+                if s.hist is not None:  # committed tokens land at positions ctx+1 .. ctx+c
+                    hs.append(np.full(c, i))
+                    hp.append(s.ctx[i] + 1 + np.arange(c))
+                    hv.append(tok[j, :c])
+                s.remaining[i] -= c
+                s.t_last[i] = tok[j, c - 1]
+                s.ctx[i] += c
+                total += c
+            if s.refill and s.remaining[i] <= 0:  # done: free the slot for the next prompt
+                s.active[i] = False
+                s.slot_prompt[i] = -1
+        if new.size:
+            first = s.res_first[bi][:new.size].numpy()
+            for k, i in enumerate(new):
+                pid = s.slot_prompt[i]
+                s.out[pid].append(int(first[k]))
+                L = len(s.prompts[pid])
+                s.ctx[i] = L
+                s.t_last[i] = first[k]
+                s.remaining[i] = s.max_new - 1
+                hs.append(np.array([i]))
+                hp.append(np.array([L]))
+                hv.append(first[k:k + 1])
+                if s.remaining[i] > 0:
+                    s.active[i] = True
+                    s.fresh[i] = True   # its draft state is built from the context next round
+                else:
+                    s.slot_prompt[i] = -1
+            s.pending_new[bi] = np.zeros(0, np.int64)
+        if hs and s.hist is not None:
             self._hist_write(s, np.concatenate(hs), np.concatenate(hp), np.concatenate(hv), self.drf_stream)
         return total
+
+    def _admit(self, s: DecodeSession, bi: int) -> None:
+        """Slot refill: queued prompts take the free slots of batch ``bi``
+        (prompt order); their tokens go to the draft's history now, their
+        target prefill runs inside this round's verify."""
+        b = s.batches[bi]
+        free = [i for i in range(b.lo, b.hi) if s.slot_prompt[i] < 0]
+        take = []
+        for i in free:
+            if not s.queue:
+                break
+            s.slot_prompt[i] = s.queue.pop()
+            take.append(i)
+        s.pending_new[bi] = np.asarray(take, np.int64)
+        if take and s.hist is not None:
+            lens = [len(s.prompts[s.slot_prompt[i]]) for i in take]
+            self._hist_write(s, np.repeat(take, lens), np.concatenate([np.arange(L) for L in lens]),
+                             np.concatenate([np.asarray(s.prompts[s.slot_prompt[i]], np.int32) for i in take]),
+                             self.drf_stream)
 
     # ----------------------------------------------------------------- rounds
     def first_draft(self, s: DecodeSession) -> None:
@@ -540,8 +677,13 @@ class Engine:
         rnd = s.rounds
         bi = rnd % 2
         b, o = s.batches[bi], s.batches[1 - bi]
-        verify = b.n > 0 and (s.remaining[b.lo:b.hi] > 0).any()
-        draft = o.n > 0 and (s.remaining[o.lo:o.hi] > 0).any()
+        if s.refill:
+            self._admit(s, bi)
+            verify = s.dlist[bi].size > 0 or s.pending_new[bi].size > 0
+            draft = bool(s.active[o.lo:o.hi].any())
+        else:
+            verify = b.n > 0 and (s.remaining[b.lo:b.hi] > 0).any()
+            draft = o.n > 0 and (s.remaining[o.lo:o.hi] > 0).any()
         # Two host enqueuers: the verify's launches drain only as fast as its
         # layers arrive over PCIe, so a single thread would block on a full
         # launch queue and enqueue the draft late (serialising the streams).
@@ -590,6 +732,12 @@ class Engine:
         return c
 
     def decode(self, s: DecodeSession, max_rounds: int | None = None) -> None:
+        if s.refill:
+            while s.queue or s.active.any() or any(p.size for p in s.pending_new):
+                if max_rounds is not None and s.rounds >= max_rounds:
+                    break
+                self.round(s)
+            return
         while (s.remaining > 0).any():
             if max_rounds is not None and s.rounds >= max_rounds:
                 break
@@ -598,13 +746,29 @@ class Engine:
     # ------------------------------------------------------------ public API
     def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
                  mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None,
-                 draft_kv: str = "cached", draft_cached: int | None = None) -> list[list[int]]:
-        """prompts (token id lists) → committed continuations, max_new_tokens each."""
+                 draft_kv: str = "cached", draft_cached: int | None = None,
+                 refill: bool | None = None) -> list[list[int]]:
+        """prompts (token id lists) → committed continuations, max_new_tokens each.
+
+        With more prompts than the two batches hold (or ``refill=True``), the
+        2·bs_decoding sequences are slots of a pool refilled as sequences
+        finish: no straggler rounds and no separate prefill
+        pass; otherwise every prompt is prefilled layer-major first."""
         S = len(prompts)
         if policy is None:
             policy = Policy(bs_prefill=min(S, 2 * ((S + 1) // 2)), bs_decoding=(S + 1) // 2,
                             bs_draft=(S + 1) // 2, n_cand=4)
         max_len = max(len(p) for p in prompts) + max_new_tokens + policy.n_cand + 2
+        if refill is None:
+            refill = S > 2 * policy.bs_decoding
+        if refill:
+            slots = min(S, 2 * policy.bs_decoding)
+            s = self.new_session(slots, min(policy.bs_decoding, slots), max_len, policy.n_cand, mode, seed,
+                                 temperature, forced_p, policy.bs_draft, draft_kv, draft_cached,
+                                 prompts=[np.asarray(p, np.int32) for p in prompts], max_new=max_new_tokens)
+            self.decode(s)
+            self.last_session = s
+            return [o[:max_new_tokens] for o in s.out]
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, temperature, forced_p,
                              policy.bs_draft, draft_kv, draft_cached)
         self.prefill(s, prompts, max_new_tokens, policy.bs_prefill)

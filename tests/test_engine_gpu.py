@@ -214,3 +214,48 @@ def test_mixed_draft_kv_matches_oracle(pair, draft_cached, bs_draft):
     want, _ = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts, 14, 4, 4, margins=margins)
     assert_greedy_parity(got, want, margins)
     assert got == cached
+
+
+def _oracle_groups(tw, dw, prompts, max_new, n_cand, bs):
+    """Per-prompt greedy continuations from the oracle, run in groups it accepts."""
+    want, margins = [], []
+    for g0 in range(0, len(prompts), 2 * bs):
+        m = []
+        w, _ = decode_ref.generate(tiny.TARGET, tw, tiny.DRAFT, dw, prompts[g0:g0 + 2 * bs], max_new, n_cand, bs,
+                                   margins=m)
+        want += w
+        margins += m
+    return want, margins
+
+
+@pytest.mark.parametrize("draft_kv,draft_cached,bs_draft", [("cached", None, 4), ("mixed", 2, 2),
+                                                            ("reprefill", None, 3)])
+def test_slot_refill_generate_matches_oracle(pair, draft_kv, draft_cached, bs_draft):
+    """21 prompts through 8 slots — finished sequences free
+    their slot, queued prompts are prefilled inside a verify pass and drafted
+    from their context the next round.  Every prompt's tokens are its greedy
+    continuation (oracle), whatever slot and round it ran in."""
+    tw, dw = pair
+    prompts = tiny.prompts(21, seed=23)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 3})
+    got = eng.generate(prompts, 10, Policy(8, 4, bs_draft, 4), draft_kv=draft_kv, draft_cached=draft_cached)
+    s = eng.last_session
+    assert s.refill and s.n_seq == 8 and not s.queue and not s.active.any()
+    assert all(len(g) == 10 for g in got)
+    want, margins = _oracle_groups(tw, dw, prompts, 10, 4, 4)
+    assert_greedy_parity(got, want, margins)
+
+
+def test_slot_refill_edges(pair):
+    """max_new = 1 frees a slot at its prefill; forced refill with fewer prompts
+    than slots; the refill and the classic paths agree token for token."""
+    tw, dw = pair
+    prompts = tiny.prompts(6, seed=29)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 2})
+    pol = Policy(8, 4, 4, 4)
+    one = eng.generate(prompts, 1, pol, refill=True)
+    assert [len(t) for t in one] == [1] * 6
+    classic = eng.generate(prompts, 9, pol, refill=False)
+    refill = eng.generate(prompts, 9, pol, refill=True)
+    assert refill == classic
+    assert [t[0] for t in refill] == [t[0] for t in one]
