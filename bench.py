@@ -60,6 +60,9 @@ def parse():
                     help="mixed draft KV: cached sequences per batch (-1 = planner)")
     ap.add_argument("--no-shards", action="store_true",
                     help="N > 1: stream every non-pinned layer over the host links (no HBM-sharded layers, §8 f3)")
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo = functional check of the N>1 path with ranks sharing GPUs (collectives staged "
+                         "through host memory; not a performance configuration)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
@@ -74,6 +77,11 @@ def parse():
 
 
 NVLINK_PEER_BPS = 770e9  # B200_PROFILING.md: measured NVLink 5 peer copy per direction
+
+
+def log(msg: str) -> None:
+    """Progress line on stderr (rank-tagged): locates a stall in multi-rank runs."""
+    print(f"[rank {os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
 def mem_available() -> int:
@@ -195,22 +203,33 @@ def main():
     from paper_2505_10259_b200.streamer import HostStore
     from paper_2505_10259_b200.weights import ffn_offsets, unit_layout
 
-    device = torch.device("cuda", local)
+    n_dev = torch.cuda.device_count()
+    device = torch.device("cuda", local % n_dev)
     torch.cuda.set_device(device)
+    share = -(-min(world, int(os.environ.get("LOCAL_WORLD_SIZE", world))) // n_dev)  # ranks per GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
     tgt, drf = pair(args.config, args.layers)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
                                                          "bf16_tflops_sustained": 1400.0}
     link = h2d_peak(torch, device)
     free, total = torch.cuda.mem_get_info(device)
+    free //= share  # ranks sharing a GPU (gloo functional check) split its memory
     hbm = int(args.hbm_gb * 1e9) if args.hbm_gb else (int(24 * 2**30) if args.config == "8x7b" else free)
     if hbm < free:
         # enforce the cap (configs[1]: "HBM capped to 24 GB") on the allocator itself
         torch.cuda.set_per_process_memory_fraction(min(1.0, hbm / total), device)
     # one host copy of the streamed layers serves every rank (SharedHostStore)
     host = int(args.host_gb * 1e9) if args.host_gb else max(0, mem_available() - int(14e9))
+    if world > 1:  # every rank must build the same plan: agree on the smallest measured budgets / rates
+        agree = torch.tensor([float(link), float(hbm), float(host)], dtype=torch.float64,
+                             device=device if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        link, hbm, host = float(agree[0]), int(agree[1]), int(agree[2])
     steps, warm = args.steps, args.warmup
     verifies_per_batch = (warm + steps) // 2 + 2
     max_new = verifies_per_batch * (args.n_cand + 1) + 1
@@ -236,6 +255,8 @@ def main():
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
                         draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
                         world=world, allow_shards=not args.no_shards)
+    log(f"plan: bs {plan.bs_decoding} draft {plan.draft_kv}/{plan.draft_cached} pinned {len(plan.pinned_layers)} "
+        f"streamed {len(plan.stream_layers)} sharded {len(plan.shard_layers)} link {link / 1e9:.1f} GB/s")
     t_setup = time.perf_counter()
     layer_bytes = ffn_offsets(tgt)[2]
     if world > 1:
@@ -262,8 +283,10 @@ def main():
     eng.synthetic_context(s, args.ctx, max_new, seed=rank)
     eng.first_draft(s)
     setup_s = time.perf_counter() - t_setup
-    for _ in range(warm):
+    log(f"setup {setup_s:.1f} s")
+    for i in range(warm):
         eng.round(s)
+        log(f"warm-up round {i}")
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
@@ -303,10 +326,11 @@ def main():
     nvl = (st.nvlink_bytes_issued - nvl0) if st else 0       # bytes this rank received from HBM shards
     launches = dict(native.launches)
     if world > 1:
-        t = torch.tensor([dev_s, wall], device=device, dtype=torch.float64)
+        rdev = device if args.dist_backend == "nccl" else "cpu"
+        t = torch.tensor([dev_s, wall], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, wall = t.tolist()
-        c = torch.tensor([committed], device=device, dtype=torch.float64)
+        c = torch.tensor([committed], device=rdev, dtype=torch.float64)
         dist.all_reduce(c)
         committed = int(c.item())
     value = committed / dev_s

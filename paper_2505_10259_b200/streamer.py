@@ -172,18 +172,32 @@ class SharedHostStore:
             os.unlink(self.path)
 
 
+def _gloo_gather(out: torch.Tensor, mine: torch.Tensor, group) -> None:
+    """All-gather through host memory: the CPU-test path, and the single-GPU
+    multi-rank check (several ranks sharing one device under gloo), which
+    exercises every N > 1 code path except NCCL itself."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if out.is_cuda:
+        torch.cuda.current_stream(out.device).synchronize()
+        host_out = torch.empty(out.numel(), dtype=out.dtype)
+        dist.all_gather(list(host_out.view(world, -1).unbind(0)), mine.cpu(), group=group)
+        out.copy_(host_out)
+    else:
+        dist.all_gather(list(out.view(world, -1).unbind(0)), mine.clone(), group=group)
+
+
 def gather_layer(slot: torch.Tensor, rank: int, world: int, group=None) -> None:
     """In-place all-gather of the 1/N slices of one layer into ``slot`` (every
-    rank ends with the full layer).  NCCL reassembles over NVLink; gloo (CPU
-    tests) takes the list form."""
+    rank ends with the full layer).  NCCL reassembles over NVLink."""
     import torch.distributed as dist
 
     lo, hi = slice_bounds(slot.numel(), rank, world)
-    if slot.is_cuda:
+    if slot.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(slot, slot[lo:hi], group=group)
     else:
-        parts = list(slot.view(world, -1).unbind(0))
-        dist.all_gather(parts, slot[lo:hi].clone(), group=group)
+        _gloo_gather(slot, slot[lo:hi], group)
 
 
 def gather_shards(slot: torch.Tensor, shard: torch.Tensor, group=None) -> None:
@@ -192,11 +206,10 @@ def gather_shards(slot: torch.Tensor, shard: torch.Tensor, group=None) -> None:
     the list form."""
     import torch.distributed as dist
 
-    if slot.is_cuda:
+    if slot.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(slot, shard, group=group)
     else:
-        world = dist.get_world_size(group)
-        dist.all_gather(list(slot.view(world, -1).unbind(0)), shard, group=group)
+        _gloo_gather(slot, shard, group)
 
 
 class LayerStreamer:
@@ -336,7 +349,7 @@ class LayerStreamer:
             self._ensure_issued(self.k_use + self.n_slots - 1)
 
     def acquire(self, layer: int, stream: torch.cuda.Stream) -> int:
-        if layer not in self.host:
+        if layer not in self.host and layer not in self.shards:
             return self.resident[layer].data_ptr()
         k = self.k_use
         assert self.streamed[k % len(self.streamed)] == layer, "layers must be consumed in pass order"
@@ -345,7 +358,7 @@ class LayerStreamer:
         return self.slots[k % self.n_slots].data_ptr()
 
     def release(self, layer: int, stream: torch.cuda.Stream) -> None:
-        if layer not in self.host:
+        if layer not in self.host and layer not in self.shards:
             return
         k = self.k_use
         self.free[k % self.n_slots].record(stream)

@@ -44,6 +44,10 @@ def main():
         # name, M(rows), N, K, epilogue, grouped experts (0 = dense)
         ("8x22B MoE gate_up (bs 248, n 8)", 4464, 32768, 6144, native.EPI_SWIGLU, 8),
         ("8x22B MoE down (bs 248, n 8)", 4464, 6144, 16384, native.EPI_BF16_ROWSCALE, 8),
+        ("8x22B MoE gate_up (bs 472, n 8)", 8496, 32768, 6144, native.EPI_SWIGLU, 8),
+        ("8x22B MoE down (bs 472, n 8)", 8496, 6144, 16384, native.EPI_BF16_ROWSCALE, 8),
+        ("8x22B MoE gate_up (refill prefill 16k tokens)", 32768, 32768, 6144, native.EPI_SWIGLU, 8),
+        ("8x22B MoE down (refill prefill 16k tokens)", 32768, 6144, 16384, native.EPI_BF16_ROWSCALE, 8),
         ("8x22B QKV (T 2232)", 2232, 8192, 6144, native.EPI_BF16, 0),
         ("8x22B LM head (T 2232)", 2232, 32768, 6144, native.EPI_F32, 0),
         ("Mistral-7B re-prefill gate_up (64 seqs x 520)", 33280, 28672, 4096, native.EPI_SWIGLU, 0),
