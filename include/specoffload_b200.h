@@ -154,7 +154,7 @@ int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_off
 /* ---- K8: auxiliary ------------------------------------------------------- */
 int so_embed(const int32_t* tokens, const void* table, int T, int H, void* out, void* stream);
 int so_rmsnorm(const void* x, const void* w, int T, int H, float eps, void* out, void* stream);
-/* qkv [T, (hq+2hkv)·dh] → RoPE(q) into q_out [T,hq,dh]; RoPE(k), v appended
+/* qkv [T, (hq+2hkv)·dh] (dh % 8 == 0, dh ≤ 128, 16-B aligned) → RoPE(q) into q_out [T,hq,dh]; RoPE(k), v appended
  * to the paged caches at slot_mapping[t] (page·page_size + offset).
  * cache layout: [num_pages, hkv, page_size, dh]. */
 int so_rope_kv_append(const void* qkv, const int32_t* positions, const int32_t* slot_mapping,

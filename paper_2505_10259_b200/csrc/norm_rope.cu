@@ -68,46 +68,57 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const __nv_bfloat
   }
 }
 
-// One CTA per token.  Rotate-half RoPE (HF Mistral convention): for i < dh/2,
+// One warp per token (grid-stride).  Rotate-half RoPE (HF Mistral convention):
+// for i < dh/2,
 //   y[i]        = x[i]·cos(p·f_i) − x[i+dh/2]·sin(p·f_i)
 //   y[i+dh/2]   = x[i+dh/2]·cos(p·f_i) + x[i]·sin(p·f_i),   f_i = θ^(−2i/dh)
-// computed in fp32 and rounded once.  K and V go to the paged caches laid out
-// [page][kv_head][page_slot][dh].
-__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
-                                   const int32_t* __restrict__ slots, int hq, int hkv, int dh, float theta,
-                                   int page_size, __nv_bfloat16* __restrict__ q_out,
-                                   __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
-  const int t = blockIdx.x;
+// computed in fp32 and rounded once.  Lane l owns frequencies i = 2l, 2l+1:
+// its two f_i come from powf once per warp, its two sincosf once per token,
+// and every rotated head is one 4-B (bf16×2) load/store per lane per half —
+// a contiguous 128-B run per warp.  K and V go to the paged caches laid out
+// [page][kv_head][page_slot][dh]; V rows move as 16-B vectors.
+constexpr int kRopeWarps = 4;
+
+__global__ void __launch_bounds__(32 * kRopeWarps) rope_append_kernel(
+    const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos, const int32_t* __restrict__ slots, int T,
+    int hq, int hkv, int dh, float theta, int page_size, __nv_bfloat16* __restrict__ q_out,
+    __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache) {
+  const int lane = threadIdx.x & 31;
   const int half = dh / 2;
   const int width = (hq + 2 * hkv) * dh;
-  const __nv_bfloat16* row = qkv + (size_t)t * width;
-  const float p = (float)pos[t];
-  const int slot = slots[t];
-  const int page = slot / page_size, off = slot % page_size;
-  // rotated heads: hq query heads then hkv key heads
-  for (int idx = threadIdx.x; idx < (hq + hkv) * half; idx += blockDim.x) {
-    const int h = idx / half, i = idx % half;
-    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)dh);
-    float sn, cs;
-    sincosf(p * inv_freq, &sn, &cs);
-    const float x0 = __bfloat162float(row[h * dh + i]);
-    const float x1 = __bfloat162float(row[h * dh + i + half]);
-    const __nv_bfloat16 y0 = __float2bfloat16_rn(x0 * cs - x1 * sn);
-    const __nv_bfloat16 y1 = __float2bfloat16_rn(x1 * cs + x0 * sn);
-    if (h < hq) {
-      __nv_bfloat16* qo = q_out + ((size_t)t * hq + h) * dh;
-      qo[i] = y0;
-      qo[i + half] = y1;
-    } else {
-      const int kh = h - hq;
-      __nv_bfloat16* ko = k_cache + (((size_t)page * hkv + kh) * page_size + off) * dh;
-      ko[i] = y0;
-      ko[i + half] = y1;
+  const bool own = 2 * lane < half;  // dh ≤ 128: at most one frequency pair per lane
+  const int i0 = 2 * lane;
+  const float f0 = own ? 1.0f / powf(theta, (float)(2 * i0) / (float)dh) : 0.0f;
+  const float f1 = own ? 1.0f / powf(theta, (float)(2 * (i0 + 1)) / (float)dh) : 0.0f;
+  for (int t = blockIdx.x * kRopeWarps + (threadIdx.x >> 5); t < T; t += gridDim.x * kRopeWarps) {
+    const __nv_bfloat16* row = qkv + (size_t)t * width;
+    const float p = (float)pos[t];
+    const int slot = slots[t];
+    const int page = slot / page_size, off = slot % page_size;
+    float s0 = 0.0f, c0 = 0.0f, s1 = 0.0f, c1 = 0.0f;
+    if (own) {
+      sincosf(p * f0, &s0, &c0);
+      sincosf(p * f1, &s1, &c1);
     }
-  }
-  for (int idx = threadIdx.x; idx < hkv * dh; idx += blockDim.x) {
-    const int kh = idx / dh, d = idx % dh;
-    v_cache[(((size_t)page * hkv + kh) * page_size + off) * dh + d] = row[(hq + hkv) * dh + idx];
+    if (own) {
+      for (int h = 0; h < hq + hkv; ++h) {
+        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(row + h * dh + i0);
+        const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(row + h * dh + half + i0);
+        const float2 x0 = __bfloat1622float2(a), x1 = __bfloat1622float2(b);
+        const __nv_bfloat162 y0 = __floats2bfloat162_rn(x0.x * c0 - x1.x * s0, x0.y * c1 - x1.y * s1);
+        const __nv_bfloat162 y1 = __floats2bfloat162_rn(x1.x * c0 + x0.x * s0, x1.y * c1 + x0.y * s1);
+        __nv_bfloat16* o = h < hq ? q_out + ((size_t)t * hq + h) * dh
+                                  : k_cache + (((size_t)page * hkv + (h - hq)) * page_size + off) * dh;
+        *reinterpret_cast<__nv_bfloat162*>(o + i0) = y0;
+        *reinterpret_cast<__nv_bfloat162*>(o + half + i0) = y1;
+      }
+    }
+    const int vec = dh / 8;  // 16-B vectors per V head row
+    for (int idx = lane; idx < hkv * vec; idx += 32) {
+      const int kh = idx / vec, c = idx % vec;
+      *reinterpret_cast<int4*>(v_cache + (((size_t)page * hkv + kh) * page_size + off) * dh + c * 8) =
+          *reinterpret_cast<const int4*>(row + (hq + hkv) * dh + kh * dh + c * 8);
+    }
   }
 }
 
@@ -200,10 +211,20 @@ extern "C" int so_rope_kv_append(const void* qkv, const int32_t* positions, cons
                                  int hq, int hkv, int dh, float rope_theta, int page_size, void* q_out,
                                  void* k_cache, void* v_cache, void* stream) {
   SO_REQUIRE(qkv && positions && slot_mapping && q_out && k_cache && v_cache, SO_E_NULLPTR);
-  SO_REQUIRE(T >= 0 && hq > 0 && hkv > 0 && hq % hkv == 0 && dh > 0 && dh % 2 == 0 && page_size > 0, SO_E_SHAPE);
+  SO_REQUIRE(T >= 0 && hq > 0 && hkv > 0 && hq % hkv == 0 && dh > 0 && dh % 8 == 0 && dh <= 128 && page_size > 0,
+             SO_E_SHAPE);
+  SO_REQUIRE(aligned16(qkv) && aligned16(q_out) && aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (T == 0) return SO_OK;
-  rope_append_kernel<<<T, 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(qkv), positions, slot_mapping, hq, hkv, dh, rope_theta, page_size,
+  static int ctas = 0;
+  if (ctas == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = 16 * sms;  // 64 warps per SM, grid-stride over the tokens
+  }
+  const int need = (T + kRopeWarps - 1) / kRopeWarps;
+  rope_append_kernel<<<need < ctas ? need : ctas, 32 * kRopeWarps, 0, as_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), positions, slot_mapping, T, hq, hkv, dh, rope_theta, page_size,
       reinterpret_cast<__nv_bfloat16*>(q_out), reinterpret_cast<__nv_bfloat16*>(k_cache),
       reinterpret_cast<__nv_bfloat16*>(v_cache));
   SO_CHECK_LAUNCH();
