@@ -21,7 +21,10 @@ namespace {
 
 constexpr int kRows = 64;   // query rows per CTA (4 warps × 16)
 constexpr int kKeys = 32;   // keys per smem tile
-constexpr int kStages = 4;  // cp.async ring depth (4 × 16 KB of K+V at dh = 128)
+#ifndef SO_ATTN_STAGES
+#define SO_ATTN_STAGES 4
+#endif
+constexpr int kStages = SO_ATTN_STAGES;  // cp.async ring depth (16 KB of K+V per stage at dh = 128)
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
