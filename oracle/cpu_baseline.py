@@ -57,11 +57,15 @@ class CpuSample:
     cores: int
 
 
-def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4, seed: int = 0) -> CpuSample:
-    """target/draft: objects with the ModelArch fields (vocab, hidden, ...)."""
+def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4, seed: int = 0,
+            cache: dict | None = None) -> CpuSample:
+    """target/draft: objects with the ModelArch fields (vocab, hidden, ...).
+    ``cache`` (a dict kept by the caller) holds the weights between repeated
+    measurements, so each repetition times only the forward passes."""
     at, ad = _arch(target), _arch(draft)
     rng = np.random.default_rng(seed)
-    wt = _weights(at, seed)
+    cache = {} if cache is None else cache
+    wt = cache.get("t") or cache.setdefault("t", _weights(at, 0))
     kv = KV(at, sample_seqs, ctx + n_cand + 2)
     kv.k[...] = rng.standard_normal(kv.k.shape, dtype=np.float32)
     kv.v[...] = rng.standard_normal(kv.v.shape, dtype=np.float32)
@@ -69,8 +73,8 @@ def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4
     t0 = time.perf_counter()
     forward(at, wt, kv, list(range(sample_seqs)), toks, [ctx] * sample_seqs, True, "all")
     t_t = time.perf_counter() - t0
-    del wt, kv
-    wd = _weights(ad, seed + 1)
+    del kv
+    wd = cache.get("d") or cache.setdefault("d", _weights(ad, 1))
     kvd = KV(ad, sample_seqs, ctx + n_cand + 2)
     t0 = time.perf_counter()
     forward(ad, wd, kvd, list(range(sample_seqs)), [[int(t[0])] for t in toks], [ctx] * sample_seqs, True, "last")
