@@ -171,6 +171,10 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* q_start, const int32_t* kv_before,
                   int bs, int max_q, int hq, int hkv, int dh, int page_size,
                   float scale, void* out, void* stream);
+/* K/V tile staging (process-wide; tests and benchmarks): 0 = TMA boxes issued
+ * by one thread where the page size allows (pages of ≤ 32 slots dividing 32,
+ * or multiples of 32), else cp.async; 1 = cp.async by every thread. */
+int so_attn_set_variant(int variant);
 
 /* ---- K1: layer streamer -------------------------------------------------
  * Pinned host → HBM window slot, `chunk`-byte cudaMemcpyAsync pieces on the

@@ -15,6 +15,10 @@
 // contiguous [page_size, dh] block per kv-head, so a tile is one coalesced
 // 8–16 KB run); S = QKᵀ and O += PV run on bf16 mma.sync with fp32 accumulate;
 // the softmax is the online (flash) form with quad-shuffle row reductions.
+#include <cuda.h>
+
+#include <cstring>
+
 #include "common.cuh"
 
 namespace {
@@ -69,28 +73,73 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int DH>
+// Two ways to stage a K/V tile (the compute that follows is shared):
+//   TMA = false  every thread issues 16-B cp.async copies (any page size),
+//                tile rows XOR-swizzled in 256-B rows;
+//   TMA = true   one thread issues 2-D TMA boxes of [min(page,32) rows × 64
+//                columns] per page and half-row (SWIZZLE_128B), completion on
+//                a per-stage mbarrier — the other 127 threads spend no issue
+//                slots on address generation, which ncu showed as a third of
+//                the instruction stream of this latency-bound kernel.
+template <int DH, bool TMA>
 struct Tile {
   static constexpr int kChunks = DH / 8;                 // 16-B chunks per key row
   static constexpr int kBytes = kKeys * DH * 2;          // one K or V tile
   // swizzled byte offset of (key row, chunk)
   __device__ __forceinline__ static uint32_t off(int row, int chunk) {
-    return (uint32_t)(row * DH * 2 + ((chunk ^ (row & 7)) << 4));
+    if constexpr (TMA)  // [half][row][128 B], SWIZZLE_128B: chunk ^ (row mod 8) inside each 128-B row
+      return (uint32_t)((chunk >> 3) * (kKeys * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+    else
+      return (uint32_t)(row * DH * 2 + ((chunk ^ (row & 7)) << 4));
   }
 };
 
-template <int DH>
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 #ifndef SO_ATTN_MINB
 #define SO_ATTN_MINB 3  // CTAs per SM the register budget must allow (3 × 128 threads ≤ 170 regs)
 #endif
 
+template <int DH, bool TMA>
 __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
     const int32_t* __restrict__ block_table, int max_pages, const int32_t* __restrict__ q_start,
     const int32_t* __restrict__ kv_before, int hq, int hkv, int page_size, float scale_log2,
     __nv_bfloat16* __restrict__ out) {
-  using TL = Tile<DH>;
-  extern __shared__ __align__(128) uint8_t smem[];
+  using TL = Tile<DH, TMA>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // SWIZZLE_128B boxes land on 1024-B aligned stage buffers
+  uint8_t* smem = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
+                      : smem_raw;
   const int tile = blockIdx.x, g_kv = blockIdx.y, s = blockIdx.z;
   const int G = hq / hkv;
   const int qs = q_start[s];
@@ -132,15 +181,41 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   float mA = -INFINITY, mB = -INFINITY, lA = 0.0f, lB = 0.0f;
 
   // The sequence's page list is staged in smem once: every K/V row resolves its
-  // page from it, so issuing a tile's cp.asyncs never waits on a dependent
+  // page from it, so issuing a tile's copies never waits on a dependent
   // global load (which had cost one memory latency per tile step).
-  int32_t* bt = reinterpret_cast<int32_t*>(smem + kStages * 2 * TL::kBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * 2 * TL::kBytes);  // TMA stage barriers
+  int32_t* bt = reinterpret_cast<int32_t*>(full + kStages);
+  const int used = min(max_pages, (n_keys + page_size - 1) / page_size);
   {
     const int32_t* gbt = block_table + (size_t)s * max_pages;
-    const int used = min(max_pages, (n_keys + page_size - 1) / page_size);
     for (int i = threadIdx.x; i < used; i += kThreads) bt[i] = gbt[i];
+    if (TMA && threadIdx.x == 0) {
+      for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+    }
     __syncthreads();
   }
+  // TMA: one thread puts tile kt's K and V boxes in flight on full[stage]
+  const int box_rows = page_size < kKeys ? page_size : kKeys;
+  auto issue_tile = [&](int kt, int buf) {
+    const int key0 = kt * kKeys;
+    uint8_t* sk = smem + buf * 2 * TL::kBytes;
+    uint8_t* sv = sk + TL::kBytes;
+    mbar_expect_tx(&full[buf], 2 * TL::kBytes);
+    for (int r = 0; r < kKeys; r += box_rows) {
+      const int key = key0 + r;
+      const int pi = key / page_size;
+      const int page = pi < used ? bt[pi] : bt[0];  // past the sequence: any valid page (masked / zeroed below)
+      const int row = (page * hkv + g_kv) * page_size + key % page_size;
+#pragma unroll
+      for (int h = 0; h < DH / 64; ++h) {
+        tma_box(sk + h * (kKeys * 128) + r * 128, &tmK, &full[buf], h * 64, row);
+        tma_box(sv + h * (kKeys * 128) + r * 128, &tmV, &full[buf], h * 64, row);
+      }
+    }
+  };
   // Each key row resolves its own page, so any page size works (a tile may
   // span several pages); rows at or past n_keys are zero-filled, keeping
   // 0·V finite for masked keys whatever the unwritten cache holds.
@@ -161,20 +236,41 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
     }
   };
 
-  // kStages-deep cp.async ring: kStages−1 tiles stream from HBM while one is
-  // consumed (one commit group per tile, empty groups past the end keep the
-  // wait_group arithmetic uniform)
+  // kStages-deep ring: kStages−1 tiles stream from HBM while one is consumed
+  // (cp.async: one commit group per tile, empty groups past the end keep the
+  // wait_group arithmetic uniform; TMA: one mbarrier phase per tile and stage)
+  if constexpr (TMA) {
+    if (threadIdx.x == 0)
+      for (int p = 0; p < kStages - 1 && p < n_tiles; ++p) issue_tile(p, p);
+  } else {
 #pragma unroll
-  for (int p = 0; p < kStages - 1; ++p) {
-    if (p < n_tiles) load_tile(p, p);
-    cp_commit();
+    for (int p = 0; p < kStages - 1; ++p) {
+      if (p < n_tiles) load_tile(p, p);
+      cp_commit();
+    }
   }
   for (int kt = 0; kt < n_tiles; ++kt) {
     const int nxt = kt + kStages - 1;
-    if (nxt < n_tiles) load_tile(nxt, nxt % kStages);
-    cp_commit();
-    cp_wait<kStages - 1>();
-    __syncthreads();
+    if constexpr (TMA) {
+      // the stage of tile nxt was consumed in iteration kt−1 (closing barrier)
+      if (threadIdx.x == 0 && nxt < n_tiles) issue_tile(nxt, nxt % kStages);
+      mbar_wait(&full[kt % kStages], (kt / kStages) & 1);
+      const int valid = n_keys - kt * kKeys;
+      if (valid < kKeys) {  // last tile: V rows past the keys hold stale data (0·NaN must not reach O)
+        uint8_t* sv = smem + (kt % kStages) * 2 * TL::kBytes + TL::kBytes;
+        for (int i = threadIdx.x; i < (kKeys - valid) * (DH / 64) * 8; i += kThreads) {
+          const int row = valid + i / ((DH / 64) * 8), rest = i % ((DH / 64) * 8);
+          *reinterpret_cast<int4*>(sv + (rest >> 3) * (kKeys * 128) + row * 128 + ((rest & 7) << 4)) =
+              make_int4(0, 0, 0, 0);
+        }
+        __syncthreads();
+      }
+    } else {
+      if (nxt < n_tiles) load_tile(nxt, nxt % kStages);
+      cp_commit();
+      cp_wait<kStages - 1>();
+      __syncthreads();
+    }
     if (warp_live) {
       const uint32_t sk = smem_u32(smem + (kt % kStages) * 2 * TL::kBytes);
       const uint32_t sv = sk + TL::kBytes;
@@ -261,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
     }
     __syncthreads();
   }
-  cp_wait<0>();
+  if constexpr (!TMA) cp_wait<0>();
   if (!warp_live) return;
   // ---- normalise and store ----
   lA += __shfl_xor_sync(0xffffffffu, lA, 1);
@@ -280,28 +376,88 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   }
 }
 
-template <int DH>
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// The cache of one layer as a 2-D tensor [rows = page·hkv·page_size + slot, dh]; every coordinate the kernel
+// issues names a page of the block table, so the row extent only bounds the map.
+int cache_map(CUtensorMap* m, const void* base, int dh, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return SO_E_DRIVER;
+  cuuint64_t dims[2] = {(cuuint64_t)dh, (cuuint64_t)1 << 31};
+  cuuint64_t strides[1] = {(cuuint64_t)dh * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SO_OK : SO_E_DRIVER;
+}
+
+int g_attn_variant = 0;  // 0 = TMA staging where the page size allows it, 1 = cp.async staging
+
+template <int DH, bool TMA>
 int launch(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
            const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
            cudaStream_t st) {
   const int G = hq / hkv;
   const int tiles = (max_q * G + kRows - 1) / kRows;
-  const size_t smem = (size_t)kStages * 2 * Tile<DH>::kBytes + (size_t)max_pages * sizeof(int32_t);
+  const size_t smem = (TMA ? 1024 : 0) + (size_t)kStages * 2 * Tile<DH, TMA>::kBytes + kStages * sizeof(uint64_t) +
+                      (size_t)max_pages * sizeof(int32_t);
+  auto kern = attn_paged_kernel<DH, TMA>;
   static size_t attr_bytes = 0;  // raised when a longer block table needs more smem
   if (smem > attr_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
-      e = cudaFuncSetAttribute(attn_paged_kernel<DH>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return (int)e;
     attr_bytes = smem;
   }
+  CUtensorMap mk, mv;
+  memset(&mk, 0, sizeof(mk));
+  memset(&mv, 0, sizeof(mv));
+  if (TMA) {
+    const int box_rows = page_size < kKeys ? page_size : kKeys;
+    int rc = cache_map(&mk, k, DH, box_rows);
+    if (rc) return rc;
+    rc = cache_map(&mv, v, DH, box_rows);
+    if (rc) return rc;
+  }
   dim3 grid(tiles, hkv, bs);
-  attn_paged_kernel<DH><<<grid, kThreads, smem, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
-      reinterpret_cast<const __nv_bfloat16*>(v), bt, max_pages, q_start, kv_before, hq, hkv, page_size,
-      scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));
+  kern<<<grid, kThreads, smem, st>>>(mk, mv, reinterpret_cast<const __nv_bfloat16*>(q),
+                                     reinterpret_cast<const __nv_bfloat16*>(k),
+                                     reinterpret_cast<const __nv_bfloat16*>(v), bt, max_pages, q_start, kv_before, hq,
+                                     hkv, page_size, scale * 1.4426950408889634f,
+                                     reinterpret_cast<__nv_bfloat16*>(out));
   SO_CHECK_LAUNCH();
   return SO_OK;
+}
+
+template <int DH>
+int launch_dh(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
+              const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
+              cudaStream_t st) {
+  // TMA boxes cover whole pages (≤ 32 rows) or 32-row halves of larger pages
+  const bool tma_ok = (page_size <= kKeys ? kKeys % page_size == 0 : page_size % kKeys == 0) &&
+                      (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+  if (g_attn_variant == 0 && tma_ok)
+    return launch<DH, true>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
+  return launch<DH, false>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
 }
 
 }  // namespace
@@ -315,9 +471,15 @@ extern "C" int so_attn_paged(const void* q, const void* k_cache, const void* v_c
   SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (bs == 0) return SO_OK;
   cudaStream_t st = as_stream(stream);
-  if (dh == 128) return launch<128>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+  if (dh == 128) return launch_dh<128>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
                                     page_size, scale, out, st);
-  if (dh == 64) return launch<64>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+  if (dh == 64) return launch_dh<64>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
                                   page_size, scale, out, st);
   return SO_E_UNSUPPORTED;
+}
+
+extern "C" int so_attn_set_variant(int variant) {
+  SO_REQUIRE(variant == 0 || variant == 1, SO_E_SHAPE);
+  g_attn_variant = variant;
+  return SO_OK;
 }

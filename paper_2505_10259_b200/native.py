@@ -34,6 +34,7 @@ _SIGNATURES = {
     "so_device_sm_count": (c_int, []),
     "so_set_device": (c_int, [c_int]),
     "so_gemm_set_variant": (c_int, [c_int]),
+    "so_attn_set_variant": (c_int, [c_int]),
     "so_accept_greedy": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_accept_sample": (c_int, [_P, _P, _P, _P, _P, _P, c_float, c_int, c_int, c_int, _P, _P, _P]),
     "so_sample_tokens": (c_int, [_P, c_int64, _P, c_float, c_int, c_int, _P, c_int64, _P, c_int64, _P]),
@@ -114,6 +115,11 @@ def reset_launch_counter() -> None:
 def gemm_set_variant(variant: int) -> None:
     """0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair (cta_group::2) tiles wherever legal."""
     _check(lib().so_gemm_set_variant(variant), "so_set_device")
+
+
+def attn_set_variant(variant: int) -> None:
+    """0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging."""
+    _check(lib().so_attn_set_variant(variant), "so_set_device")
 
 
 def set_device(index: int) -> None:

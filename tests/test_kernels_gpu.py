@@ -314,8 +314,19 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
     (64, 4, 2, [5, 5, 5], [10, 100, 0], 32),                 # verify, tiny heads
     (128, 32, 8, [17, 1, 64, 100], [0, 0, 0, 0], 16),        # prefill
     (64, 4, 2, [33, 1], [3, 200], 64),                       # mixed
+    (128, 32, 8, [9, 1, 40], [300, 31, 0], 8),               # small pages: 4 TMA boxes per tile
+    (64, 4, 2, [5, 3], [20, 7], 5),                          # odd pages: cp.async staging only
 ])
-def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps):
+@pytest.mark.parametrize("attn_variant", [0, 1], ids=["tma", "cp_async"])
+def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
+    native.attn_set_variant(attn_variant)
+    try:
+        _check_attn(dh, hq, hkv, qlens, kvbs, ps)
+    finally:
+        native.attn_set_variant(0)
+
+
+def _check_attn(dh, hq, hkv, qlens, kvbs, ps):
     bs = len(qlens)
     max_len = max(q + k for q, k in zip(qlens, kvbs))
     pps = (max_len + ps - 1) // ps + 1

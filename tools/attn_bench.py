@@ -54,6 +54,9 @@ def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20):
 
 
 if __name__ == "__main__":
-    res = [run(), run(bs=128, n=4), run(bs=248, n=8, ctx=2000)]
-    for r in res:
-        print(json.dumps(r))
+    for variant, label in ((1, "cp_async"), (0, "tma")):
+        native.attn_set_variant(variant)
+        for r in [run(), run(bs=128, n=4), run(bs=248, n=8, ctx=2000), run(bs=472, n=8, ctx=520),
+                  run(bs=64, n=519, ctx=1, hq=32, hkv=8)]:
+            r["staging"] = label
+            print(json.dumps(r))
