@@ -184,13 +184,17 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   // page from it, so issuing a tile's copies never waits on a dependent
   // global load (which had cost one memory latency per tile step).
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * 2 * TL::kBytes);  // TMA stage barriers
-  int32_t* bt = reinterpret_cast<int32_t*>(full + kStages);
+  uint64_t* empty = full + kStages;  // TMA: every warp arrives once it has consumed the stage
+  int32_t* bt = reinterpret_cast<int32_t*>(empty + kStages);
   const int used = min(max_pages, (n_keys + page_size - 1) / page_size);
   {
     const int32_t* gbt = block_table + (size_t)s * max_pages;
     for (int i = threadIdx.x; i < used; i += kThreads) bt[i] = gbt[i];
     if (TMA && threadIdx.x == 0) {
-      for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+      for (int i = 0; i < kStages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], kThreads / 32);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
@@ -252,8 +256,13 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   for (int kt = 0; kt < n_tiles; ++kt) {
     const int nxt = kt + kStages - 1;
     if constexpr (TMA) {
-      // the stage of tile nxt was consumed in iteration kt−1 (closing barrier)
-      if (threadIdx.x == 0 && nxt < n_tiles) issue_tile(nxt, nxt % kStages);
+      // the stage of tile nxt held tile kt−1: refill it once every warp is done
+      // with that tile — warps otherwise run up to kStages−1 tiles apart, no
+      // CTA-wide barrier per tile
+      if (threadIdx.x == 0 && nxt < n_tiles) {
+        if (kt >= 1) mbar_wait(&empty[(kt - 1) % kStages], ((kt - 1) / kStages) & 1);
+        issue_tile(nxt, nxt % kStages);
+      }
       mbar_wait(&full[kt % kStages], (kt / kStages) & 1);
       const int valid = n_keys - kt * kKeys;
       if (valid < kKeys) {  // last tile: V rows past the keys hold stale data (0·NaN must not reach O)
@@ -355,7 +364,12 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
         }
       }
     }
-    __syncthreads();
+    if constexpr (TMA) {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[kt % kStages])) : "memory");
+    } else {
+      __syncthreads();
+    }
   }
   if constexpr (!TMA) cp_wait<0>();
   if (!warp_live) return;
@@ -417,7 +431,7 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
            cudaStream_t st) {
   const int G = hq / hkv;
   const int tiles = (max_q * G + kRows - 1) / kRows;
-  const size_t smem = (TMA ? 1024 : 0) + (size_t)kStages * 2 * Tile<DH, TMA>::kBytes + kStages * sizeof(uint64_t) +
+  const size_t smem = (TMA ? 1024 : 0) + (size_t)kStages * 2 * Tile<DH, TMA>::kBytes + 2 * kStages * sizeof(uint64_t) +
                       (size_t)max_pages * sizeof(int32_t);
   auto kern = attn_paged_kernel<DH, TMA>;
   static size_t attr_bytes = 0;  // raised when a longer block table needs more smem
