@@ -136,6 +136,14 @@ int so_moe_combine(const void* y_perm, const int32_t* token_rows, const void* re
  * columns. */
 int so_gemm_bf16(const void* A, const void* B, int M, int N, int K,
                  void* C, int ldc, int epilogue, const void* aux, void* stream);
+/* Same contract with caller-owned scratch: skinny GEMMs (M ≤ 256 with fewer
+ * output tiles than half the SMs — the draft's decode steps) split K across
+ * the SMs into fp32 partials in `workspace`, then one reduce kernel applies
+ * the epilogue.  so_gemm_workspace_bytes(M, N, K) is the scratch that choice
+ * needs (0 = no split); a smaller workspace falls back to so_gemm_bf16. */
+size_t so_gemm_workspace_bytes(int M, int N, int K);
+int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
+                    const void* aux, void* workspace, size_t ws_bytes, void* stream);
 
 /* Tile variant of the GEMMs (process-wide; for tests and benchmarks):
  * 0 = auto (persistent kernels with double-buffered TMEM accumulators:

@@ -562,15 +562,22 @@ struct CfgP {
 
 struct TileInfo {
   int expert, row0, row_end, n0;
+  int ks, kb0, kb1;  // split-K slice of this tile (k-blocks [kb0, kb1))
   bool valid;
 };
 
-// tile t → rows/expert/columns (tileM = output rows of one tile: 128, or 256 for a pair)
+// tile t → rows/expert/columns (tileM = output rows of one tile: 128, or 256 for a
+// pair); with k_split > 1, consecutive tiles are the K slices of one output tile
 __device__ __forceinline__ TileInfo tile_info(int t, const int32_t* __restrict__ offs, int E, int M, int m_tiles,
-                                              int n_tiles, int tileM, int BNc) {
+                                              int n_tiles, int tileM, int BNc, int k_split = 1, int num_kb = 0) {
   int mt, nt;
-  raster_tile(t, m_tiles, n_tiles, mt, nt);
   TileInfo ti;
+  ti.ks = t % k_split;
+  t /= k_split;
+  const int kbs = (num_kb + k_split - 1) / k_split;
+  ti.kb0 = ti.ks * kbs;
+  ti.kb1 = min(num_kb, ti.kb0 + kbs);
+  raster_tile(t, m_tiles, n_tiles, mt, nt);
   ti.expert = 0;
   ti.row0 = mt * tileM;
   ti.row_end = M;
@@ -595,17 +602,23 @@ __device__ __forceinline__ TileInfo tile_info(int t, const int32_t* __restrict__
   return ti;
 }
 
+// EPI == SO_EPI_PARTIAL: split-K slice — the fp32 accumulator goes to
+// partial[ks][row][col]; splitk_reduce_kernel sums the slices and applies the
+// real epilogue.  Used for skinny GEMMs (draft decode steps, M ≤ 128) whose
+// few output tiles would otherwise stream the weights through a few SMs.
+constexpr int SO_EPI_PARTIAL = 100;
+
 template <int CG, int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const int32_t* __restrict__ offs, int E, int M, int N, int K, void* __restrict__ C, int ldc,
-                    const void* __restrict__ aux, int m_tiles, int n_tiles) {
+                    const void* __restrict__ aux, int m_tiles, int n_tiles, int k_split) {
   using CF = CfgP<CG, BN>;
   constexpr int kTileM = 128 * CG;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int total = m_tiles * n_tiles;
+  const int total = m_tiles * n_tiles * k_split;
   const int num_kb = K / BK;
 
   extern __shared__ uint8_t smem_raw[];
@@ -657,11 +670,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t leader_full0 = smem_u32(&full[0]) & 0xFEFFFFFFu;
       uint32_t it = 0;
       for (int t = unit; t < total; t += units) {
-        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN, k_split, num_kb);
         if (!ti.valid) continue;
         const int rowA = ti.row0 + (int)rank * 128;
         const int rowB = ti.n0 + (CG == 2 ? (int)rank * (BN / 2) : 0);
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++it) {
           const int s = it % CF::kStages;
           const uint32_t ph = (it / CF::kStages) & 1;
           mbar_wait_guard(&empty[s], ph ^ 1);
@@ -685,13 +698,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  ((uint32_t)(kTileM >> 4) << 24);
       uint32_t it = 0, acc = 0;
       for (int t = unit; t < total; t += units) {
-        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+        const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN, k_split, num_kb);
         if (!ti.valid) continue;
         const uint32_t buf = acc & 1, aph = (acc >> 1) & 1;
         mbar_wait_guard(&tmem_empty[buf], aph ^ 1);  // the epilogue drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem_base + buf * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb, ++it) {
           const int s = it % CF::kStages;
           const uint32_t ph = (it / CF::kStages) & 1;
           mbar_wait_guard(&full[s], ph);
@@ -700,10 +713,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(sB + s * CF::kBBytes);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t accum = (kb != ti.kb0) | (kk != 0);
             if constexpr (CG == 2)
-              umma_bf16_pair(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+              umma_bf16_pair(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, accum);
             else
-              umma_bf16(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, (kb | kk) != 0);
+              umma_bf16(d, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc, accum);
           }
           if constexpr (CG == 2) umma_commit_pair(&empty[s]);
           else umma_commit(&empty[s]);
@@ -724,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("mapa.shared::cluster.u32 %0, %0, 0;" : "+r"(empty1));
     }
     for (int t = unit; t < total; t += units) {
-      const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN);
+      const TileInfo ti = tile_info(t, offs, E, M, m_tiles, n_tiles, kTileM, BN, k_split, num_kb);
       if (!ti.valid) continue;
       const uint32_t buf = acc & 1, aph = (acc >> 1) & 1;
       mbar_wait_guard(&tmem_full[buf], aph);
@@ -732,7 +746,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int grow = ti.row0 + (int)rank * 128 + row;
       const bool valid = grow < ti.row_end && grow < M;
       const uint32_t tbase = tmem_base + buf * BN + ((uint32_t)(quarter * 32) << 16);
-      epilogue_tile<BN, EPI>(tbase, valid, grow, ti.n0, N, C, ldc, aux);
+      if constexpr (EPI == SO_EPI_PARTIAL)
+        epilogue_tile<BN, SO_EPI_F32>(tbase, valid, grow, ti.n0, N,
+                                      reinterpret_cast<float*>(C) + (size_t)ti.ks * M * N, N, nullptr);
+      else
+        epilogue_tile<BN, EPI>(tbase, valid, grow, ti.n0, N, C, ldc, aux);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -755,6 +773,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::kTmemCols));
   }
+}
+
+// Split-K finish: out = EPI(Σ_ks partial[ks]) with the same arithmetic as the
+// fused epilogues (bf16 rounding before the residual add, SwiGLU on the 64-row
+// interleaved gate/up column blocks).  One thread per 8 output columns.
+template <int EPI>
+__global__ void splitk_reduce_kernel(const float* __restrict__ partial, int k_split, int M, int N, void* __restrict__ C,
+                                     int ldc, const void* __restrict__ aux) {
+  const int out_cols = EPI == SO_EPI_SWIGLU ? N / 2 : N;
+  const int groups = out_cols / 8;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * groups) return;
+  const int row = idx / groups, c0 = (idx % groups) * 8;
+  float f[8];
+  if constexpr (EPI == SO_EPI_SWIGLU) {
+    // output column c ↔ gate column 128·(c/64) + c%64, up column +64
+    const int gcol = 128 * (c0 / 64) + c0 % 64;
+    float g[8], u[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = u[j] = 0.0f;
+    for (int ks = 0; ks < k_split; ++ks) {
+      const float* pr = partial + ((size_t)ks * M + row) * N;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        g[j] += pr[gcol + j];
+        u[j] += pr[gcol + 64 + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = silu(g[j]) * u[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = 0.0f;
+    for (int ks = 0; ks < k_split; ++ks) {
+      const float4* pr = reinterpret_cast<const float4*>(partial + ((size_t)ks * M + row) * N + c0);
+      const float4 a = pr[0], b = pr[1];
+      f[0] += a.x, f[1] += a.y, f[2] += a.z, f[3] += a.w, f[4] += b.x, f[5] += b.y, f[6] += b.z, f[7] += b.w;
+    }
+  }
+  if constexpr (EPI == SO_EPI_F32) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + (size_t)row * ldc + c0);
+    dst[0] = make_float4(f[0], f[1], f[2], f[3]);
+    dst[1] = make_float4(f[4], f[5], f[6], f[7]);
+    return;
+  }
+  if constexpr (EPI == SO_EPI_BF16_RESID) {
+    float rr[8];
+    unpack8(*reinterpret_cast<const int4*>(reinterpret_cast<const __nv_bfloat16*>(aux) + (size_t)row * ldc + c0), rr);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = __bfloat162float(__float2bfloat16_rn(f[j])) + rr[j];
+  } else if constexpr (EPI == SO_EPI_BF16_ROWSCALE) {
+    const float w = reinterpret_cast<const float*>(aux)[row];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] *= w;
+  }
+  *reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(C) + (size_t)row * ldc + c0) = pack8(f);
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -838,7 +912,7 @@ int g_variant = 0;  // 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where 
 // persistent launch: one CTA (pair) per SM (pair), never more than the tiles
 template <int CG, int BN, int EPI>
 int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs, int E, int m_tiles,
-                      int M, int N, int K, void* C, int ldc, const void* aux, cudaStream_t st) {
+                      int M, int N, int K, void* C, int ldc, const void* aux, cudaStream_t st, int k_split = 1) {
   using CF = CfgP<CG, BN>;
   auto kern = gemm_tcp_kernel<CG, BN, EPI>;
   static bool attr_set = false;
@@ -848,7 +922,7 @@ int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_
     attr_set = true;
   }
   const int n_tiles = (N + BN - 1) / BN;
-  const int tiles = m_tiles * n_tiles;
+  const int tiles = m_tiles * n_tiles * k_split;
   int units = sm_count() / CG;
   if (units > tiles) units = tiles;
   if (units < 1) units = 1;
@@ -865,10 +939,10 @@ int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles, k_split);
     if (e != cudaSuccess) return (int)e;
   } else {
-    kern<<<units, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
+    kern<<<units, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles, k_split);
   }
   SO_CHECK_LAUNCH();
   return SO_OK;
@@ -947,7 +1021,71 @@ int gemm_dispatch(const void* A, const void* B, const int32_t* offs, int E, int 
   }
 }
 
+// Split-K choice for a dense GEMM with few output tiles (0 = not worth it)
+int splitk_factor(int M, int N, int K) {
+  if (M > 256 || g_variant == 3) return 0;
+  const int tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
+  const int sms = sm_count();
+  if (2 * tiles >= sms) return 0;
+  const int num_kb = K / BK;
+  int ks = (sms + tiles - 1) / tiles;
+  if (ks > num_kb / 4) ks = num_kb / 4;  // ≥ 4 k-blocks per slice
+  if (ks > 16) ks = 16;
+  while (ks > 1) {  // no empty slice
+    const int kbs = (num_kb + ks - 1) / ks;
+    if ((ks - 1) * kbs < num_kb) break;
+    --ks;
+  }
+  return ks >= 2 ? ks : 0;
+}
+
+template <int EPI>
+int launch_splitk(const void* A, const void* B, int M, int N, int K, void* C, int ldc, const void* aux, int ks,
+                  float* ws, cudaStream_t st) {
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, A, (uint64_t)M, (uint64_t)K, BM);
+  if (rc) return rc;
+  rc = make_map_3d(&mb, B, 1, (uint64_t)N, (uint64_t)K, 128);
+  if (rc) return rc;
+  rc = launch_persistent<1, 128, SO_EPI_PARTIAL>(ma, mb, nullptr, 1, (M + BM - 1) / BM, M, N, K, ws, N, nullptr, st,
+                                                ks);
+  if (rc) return rc;
+  const int out_cols = EPI == SO_EPI_SWIGLU ? N / 2 : N;
+  const int threads = M * (out_cols / 8);
+  splitk_reduce_kernel<EPI><<<(threads + 255) / 256, 256, 0, st>>>(ws, ks, M, N, C, ldc, aux);
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
 }  // namespace
+
+extern "C" size_t so_gemm_workspace_bytes(int M, int N, int K) {
+  const int ks = (M > 0 && N > 0 && K >= BK) ? splitk_factor(M, N, K) : 0;
+  return ks ? (size_t)ks * M * N * sizeof(float) : 0;
+}
+
+extern "C" int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
+                               const void* aux, void* workspace, size_t ws_bytes, void* stream) {
+  const int ks = (M > 0 && N > 0 && K >= BK && K % BK == 0 && N % 128 == 0) ? splitk_factor(M, N, K) : 0;
+  if (ks == 0 || workspace == nullptr || ws_bytes < (size_t)ks * M * N * sizeof(float))
+    return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, as_stream(stream));
+  SO_REQUIRE(A && B && C, SO_E_NULLPTR);
+  SO_REQUIRE(aligned16(A) && aligned16(B) && aligned16(C) && aligned16(workspace), SO_E_ALIGN);
+  if (epilogue == SO_EPI_SWIGLU) SO_REQUIRE(ldc % 8 == 0 && ldc >= N / 2, SO_E_SHAPE);
+  else if (epilogue == SO_EPI_F32) SO_REQUIRE(ldc % 4 == 0 && ldc >= N, SO_E_SHAPE);
+  else SO_REQUIRE(ldc % 8 == 0 && ldc >= N, SO_E_SHAPE);
+  if (epilogue == SO_EPI_BF16_RESID || epilogue == SO_EPI_BF16_ROWSCALE) SO_REQUIRE(aux != nullptr, SO_E_NULLPTR);
+  float* ws = reinterpret_cast<float*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  switch (epilogue) {
+    case SO_EPI_BF16: return launch_splitk<SO_EPI_BF16>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
+    case SO_EPI_F32: return launch_splitk<SO_EPI_F32>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
+    case SO_EPI_BF16_RESID: return launch_splitk<SO_EPI_BF16_RESID>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
+    case SO_EPI_SWIGLU: return launch_splitk<SO_EPI_SWIGLU>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
+    case SO_EPI_BF16_ROWSCALE: return launch_splitk<SO_EPI_BF16_ROWSCALE>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
+    default: return SO_E_UNSUPPORTED;
+  }
+}
 
 extern "C" int so_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
                             const void* aux, void* stream) {

@@ -42,6 +42,8 @@ _SIGNATURES = {
     "so_router_top2": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "so_moe_combine": (c_int, [_P, _P, _P, c_int, c_int, _P, _P]),
     "so_gemm_bf16": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
+    "so_gemm_workspace_bytes": (c_size_t, [c_int, c_int, c_int]),
+    "so_gemm_bf16_ex": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, _P]),
     "so_gemm_grouped_bf16": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
     "so_embed": (c_int, [_P, _P, c_int, c_int, _P, _P]),
     "so_rmsnorm": (c_int, [_P, _P, c_int, c_int, c_float, _P, _P]),
@@ -222,15 +224,36 @@ def moe_combine(y_perm, token_rows, resid, out, stream=None):
 
 # ---------------------------------------------------------------- GEMMs ---
 
+_splitk_ws: dict[int, torch.Tensor] = {}  # stream handle → grow-only split-K scratch (one per enqueuing stream)
+_splitk_lock = threading.Lock()
+
+
+def _gemm_workspace(M: int, N: int, K: int, stream: int, device) -> tuple[int, int]:
+    need = int(lib().so_gemm_workspace_bytes(M, N, K))
+    if need == 0:
+        return 0, 0
+    with _splitk_lock:
+        ws = _splitk_ws.get(stream)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(max(need, 16 << 20), dtype=torch.uint8, device=device)
+            _splitk_ws[stream] = ws
+    return ws.data_ptr(), ws.numel()
+
+
 def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None):
-    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05."""
+    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (skinny shapes: split-K over the SMs)."""
     M, K = a.shape
     N = b.shape[-2]
     assert b.shape[-1] == K
     _need(a, torch.bfloat16, "a")
     assert b.dtype == torch.bfloat16
-    _check(lib().so_gemm_bf16(_ptr(a), _ptr(b), M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux),
-                              _stream(stream)), "so_gemm_bf16")
+    st = _stream(stream)
+    ws, ws_bytes = _gemm_workspace(M, N, K, st, a.device)
+    _check(lib().so_gemm_bf16_ex(_ptr(a), _ptr(b), M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux), ws,
+                                 ws_bytes, st), "so_gemm_bf16")
+    if ws:
+        with _count_lock:
+            launches["kernels"] += 1  # the split-K reduce
 
 
 def gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None, stream=None):

@@ -354,3 +354,31 @@ def _check_attn(dh, hq, hkv, qlens, kvbs, ps):
     ref = _attn_ref(q, kc, vc, bt.long().cpu().numpy(), qs.cpu().numpy(), kvb.cpu().numpy(), hq, hkv, dh, ps)
     # P is rounded to bf16 for the PV product: |err| ≤ 2e-2 absolute on O(1) outputs
     torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 4096), (112, 4096, 14336), (64, 6144, 4096), (33, 2048, 2048),
+                                   (200, 1024, 8192)])
+def test_gemm_splitk_skinny(M, N, K):
+    """Draft decode-step shapes: K split over the SMs into fp32 partials, then
+    one reduce applies the epilogue — every epilogue against an fp32 reference."""
+    assert native.lib().so_gemm_workspace_bytes(M, N, K) > 0  # the split is taken for these shapes
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
+    a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ref = a.float() @ b.float().T
+    out = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
+    native.gemm(a, b, out)
+    _bf16_close(out, ref)
+    out32 = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    native.gemm(a, b, out32, native.EPI_F32)
+    torch.testing.assert_close(out32, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+    r = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
+    outr = torch.empty_like(out)
+    native.gemm(a, b, outr, native.EPI_BF16_RESID, r)
+    _bf16_close(outr, ref.to(torch.bfloat16).float() + r.float())
+    from paper_2505_10259_b200.weights import interleave_gate_up
+
+    wg, wu = b[: N // 2], b[N // 2:]
+    outs = torch.empty(M, N // 2, dtype=torch.bfloat16, device=DEV)
+    native.gemm(a, interleave_gate_up(wg, wu).contiguous(), outs, native.EPI_SWIGLU)
+    _bf16_close(outs, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T))

@@ -53,6 +53,11 @@ def main():
         ("Mistral-7B re-prefill gate_up (64 seqs x 520)", 33280, 28672, 4096, native.EPI_SWIGLU, 0),
         ("Mistral-7B re-prefill down", 33280, 4096, 14336, native.EPI_BF16_RESID, 0),
         ("square 8192^3", 8192, 8192, 8192, native.EPI_BF16, 0),
+        ("draft decode step QKV (64 seqs)", 64, 6144, 4096, native.EPI_BF16, 0),
+        ("draft decode step O (64 seqs)", 64, 4096, 4096, native.EPI_BF16_RESID, 0),
+        ("draft decode step gate_up (64 seqs)", 64, 28672, 4096, native.EPI_SWIGLU, 0),
+        ("draft decode step down (64 seqs)", 64, 4096, 14336, native.EPI_BF16_RESID, 0),
+        ("draft decode step down (112 seqs)", 112, 4096, 14336, native.EPI_BF16_RESID, 0),
     ]
     for name, M, N, K, epi, E in shapes:
         if only and only not in name:
@@ -82,9 +87,11 @@ def main():
                 native.gemm_set_variant(variant)
                 t = timed(fn, reps=20)
                 best[label] = min(best.get(label, t), t)
+        wbytes = max(E, 1) * N * K * 2  # weight bytes each launch streams (decode steps are bound by these)
         for _, label in variants:
             t = best[label]
-            res[label] = {"ms": t * 1e3, "tflops": flops / t / 1e12, "frac_of_peak": flops / t / 1e12 / PEAK}
+            res[label] = {"ms": t * 1e3, "tflops": flops / t / 1e12, "frac_of_peak": flops / t / 1e12 / PEAK,
+                          "weight_GBps": wbytes / t / 1e9}
         native.gemm_set_variant(0)
         rows.append(res)
         print(json.dumps(res), flush=True)
