@@ -37,8 +37,9 @@ class B200Rates:
     tensor_flops: float = 1375.5e12        # sustained bf16, MEASURED_PEAKS.json
     # achieved fraction of the sustained peak for a round's mixed compute (verify MoE + draft re-prefill,
     # the two streams concurrent, power-capped): 0.68 measured with the persistent GEMMs
-    # (profiles/planner_sweep_r1.md, bs 440 / 48 cached: 3.3 PFLOP in 3.5 s); 0.65 keeps a margin
-    tensor_efficiency: float = 0.65
+    # (profiles/planner_sweep_r1.md, bs 440 / 48 cached: 3.3 PFLOP in 3.5 s), 0.69 after the split-K
+    # decode steps and the RoPE rewrite (bs 472 / 112 cached: 2.92 PFLOP in 3.1 s)
+    tensor_efficiency: float = 0.68
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
     # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
     # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin

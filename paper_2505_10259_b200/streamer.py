@@ -262,7 +262,7 @@ class LayerStreamer:
         self.ring = None
         if self.coded:
             for u in host.values():
-                if u.raw_bytes != layer_bytes:  # noqa: SIM102
+                if u.raw_bytes != layer_bytes:
                     raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
             self.frames = {li: u.frame_range(rank, world) for li, u in host.items()}
             self.ring_slot_bytes = (max(u.max_frame_bytes() for u in host.values()) + 255) // 256 * 256
