@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo = functional check of the N>1 path with ranks sharing GPUs (collectives staged "
                          "through host memory; not a performance configuration)")
+    ap.add_argument("--disk-gb", type=float, default=0.0,
+                    help="disk tier budget (§8 f4): streamed units beyond the host budget go to a file")
+    ap.add_argument("--disk-path", default="", help="file of the disk tier (default: a temporary file)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
@@ -256,9 +259,10 @@ def main():
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
                         draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
-                        world=world, allow_shards=not args.no_shards)
+                        world=world, allow_shards=not args.no_shards, disk_budget=int(args.disk_gb * 1e9))
     log(f"plan: bs {plan.bs_decoding} draft {plan.draft_kv}/{plan.draft_cached} pinned {len(plan.pinned_layers)} "
-        f"streamed {len(plan.stream_layers)} sharded {len(plan.shard_layers)} link {link / 1e9:.1f} GB/s")
+        f"streamed {len(plan.stream_layers)} (disk {len(plan.disk_layers)}) sharded {len(plan.shard_layers)} "
+        f"link {link / 1e9:.1f} GB/s")
     t_setup = time.perf_counter()
     layer_bytes = ffn_offsets(tgt)[2]
     if world > 1:
@@ -277,7 +281,7 @@ def main():
         store = HostStore()
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
                            seed=1, trace=bool(args.trace_out), host_store=store, stream_attn=plan.stream_attn,
-                           codec=args.codec)
+                           codec=args.codec, disk_layers=set(plan.disk_layers), disk_path=args.disk_path or None)
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
@@ -474,7 +478,7 @@ def main():
                    "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
-                   "hbm_sharded_layers": len(plan.shard_layers),
+                   "hbm_sharded_layers": len(plan.shard_layers), "disk_layers": len(plan.disk_layers),
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
                    "streamed_bytes_per_round": int(streamed / steps * world),

@@ -7,6 +7,9 @@ memory, creates the two-or-more-slot HBM window and returns an ``Engine``.
 """
 from __future__ import annotations
 
+import tempfile
+import weakref
+
 import torch
 
 from . import codec as C
@@ -14,7 +17,7 @@ from . import weights as W
 from .config import ModelArch
 from .engine import Engine
 from .models import DraftModel, TargetModel
-from .streamer import HostStore, LayerStreamer, SharedHostStore
+from .streamer import DiskRef, DiskTier, HostStore, LayerStreamer, SharedHostStore
 
 
 def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: dict | None = None,
@@ -22,7 +25,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  seed: int = 0, trace: bool = True, page_size: int = 16, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
                  shared_store: SharedHostStore | None = None, stream_attn: bool = False,
-                 codec: str = "none", shard_layers=None) -> Engine:
+                 codec: str = "none", shard_layers=None, disk_layers=None, disk_path: str | None = None) -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
@@ -32,7 +35,9 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     ``codec="xc4"`` keeps the streamed units XC4-encoded in host DRAM (K9:
     0.70–0.75 of the bytes cross the link, decoded bit-exactly on the GPU).
     ``shard_layers`` (world > 1): layers kept 1/N per GPU in
-    HBM and rebuilt each pass by an NVLink all-gather instead of the host link."""
+    HBM and rebuilt each pass by an NVLink all-gather instead of the host link.
+    ``disk_layers`` (§8 f4): streamed layers kept in a file at ``disk_path``
+    (default: a temporary file) and staged through pinned DRAM each pass."""
     if codec not in ("none", "xc4"):
         raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
@@ -43,6 +48,17 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     if shard_layers and world < 2:
         raise ValueError("shard_layers needs world > 1")
     stream_layers -= shard_layers
+    disk_layers = set(disk_layers or ()) & stream_layers
+    disk = None
+    if disk_layers:
+        if world > 1:
+            raise ValueError("the disk tier is single-GPU (the N-GPU host store is shared DRAM)")
+        if target_weights is not None:
+            raise ValueError("disk_layers is supported for synthetic weights")
+        if disk_path is None:
+            with tempfile.NamedTemporaryFile(prefix="specoffload_disk_", suffix=".bin", delete=False) as f:
+                disk_path = f.name
+        disk = DiskTier(disk_path)
     enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
     if target_weights is not None:
         tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc)
@@ -53,7 +69,8 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     else:
         store = host_store or HostStore()
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc,
-                         stream_attn=stream_attn, encoder=enc, shard_layers=shard_layers, shard=(rank, world))
+                         stream_attn=stream_attn, encoder=enc, shard_layers=shard_layers, shard=(rank, world),
+                         disk=disk, disk_layers=disk_layers)
     if enc is not None:
         enc.release()
         torch.cuda.empty_cache()  # hand the encoder's staging back before KV / workspaces are sized
@@ -63,10 +80,12 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
         dw = W.synthetic(draft_arch, dev, seed=seed + 1)
     _, ffn_bytes = W.unit_layout(target_arch, stream_attn)  # bytes of one streamed layer unit
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
-    host = {li: t if isinstance(t, C.XC4Unit) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
+    host = {li: t if isinstance(t, (C.XC4Unit, DiskRef)) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
                              chunk_bytes=chunk_bytes, rank=rank, world=world, group=group,
-                             shards=tw.shard_ffn) if (host or tw.shard_ffn) else None
+                             shards=tw.shard_ffn, disk=disk) if (host or tw.shard_ffn) else None
+    if disk is not None:
+        weakref.finalize(streamer, disk.close)
     target = TargetModel(tw, dev, streamer)
     draft = DraftModel(dw, dev)
     return Engine(target, draft, device=dev, page_size=page_size, trace=trace)

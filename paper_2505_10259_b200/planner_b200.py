@@ -44,6 +44,7 @@ class B200Rates:
     # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
     # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin
     nvlink_bytes_per_s: float = 650e9
+    disk_bytes_per_s: float = 12e9         # NVMe Gen5 sequential read (disk tier, §8 f4); no drive on the test box
 
 
 @dataclasses.dataclass(frozen=True)
@@ -69,12 +70,15 @@ class OffloadPlan:
     shard_layers: tuple[int, ...] = ()  # f3 (world > 1): 1/N per GPU in HBM, NVLink all-gather each pass
     world: int = 1
     t_nvlink_s: float = 0.0
+    disk_layers: tuple[int, ...] = ()   # f4: streamed layers kept on disk (subset of stream_layers)
+    t_disk_s: float = 0.0
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
         d["stream_layers"] = len(self.stream_layers)
         d["pinned_layers"] = len(self.pinned_layers)
         d["shard_layers"] = len(self.shard_layers)
+        d["disk_layers"] = len(self.disk_layers)
         return d
 
 
@@ -131,7 +135,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,
-                 world: int = 1, allow_shards: bool = True) -> OffloadPlan:
+                 world: int = 1, allow_shards: bool = True, disk_budget: int = 0) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
@@ -145,7 +149,11 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     link plus an NVLink all-gather; with ``allow_shards`` (§8 f3) layers may
     instead live 1/N per GPU in HBM and cross only NVLink — the aggregate HBM
     of N GPUs holds what one GPU's cannot.  Per layer and pass each rank
-    receives (N−1)/N of the layer over NVLink either way."""
+    receives (N−1)/N of the layer over NVLink either way.
+
+    ``disk_budget`` > 0 (§8 f4, placement.py:241-243): streamed units beyond
+    host DRAM (less two pinned staging units) live on disk and are read once
+    per pass, so the pass also costs disk bytes / disk_bytes_per_s."""
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     best = None
@@ -186,10 +194,16 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                         break
                     pinned = min(L - n_sh, int(room // layer_bytes), cap)
                     streamed = L - pinned - n_sh
+                    n_disk = 0
                     if streamed * host_unit > host_budget:
-                        continue
+                        if disk_budget <= 0 or world > 1:
+                            continue
+                        n_host = max(0, (host_budget - 2 * host_unit) // host_unit)  # 2 staging units
+                        n_disk = streamed - n_host
+                        if n_disk * host_unit > disk_budget:
+                            continue
                     S = streamed * host_unit // world         # this rank's link bytes per pass
-                    t_stream = S / rates.h2d_bytes_per_s
+                    t_stream = max(S / rates.h2d_bytes_per_s, n_disk * host_unit / rates.disk_bytes_per_s)
                     t_nvl = ((streamed + n_sh) * layer_bytes * (world - 1) / world / rates.nvlink_bytes_per_s
                              if world > 1 else 0.0)
                     t_comp = t_base + (streamed * layer_bytes / world * 1.75 / rates.hbm_bytes_per_s
@@ -198,11 +212,11 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                     tps = bs * e_tok / t_round
                     if best is None or tps > best[0] * 1.001:
                         best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
-                                stream_attn, fixed, layer_bytes, kc, n_sh, t_nvl, host_unit)
+                                stream_attn, fixed, layer_bytes, kc, n_sh, t_nvl, host_unit, n_disk)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
     (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes, kc,
-     n_sh, t_nvl, host_unit) = best
+     n_sh, t_nvl, host_unit, n_disk) = best
     # pin the first layers (ascending order, placement.py:220-231); among the
     # rest, host-streamed layers are spread evenly between the sharded ones so
     # the PCIe link keeps a layer in flight while NVLink gathers the others
@@ -211,11 +225,14 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     host_pos = {int((i + 0.5) * len(rest) / streamed) for i in range(streamed)} if streamed else set()
     stream_l = tuple(li for j, li in enumerate(rest) if j in host_pos)
     shard_l = tuple(li for j, li in enumerate(rest) if j not in host_pos)
+    disk_pos = {int((i + 0.5) * streamed / n_disk) for i in range(n_disk)} if n_disk else set()
+    disk_l = tuple(li for j, li in enumerate(stream_l) if j in disk_pos)  # spread among the DRAM-streamed ones
     return OffloadPlan(bs, n_cand, mode, bs_draft, stream_l, pinned_l, n_slots if rest else 0,
                        {"fixed": fixed, "kv": kv, "workspace": ws, "pinned_layers": pinned * layer_bytes,
                         "shards": int(n_sh * layer_bytes / world)},
                        streamed * host_unit, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
-                       kc if mode == "mixed" else 0, shard_l, world, t_nvl)
+                       kc if mode == "mixed" else 0, shard_l, world, t_nvl, disk_l,
+                       n_disk * host_unit / rates.disk_bytes_per_s)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

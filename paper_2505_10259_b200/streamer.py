@@ -15,6 +15,7 @@ attention runs while its FFN bytes are still in flight.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import mmap
 import os
 import threading
@@ -200,6 +201,115 @@ def gather_layer(slot: torch.Tensor, rank: int, world: int, group=None) -> None:
         _gloo_gather(slot, slot[lo:hi], group)
 
 
+class DiskRef:
+    """A streamed layer whose unit lives in the DiskTier's file; ``meta`` is
+    its XC4Unit (header and frame table, no data) or None for a raw unit."""
+
+    __slots__ = ("layer", "nbytes", "meta")
+
+    def __init__(self, layer: int, nbytes: int, meta):
+        self.layer, self.nbytes, self.meta = layer, nbytes, meta
+
+
+class DiskTier:
+    """the DISK tier below pinned host DRAM.
+
+    Reference: groups that fit neither the GPU nor the CPU go to disk
+    (placement.py:241-243) and each is staged DISK → CPU one layer ahead of
+    its use (prefetch_schedule, placement.py:275-282; IO_DISK events,
+    simulator.py:200-207).  Here the units (raw or XC4-encoded) are appended
+    to one file; a reader thread streams them, in pass order, into two
+    page-locked staging buffers with ``preadv`` (the GIL is released), so the
+    disk read of use j+1 overlaps the host→GPU copy of use j, and a buffer is
+    refilled only after the copy engine has finished with it (a CUDA event
+    recorded behind its copies)."""
+
+    ALIGN = 1 << 21
+
+    def __init__(self, path: str):
+        self.path = path
+        self.fd = os.open(path, os.O_RDWR | os.O_CREAT | os.O_TRUNC, 0o600)
+        self.entries: dict[int, tuple[int, int]] = {}   # layer → (file offset, bytes)
+        self.size = 0
+        self.bytes_read = 0
+        self._thread = None
+
+    def write(self, layer: int, data: torch.Tensor, meta=None) -> DiskRef:
+        """Append a unit's bytes (any device) to the file."""
+        buf = data.reshape(-1).view(torch.uint8)
+        if buf.is_cuda:
+            buf = buf.cpu()
+        off = self.size
+        mv = memoryview(buf.numpy())
+        done = 0
+        while done < len(mv):
+            done += os.pwrite(self.fd, mv[done:], off + done)
+        self.entries[layer] = (off, buf.numel())
+        self.size = (off + buf.numel() + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        return DiskRef(layer, buf.numel(), meta)
+
+    # ---- staging pipeline (started by the streamer) ----
+    def start(self, order: list[int]) -> None:
+        self.order = list(order)
+        cap = max(self.entries[li][1] for li in self.order)
+        self.bufs = [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.copy_done = [native.Event(), native.Event()]  # recorded behind the copies that read each buffer
+        self.cv = threading.Condition()
+        self.filled = 0     # uses staged so far
+        self.released = 0   # uses whose copies are enqueued (their buffer's event is recorded)
+        self.stop = False
+        self._thread = threading.Thread(target=self._reader, name="disk-stage", daemon=True)
+        self._thread.start()
+
+    def _reader(self) -> None:
+        dk = 0
+        while True:
+            with self.cv:
+                # buffer dk % 2 last held use dk − 2: wait until its copies are enqueued
+                while not self.stop and self.released < dk - 1:
+                    self.cv.wait(0.1)
+                if self.stop:
+                    return
+            if dk >= 2:
+                self.copy_done[dk % 2].synchronize()  # the copy engine is done reading it
+            off, n = self.entries[self.order[dk % len(self.order)]]
+            mv = memoryview(self.bufs[dk % 2].numpy())[:n]
+            got = 0
+            while got < n:
+                got += os.preadv(self.fd, [mv[got:]], off + got)
+            with self.cv:
+                self.filled = dk + 1
+                self.bytes_read += n
+                self.cv.notify_all()
+            dk += 1
+
+    def acquire(self, dk: int, ref: DiskRef):
+        """Host view of use ``dk`` (waits for the reader): a uint8 tensor, or an
+        XC4Unit over the staged bytes."""
+        with self.cv:
+            while self.filled <= dk:
+                self.cv.wait()
+        buf = self.bufs[dk % 2][: ref.nbytes]
+        return buf if ref.meta is None else dataclasses.replace(ref.meta, data=buf)
+
+    def release(self, dk: int, stream) -> None:
+        """The copies reading use ``dk``'s buffer are enqueued on ``stream``."""
+        self.copy_done[dk % 2].record(stream)
+        with self.cv:
+            self.released = dk + 1
+            self.cv.notify_all()
+
+    def close(self) -> None:
+        if self._thread is not None:
+            with self.cv:
+                self.stop = True
+                self.cv.notify_all()
+            self._thread.join(timeout=5)
+        os.close(self.fd)
+        if os.path.exists(self.path):
+            os.unlink(self.path)
+
+
 def gather_shards(slot: torch.Tensor, shard: torch.Tensor, group=None) -> None:
     """Rebuild a layer in ``slot`` from every rank's resident 1/N shard (f3).
     NCCL moves the (N−1)/N foreign bytes over NVLink; gloo (CPU tests) takes
@@ -226,8 +336,12 @@ class LayerStreamer:
 
     def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict,
                  n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False,
-                 rank: int = 0, world: int = 1, group=None, shards: dict[int, torch.Tensor] | None = None):
+                 rank: int = 0, world: int = 1, group=None, shards: dict[int, torch.Tensor] | None = None,
+                 disk: "DiskTier | None" = None):
         self.layer_bytes = layer_bytes
+        # f4: host values that are DiskRefs are staged from ``disk`` each use
+        self.disk = disk
+        self.disk_uses = 0
         # layers sharded across the N GPUs' HBM: rank r keeps
         # bytes slice_bounds(r) of the layer resident, and every pass rebuilds
         # the layer in a window slot with an NVLink all-gather (no host link)
@@ -238,9 +352,11 @@ class LayerStreamer:
             raise ValueError("a layer is either host-streamed or HBM-sharded")
         # host values are raw pinned uint8 tensors, or XC4Unit (K9: encoded
         # frames cross the link and are decoded into the slot on the GPU)
-        self.coded = any(isinstance(v, XC4Unit) for v in host.values())
-        if self.coded and not all(isinstance(v, XC4Unit) for v in host.values()):
+        kinds = {isinstance(v.meta if isinstance(v, DiskRef) else v, XC4Unit) for v in host.values()}
+        self.coded = kinds == {True}
+        if len(kinds) > 1:
             raise ValueError("streamed layers must be all raw or all XC4-encoded")
+        metas = {li: (v.meta if isinstance(v, DiskRef) else v) for li, v in host.items()}
         self.resident = resident
         self.host = host
         self.streamed = [li for li in range(n_layer) if li in host or li in self.shards]
@@ -261,11 +377,11 @@ class LayerStreamer:
         self.free = [native.Event() for _ in range(self.n_slots)]
         self.ring = None
         if self.coded:
-            for u in host.values():
+            for u in metas.values():
                 if u.raw_bytes != layer_bytes:
                     raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
-            self.frames = {li: u.frame_range(rank, world) for li, u in host.items()}
-            self.ring_slot_bytes = (max(u.max_frame_bytes() for u in host.values()) + 255) // 256 * 256
+            self.frames = {li: u.frame_range(rank, world) for li, u in metas.items()}
+            self.ring_slot_bytes = (max(u.max_frame_bytes() for u in metas.values()) + 255) // 256 * 256
             self.ring = torch.empty(self.RING_SLOTS * self.ring_slot_bytes, dtype=torch.uint8, device=self.device)
             self.ring_events = [native.Event() for _ in range(2 * self.RING_SLOTS)]
             self.ring_cursor = Cursor(0)
@@ -278,6 +394,8 @@ class LayerStreamer:
         self.nvlink_bytes_issued = 0  # bytes this rank receives in the all-gathers
         self.trace = trace
         self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
+        if disk is not None:
+            disk.start([li for li in self.streamed if isinstance(host.get(li), DiskRef)])
 
     @property
     def window_bytes(self) -> int:
@@ -301,6 +419,11 @@ class LayerStreamer:
         if k >= self.n_slots and not self.coded:  # coded: the decoder waits instead, the link runs ahead
             self.free[slot].wait(self.copy_stream)
         src = self.host[layer]
+        dk = None
+        if isinstance(src, DiskRef):  # f4: the reader thread staged it in pinned memory
+            dk = self.disk_uses
+            self.disk_uses += 1
+            src = self.disk.acquire(dk, src)
         start = None
         if self.trace:
             start = native.Event(timing=True).record(self.copy_stream)
@@ -311,6 +434,8 @@ class LayerStreamer:
             native.xc4_stream(self.slots[slot].data_ptr(), unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
                               self.ring_slot_bytes, self.ring_events, self.ring_cursor, self.copy_stream,
                               self.decode_stream, self.free[slot] if k >= self.n_slots else None, done)
+            if dk is not None:
+                self.disk.release(dk, self.copy_stream)
             if self.world > 1:
                 self.copied[slot].wait(self.comm_stream)
                 with torch.cuda.stream(self.comm_stream):
@@ -325,9 +450,13 @@ class LayerStreamer:
         if self.world == 1:
             native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
                                 self.copy_stream, self.loaded[slot])
+            if dk is not None:
+                self.disk.release(dk, self.copy_stream)
         else:
             native.stream_layer(self.slots[slot].data_ptr() + self.lo, src.data_ptr() + self.lo, self.hi - self.lo,
                                 self.chunk, self.copy_stream, self.copied[slot])
+            if dk is not None:
+                self.disk.release(dk, self.copy_stream)
             self.copied[slot].wait(self.comm_stream)
             with torch.cuda.stream(self.comm_stream):
                 gather_layer(self.slots[slot], self.rank, self.world, self.group)

@@ -137,7 +137,8 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
               host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False,
-              encoder=None, shard_layers: set[int] = frozenset(), shard: tuple[int, int] = (0, 1)) -> ModelWeights:
+              encoder=None, shard_layers: set[int] = frozenset(), shard: tuple[int, int] = (0, 1),
+              disk=None, disk_layers: set[int] = frozenset()) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
@@ -148,7 +149,9 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
     units are XC4-encoded on the GPU first and the host keeps the encoding
     (the sink then receives the encoded device bytes).  ``shard_layers`` (f3,
     N > 1): this rank keeps only its ``slice_bounds`` share of the layer unit in
-    HBM; the streamer all-gathers the shards every pass.
+    HBM; the streamer all-gathers the shards every pass.  ``disk_layers``
+    (with ``disk``, a streamer.DiskTier; §8 f4): streamed units written to
+    the disk tier's file instead of pinned DRAM.
     """
     from .streamer import slice_bounds
     dev = torch.device(device)
@@ -173,6 +176,12 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
         if sharded:
             lo, hi = slice_bounds(unit.numel() * 2, *shard)
             shards[li] = unit.view(torch.uint8)[lo:hi].clone()
+        elif streamed and li in disk_layers:
+            if encoder is not None:
+                enc = encoder.encode(unit)[0]
+                host[li] = disk.write(li, enc, dataclasses.replace(codec.XC4Unit.parse(enc), data=None))
+            else:
+                host[li] = disk.write(li, unit)
         elif streamed and encoder is not None:
             if host_sink is not None:
                 host[li] = host_sink(li, encoder.encode(unit)[0])

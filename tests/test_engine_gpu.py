@@ -259,3 +259,21 @@ def test_slot_refill_edges(pair):
     refill = eng.generate(prompts, 9, pol, refill=True)
     assert refill == classic
     assert [t[0] for t in refill] == [t[0] for t in one]
+
+
+@pytest.mark.parametrize("codec", ["none", "xc4"])
+def test_disk_tier_layers_match(pair, codec):
+    """streamed layers kept in a file, staged DISK → pinned
+    DRAM by the reader thread one use ahead, then copied (and decoded) as
+    usual — the same tokens as the DRAM-resident streamer."""
+    tw, dw = pair
+    prompts = tiny.prompts(8, seed=31)
+    pol = Policy(8, 4, 4, 4)
+    ref = build_engine(TINY_TARGET, TINY_DRAFT, None, None, stream_layers={0, 1, 2, 3}, seed=5,
+                       codec=codec).generate(prompts, 12, pol)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, None, None, stream_layers={0, 1, 2, 3}, seed=5, codec=codec,
+                       disk_layers={1, 3})
+    st = eng.target.streamer
+    assert st.disk is not None and set(st.disk.entries) == {1, 3}
+    assert eng.generate(prompts, 12, pol) == ref
+    assert st.disk.bytes_read > 0 and st.disk_uses >= 2

@@ -121,3 +121,18 @@ def test_multi_gpu_plan_uses_hbm_shards():
                       stream_ratio=0.7, ring_bytes=800 << 20, world=8, allow_shards=False,
                       bs_candidates=list(range(64, 1025, 32)))
     assert not no.shard_layers and no.tokens_per_s < prev
+
+
+def test_disk_tier_spill():
+    """§8 f4 (placement.py:241-243): with too little host DRAM the planner
+    spills streamed units to disk instead of failing, and the pass pays the
+    disk read time; without a disk budget the same budgets are infeasible."""
+    kw = dict(stream_ratio=0.7, ring_bytes=800 << 20, bs_candidates=list(range(64, 1025, 32)))
+    with pytest.raises(InfeasiblePlan):
+        plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(60e9), 8, 0.8, 503, 45, RATES, **kw)
+    p = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(190e9), int(60e9), 8, 0.8, 503, 45, RATES,
+                     disk_budget=int(2e12), **kw)
+    assert p.disk_layers and set(p.disk_layers) <= set(p.stream_layers)
+    host_units = len(p.stream_layers) - len(p.disk_layers)
+    assert (host_units + 2) * p.host_bytes / len(p.stream_layers) <= 60e9 * 1.001
+    assert p.t_disk_s > 0 and p.t_round_s >= p.t_disk_s
