@@ -14,6 +14,7 @@ attention runs while its FFN bytes are still in flight.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes
 import dataclasses
 import mmap
@@ -225,6 +226,7 @@ class DiskTier:
     recorded behind its copies)."""
 
     ALIGN = 1 << 21
+    READERS = 8  # concurrent preadv streams per unit (NVMe queues / page-cache copies in parallel)
 
     def __init__(self, path: str):
         self.path = path
@@ -258,6 +260,7 @@ class DiskTier:
         self.filled = 0     # uses staged so far
         self.released = 0   # uses whose copies are enqueued (their buffer's event is recorded)
         self.stop = False
+        self._pool = concurrent.futures.ThreadPoolExecutor(self.READERS, thread_name_prefix="disk-read")
         self._thread = threading.Thread(target=self._reader, name="disk-stage", daemon=True)
         self._thread.start()
 
@@ -274,14 +277,17 @@ class DiskTier:
                 self.copy_done[dk % 2].synchronize()  # the copy engine is done reading it
             off, n = self.entries[self.order[dk % len(self.order)]]
             mv = memoryview(self.bufs[dk % 2].numpy())[:n]
-            got = 0
-            while got < n:
-                got += os.preadv(self.fd, [mv[got:]], off + got)
+            piece = -(-n // self.READERS + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+            list(self._pool.map(lambda lo: self._read(mv, off, lo, min(n, lo + piece)), range(0, n, piece)))
             with self.cv:
                 self.filled = dk + 1
                 self.bytes_read += n
                 self.cv.notify_all()
             dk += 1
+
+    def _read(self, mv, off: int, lo: int, hi: int) -> None:
+        while lo < hi:
+            lo += os.preadv(self.fd, [mv[lo:hi]], off + lo)
 
     def acquire(self, dk: int, ref: DiskRef):
         """Host view of use ``dk`` (waits for the reader): a uint8 tensor, or an
@@ -305,6 +311,7 @@ class DiskTier:
                 self.stop = True
                 self.cv.notify_all()
             self._thread.join(timeout=5)
+            self._pool.shutdown(wait=True)
         os.close(self.fd)
         if os.path.exists(self.path):
             os.unlink(self.path)
