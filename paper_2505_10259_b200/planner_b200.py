@@ -38,8 +38,11 @@ class B200Rates:
     # achieved fraction of the sustained peak for a round's mixed compute (verify MoE + draft re-prefill,
     # the two streams concurrent, power-capped): 0.68 measured with the persistent GEMMs
     # (profiles/planner_sweep_r1.md, bs 440 / 48 cached: 3.3 PFLOP in 3.5 s), 0.69 after the split-K
-    # decode steps and the RoPE rewrite (bs 472 / 112 cached: 2.92 PFLOP in 3.1 s)
-    tensor_efficiency: float = 0.68
+    # decode steps and the RoPE rewrite (bs 472 / 112 cached: 2.92 PFLOP in 3.1 s).  Planned at 0.65:
+    # with 0.68 the planner chose bs 480 / 90 cached, whose draft stream (3.50-3.63 s at a 1.22 GHz
+    # power-capped clock) overran the 3.46 s link pass: 589.8 tok/s instead of 598 — a compute
+    # overrun costs linearly, a margin only a few sequences
+    tensor_efficiency: float = 0.65
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
     # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
     # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin
