@@ -95,15 +95,6 @@ def resident_bytes(arch: ModelArch, include_ffn: bool) -> int:
     return b
 
 
-def kv_bytes(target: ModelArch, draft: ModelArch, n_seq: int, max_len: int, page_size: int = 16,
-             draft_seqs: int | None = None) -> int:
-    """Target KV for every sequence; draft KV for ``draft_seqs`` (all of them when
-    cached, one bs_draft chunk when the draft re-prefills: costmodel.py:132-137)."""
-    ds = n_seq if draft_seqs is None else draft_seqs
-    return (PagedKVCache.bytes_needed(target, n_seq, max_len, page_size)
-            + PagedKVCache.bytes_needed(draft, ds, max_len, page_size))
-
-
 def _act_bytes(a: ModelArch, T: int, moe: bool) -> int:
     rows = 2 * T if moe else T
     return (T * (6 * a.hidden + a.qkv_rows + 2 * a.n_head * a.head_dim) + rows * (2 * a.hidden + a.inter)) * 2
