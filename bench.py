@@ -236,8 +236,10 @@ def main():
         dist.all_reduce(agree, op=dist.ReduceOp.MIN)
         link, hbm, host = float(agree[0]), int(agree[1]), int(agree[2])
     steps, warm = args.steps, args.warmup
-    verifies_per_batch = (warm + steps) // 2 + 2
-    max_new = verifies_per_batch * (args.n_cand + 1) + 1
+    # rounds alternate batches: batch 0 is verified ceil(R/2) times in R rounds, each committing
+    # ≤ n_cand+1 tokens, so no sequence can be clamped by `remaining` inside the run
+    verifies_per_batch = -(-(warm + steps) // 2)
+    max_new = verifies_per_batch * (args.n_cand + 1)
     from paper_2505_10259_b200.planner_b200 import B200Rates
 
     rates = B200Rates(h2d_bytes_per_s=link, hbm_bytes_per_s=peaks["hbm_gbs"] * 1e9)
