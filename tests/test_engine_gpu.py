@@ -277,3 +277,21 @@ def test_disk_tier_layers_match(pair, codec):
     assert st.disk is not None and set(st.disk.entries) == {1, 3}
     assert eng.generate(prompts, 12, pol) == ref
     assert st.disk.bytes_read > 0 and st.disk_uses >= 2
+
+
+def test_slot_refill_sampling_and_forced_modes(pair):
+    """Slot refill under sampling verification (Leviathan accept/resample with the
+    draft's probabilities of fresh and cached slots) and under forced acceptance:
+    every prompt gets exactly max_new tokens, all in the vocabulary, and the
+    sampled run is reproducible from its seed."""
+    tw, dw = pair
+    prompts = tiny.prompts(19, seed=37)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={2, 3})
+    pol = Policy(8, 4, 2, 3)
+    a = eng.generate(prompts, 11, pol, mode="sample", seed=9, temperature=0.9, draft_kv="mixed", draft_cached=2)
+    b = eng.generate(prompts, 11, pol, mode="sample", seed=9, temperature=0.9, draft_kv="mixed", draft_cached=2)
+    assert eng.last_session.refill
+    assert a == b
+    assert all(len(o) == 11 for o in a) and all(0 <= t < TINY_TARGET.vocab for o in a for t in o)
+    f = eng.generate(prompts, 11, pol, forced_p=0.8)
+    assert all(len(o) == 11 for o in f)
