@@ -70,8 +70,7 @@ def parse():
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
     ap.add_argument("--e2e-seqs", type=int, default=0,
-                    help="prompts of the generate() leg (0 = twice the decode plan's 2·bs_decoding slots, "
-                         "run with slot refill)")
+                    help="prompts of the generate() leg (0 = three times its slot pool, run with slot refill)")
     ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
@@ -429,24 +428,31 @@ def main():
     if not args.no_e2e_generate:
         del s
         torch.cuda.empty_cache()
-        S_e = args.e2e_seqs or 4 * bs
+        # Its own slot pool: with prefill inside every round the generate workload is
+        # tensor-bound, not link-bound, so the draft keeps a KV row per slot (no
+        # per-round context re-prefill) and HBM left after the engine's weights
+        # and window sets the slot count (headroom for the prefill activations).
+        from paper_2505_10259_b200.kvcache import PagedKVCache
+
+        free_now, _ = torch.cuda.mem_get_info(device)
+        free_now = free_now // share
+        g_len = args.ctx + args.e2e_new + args.n_cand + 2
+        per_slot = PagedKVCache.bytes_needed(tgt, 1, g_len) + PagedKVCache.bytes_needed(drf, 1, g_len)
+        bs_e = max(8, int((free_now - 10e9) // per_slot) // 2 // 8 * 8)
+        S_e = args.e2e_seqs or 6 * bs_e
         rng = np.random.default_rng(1234 + rank)
         prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
-        # the decode plan's two batches are the slot pool; prompts beyond them are
-        # admitted as slots free up (slot refill, prefill inside the verify passes)
-        pol = Policy(bs_prefill=min(S_e, 2 * bs), bs_decoding=min(bs, (S_e + 1) // 2),
-                     bs_draft=min(64, (S_e + 1) // 2) if plan.draft_kv != "cached" else min(bs, (S_e + 1) // 2),
-                     n_cand=args.n_cand)
+        pol = Policy(bs_prefill=min(S_e, 2 * bs_e), bs_decoding=min(bs_e, (S_e + 1) // 2),
+                     bs_draft=min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
         torch.cuda.synchronize(device)
         g0 = time.perf_counter()
-        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=plan.draft_kv,
-                            draft_cached=min(plan.draft_cached, pol.bs_decoding) if plan.draft_kv == "mixed" else None)
+        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv="cached")
         g_wall = time.perf_counter() - g0
         assert all(len(t) == args.e2e_new for t in toks)
         gs = eng.last_session
         gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
                "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
-               "policy": list(pol.as_tuple()), "draft_kv": plan.draft_kv,
+               "policy": list(pol.as_tuple()), "draft_kv": "cached",
                "refill": gs.refill, "slots": gs.n_seq,
                "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
                        "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "

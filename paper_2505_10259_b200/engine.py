@@ -184,6 +184,8 @@ class DecodeSession:
 
 
 class Engine:
+    FRESH_CHUNK = 64  # sequences per draft context prefill of freshly admitted slots
+
     def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 16,
                  trace: bool = True):
         self.target = target
@@ -400,8 +402,9 @@ class Engine:
             c_hi = min(cached.size, c_lo + cstep)
             self._draft_chunk_cached(s, bi, c_lo, order[c_lo:c_hi], u_all)
         base = cached.size
-        for c_lo in range(0, fresh_rows.size, s.bs_draft):
-            seqs = fresh_rows[c_lo:c_lo + s.bs_draft]
+        fstep = min(s.bs_draft, self.FRESH_CHUNK)  # context prefills: bounded activation workspace
+        for c_lo in range(0, fresh_rows.size, fstep):
+            seqs = fresh_rows[c_lo:c_lo + fstep]
             self._draft_chunk_reprefill(s, bi, base + c_lo, seqs, u_all, rows=s.drow[seqs], kv_dn=True)
         base += fresh_rows.size
         for c_lo in range(0, rp.size, s.bs_draft):
