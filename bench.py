@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--e2e-seqs", type=int, default=0,
                     help="prompts of the generate() leg (0 = three times its slot pool, run with slot refill)")
     ap.add_argument("--e2e-new", type=int, default=16, help="tokens per sequence (paper tables: 16)")
+    ap.add_argument("--e2e-admit", type=int, default=0, help="generate() leg: prompts admitted per round (0 = all free)")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--codec", choices=("xc4", "none"), default="xc4",
                     help="streamed units XC4-encoded in host DRAM (K9, lossless) or raw bf16")
@@ -183,6 +184,10 @@ def run_reference(args, rank: int) -> None:
 
 def main():
     args = parse()
+    if os.environ.get("SO_WATCHDOG_S"):  # debugging aid: dump every thread's stack periodically
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["SO_WATCHDOG_S"]), repeat=True)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -325,6 +330,7 @@ def main():
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
+    log("timed rounds done")
     clk = clocks.stop()
     dev_s = ev0.elapsed_time(ev1) * 1e-3
     committed = s.committed_decode - committed0
@@ -423,6 +429,7 @@ def main():
         except Exception as exc:
             codec_k = {"error": str(exc)}
 
+    log("kernel samples done")
     # ---- generate(): the paper's end-to-end tokens/s (prefill included) ----
     gen = None
     if not args.no_e2e_generate:
@@ -446,14 +453,27 @@ def main():
                      bs_draft=min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
         torch.cuda.synchronize(device)
         g0 = time.perf_counter()
-        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv="cached")
+        admit = args.e2e_admit or None
+        round0 = eng.round
+
+        def logged_round(sess, _r=round0):  # progress of the long generate leg on stderr
+            c = _r(sess)
+            if sess.rounds % 10 == 0 or sess.rounds <= 3:
+                log(f"generate: round {sess.rounds}, queue {len(sess.queue)}, active {int(sess.active.sum())}")
+            return c
+
+        log(f"generate: {S_e} prompts through {2 * pol.bs_decoding} slots")
+
+        eng.round = logged_round
+        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv="cached", max_admit=admit)
         g_wall = time.perf_counter() - g0
+        eng.round = round0
         assert all(len(t) == args.e2e_new for t in toks)
         gs = eng.last_session
         gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
                "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
                "policy": list(pol.as_tuple()), "draft_kv": "cached",
-               "refill": gs.refill, "slots": gs.n_seq,
+               "refill": gs.refill, "slots": gs.n_seq, "max_admit_per_round": admit,
                "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
                        "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "
                        "verify pass), so every round streams the layers once for prefill and decode alike; "

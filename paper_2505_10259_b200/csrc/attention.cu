@@ -102,8 +102,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// bounded wait: a protocol bug traps (a reported kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
+  uint32_t done = 0, spins = 0;
   const uint32_t a = smem_u32(bar);
   do {
     asm volatile(
@@ -113,6 +114,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+    if (++spins > (1u << 28)) __trap();
   } while (!done);
 }
 

@@ -104,7 +104,7 @@ class DecodeSession:
     def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
                  mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int,
                  draft_kv: str = "cached", draft_cached: int | None = None, prompts: list | None = None,
-                 max_new: int = 0):
+                 max_new: int = 0, max_admit: int | None = None):
         self.e = engine
         self.n_seq = n_seq
         self.n_cand = n_cand
@@ -155,6 +155,10 @@ class DecodeSession:
         self.max_new = max_new
         self.queue = list(range(len(prompts))) if self.refill else []
         self.queue.reverse()  # pop() from the end = admission in prompt order
+        # admissions per round: prefill is the heavy part of a refill round, so
+        # spreading it keeps rounds near the link pass instead of alternating
+        # prefill-bound and idle-tensor rounds (and keeps finishes staggered)
+        self.max_admit = max_admit
         # token history (position-indexed) for every draft that re-reads its context
         self.hist = (torch.zeros((n_seq, max_len), dtype=torch.int32, device=dev)
                      if (self.any_reprefill or self.refill) else None)
@@ -257,9 +261,9 @@ class Engine:
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
                     bs_draft: int | None = None, draft_kv: str = "cached",
                     draft_cached: int | None = None, prompts: list | None = None,
-                    max_new: int = 0) -> DecodeSession:
+                    max_new: int = 0, max_admit: int | None = None) -> DecodeSession:
         return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
-                             bs_draft or bs_decoding, draft_kv, draft_cached, prompts, max_new)
+                             bs_draft or bs_decoding, draft_kv, draft_cached, prompts, max_new, max_admit)
 
     def _bt(self, kv: PagedKVCache, rows, stream) -> torch.Tensor:
         """Block-table rows of an arbitrary slot list, staged to the device."""
@@ -656,6 +660,8 @@ class Engine:
         target prefill runs inside this round's verify."""
         b = s.batches[bi]
         free = [i for i in range(b.lo, b.hi) if s.slot_prompt[i] < 0]
+        if s.max_admit is not None:
+            free = free[:s.max_admit]
         take = []
         for i in free:
             if not s.queue:
@@ -750,7 +756,7 @@ class Engine:
     def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
                  mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None,
                  draft_kv: str = "cached", draft_cached: int | None = None,
-                 refill: bool | None = None) -> list[list[int]]:
+                 refill: bool | None = None, max_admit: int | None = None) -> list[list[int]]:
         """prompts (token id lists) → committed continuations, max_new_tokens each.
 
         With more prompts than the two batches hold (or ``refill=True``), the
@@ -768,7 +774,8 @@ class Engine:
             slots = min(S, 2 * policy.bs_decoding)
             s = self.new_session(slots, min(policy.bs_decoding, slots), max_len, policy.n_cand, mode, seed,
                                  temperature, forced_p, policy.bs_draft, draft_kv, draft_cached,
-                                 prompts=[np.asarray(p, np.int32) for p in prompts], max_new=max_new_tokens)
+                                 prompts=[np.asarray(p, np.int32) for p in prompts], max_new=max_new_tokens,
+                                 max_admit=max_admit)
             self.decode(s)
             self.last_session = s
             return [o[:max_new_tokens] for o in s.out]
