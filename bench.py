@@ -184,10 +184,11 @@ def run_reference(args, rank: int) -> None:
 
 def main():
     args = parse()
-    if os.environ.get("SO_WATCHDOG_S"):  # debugging aid: dump every thread's stack periodically
-        import faulthandler
+    # diagnostics for a stalled run: every thread's stack on stderr every SO_WATCHDOG_S
+    # seconds (default 600 s — past a normal run's whole duration)
+    import faulthandler
 
-        faulthandler.dump_traceback_later(float(os.environ["SO_WATCHDOG_S"]), repeat=True)
+    faulthandler.dump_traceback_later(float(os.environ.get("SO_WATCHDOG_S", "600")), repeat=True)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -396,17 +397,18 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+EncodeTiledFn lookup_encode() {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+      qr == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<EncodeTiledFn>(p);
+  return nullptr;
+}
+
+// thread-safe one-time lookup (the verify and draft streams are fed from two host threads)
 EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
+  static const EncodeTiledFn fn = lookup_encode();
   return fn;
 }
 
@@ -436,13 +438,19 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
   const size_t smem = (TMA ? 1024 : 0) + (size_t)kStages * 2 * Tile<DH, TMA>::kBytes + 2 * kStages * sizeof(uint64_t) +
                       (size_t)max_pages * sizeof(int32_t);
   auto kern = attn_paged_kernel<DH, TMA>;
-  static size_t attr_bytes = 0;  // raised when a longer block table needs more smem
-  if (smem > attr_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return (int)e;
-    attr_bytes = smem;
+  {
+    // raised when a longer block table needs more smem; the verify and the draft
+    // streams launch this kernel from two host threads, so check-and-raise is atomic
+    static std::mutex mu;
+    static size_t attr_bytes = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > attr_bytes) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return (int)e;
+      attr_bytes = smem;
+    }
   }
   CUtensorMap mk, mv;
   memset(&mk, 0, sizeof(mk));
