@@ -277,13 +277,17 @@ class DiskTier:
                 self.copy_done[dk % 2].synchronize()  # the copy engine is done reading it
             off, n = self.entries[self.order[dk % len(self.order)]]
             mv = memoryview(self.bufs[dk % 2].numpy())[:n]
-            piece = -(-n // self.READERS + self.ALIGN - 1) // self.ALIGN * self.ALIGN
-            list(self._pool.map(lambda lo: self._read(mv, off, lo, min(n, lo + piece)), range(0, n, piece)))
+            list(self._pool.map(lambda r: self._read(mv, off, *r), self.pieces(n)))
             with self.cv:
                 self.filled = dk + 1
                 self.bytes_read += n
                 self.cv.notify_all()
             dk += 1
+
+    def pieces(self, n: int) -> list[tuple[int, int]]:
+        """Byte ranges (2 MiB-aligned, ≤ READERS of them) covering an n-byte unit."""
+        piece = ((n + self.READERS - 1) // self.READERS + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        return [(lo, min(n, lo + piece)) for lo in range(0, n, piece)]
 
     def _read(self, mv, off: int, lo: int, hi: int) -> None:
         while lo < hi:
