@@ -714,15 +714,18 @@ class Engine:
                     err.append(exc)
 
             self._tev[0].record(self.drf_stream)
-            worker = threading.Thread(target=run_draft, name="draft-enqueue")
+            worker = threading.Thread(target=run_draft, name="draft-enqueue", daemon=True)
             worker.start()
-        self._tev[2].record(self.tgt_stream)
-        if verify:
-            self._cur = (rnd, bi)
-            self._verify(s, bi, rnd)
-        self._tev[3].record(self.tgt_stream)
+        try:
+            self._tev[2].record(self.tgt_stream)
+            if verify:
+                self._cur = (rnd, bi)
+                self._verify(s, bi, rnd)
+            self._tev[3].record(self.tgt_stream)
+        finally:
+            if worker is not None:  # never leave the draft enqueue running past an error
+                worker.join()
         if worker is not None:
-            worker.join()
             if err:
                 raise err[0]
             self._tev[1].record(self.drf_stream)
