@@ -73,7 +73,8 @@ _SIGNATURES = {
 }
 
 _PLUMBING = {"so_event_create", "so_event_destroy", "so_event_record", "so_stream_wait_event", "so_event_synchronize",
-             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device"}
+             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device", "so_gemm_set_variant",
+             "so_attn_set_variant"}
 
 
 def library_path() -> str:
@@ -116,12 +117,12 @@ def reset_launch_counter() -> None:
 
 def gemm_set_variant(variant: int) -> None:
     """0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair (cta_group::2) tiles wherever legal."""
-    _check(lib().so_gemm_set_variant(variant), "so_set_device")
+    _check(lib().so_gemm_set_variant(variant), "so_gemm_set_variant")
 
 
 def attn_set_variant(variant: int) -> None:
     """0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging."""
-    _check(lib().so_attn_set_variant(variant), "so_set_device")
+    _check(lib().so_attn_set_variant(variant), "so_attn_set_variant")
 
 
 def set_device(index: int) -> None:

@@ -13,7 +13,6 @@ from __future__ import annotations
 import dataclasses
 import json
 
-import torch
 
 RESOURCES = ("GPU_TARGET", "GPU_DRAFT", "CPU", "IO_C2G", "IO_G2C", "IO_DISK")
 LABELS = ("attn_gpu", "ffn_load", "ffn_gpu", "draft_prefill", "draft_decode", "accept", "kv_offload",

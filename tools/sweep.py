@@ -45,7 +45,6 @@ def main():
     from paper_2505_10259_b200.api import build_engine
     from paper_2505_10259_b200.planner_b200 import B200Rates, plan_offload
     from paper_2505_10259_b200.streamer import HostStore
-    from paper_2505_10259_b200.weights import unit_layout
 
     dev = torch.device("cuda", 0)
     link = h2d_peak(torch, dev)
