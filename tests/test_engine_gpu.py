@@ -295,3 +295,29 @@ def test_slot_refill_sampling_and_forced_modes(pair):
     assert all(len(o) == 11 for o in a) and all(0 <= t < TINY_TARGET.vocab for o in a for t in o)
     f = eng.generate(prompts, 11, pol, forced_p=0.8)
     assert all(len(o) == 11 for o in f)
+
+
+@pytest.mark.parametrize("codec", ["none", "xc4"])
+def test_trace_causality_ffn_after_its_load(pair, codec):
+    """The reference's trace invariant (pkg/tests/_checks.py:21-35,
+    assert_causality) on the measured trace: the k-th ffn_gpu interval of a
+    streamed layer starts after the k-th ffn_load of that layer ended (copy,
+    and with XC4 the decode, finished before the expert GEMMs read the slot)."""
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2}, codec=codec)
+    res = eng.run_decoding(Policy(16, 8, 8, 4), Workload(16, 32, 12, 0.8), acceptance=Forced(0.8))
+    loads, ffns = collections.defaultdict(list), collections.defaultdict(list)
+    for ev in res.trace:
+        if ev.label == "ffn_load":
+            loads[ev.layer].append(ev)
+        elif ev.label == "ffn_gpu" and ev.layer in (1, 2):
+            ffns[ev.layer].append(ev)
+    checked = 0
+    for layer in (1, 2):
+        ls = sorted(loads[layer], key=lambda e: e.start)
+        fs = sorted(ffns[layer], key=lambda e: e.start)
+        assert fs and len(ls) >= len(fs)
+        for f, load in zip(fs, ls):
+            assert f.start >= load.end - 1e-5, (layer, f, load)
+            checked += 1
+    assert checked >= 4
