@@ -443,10 +443,12 @@ def main():
         from paper_2505_10259_b200.kvcache import PagedKVCache
 
         free_now, _ = torch.cuda.mem_get_info(device)
-        free_now = free_now // share
+        # the HBM budget (configs[1]: 24 GB cap) bounds the pool, not just the device's free memory
+        free_now = min(free_now // share, hbm - torch.cuda.memory_reserved(device))
         g_len = args.ctx + args.e2e_new + args.n_cand + 2
         per_slot = PagedKVCache.bytes_needed(tgt, 1, g_len) + PagedKVCache.bytes_needed(drf, 1, g_len)
-        bs_e = max(8, int((free_now - 10e9) // per_slot) // 2 // 8 * 8)
+        headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
+        bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
         S_e = args.e2e_seqs or 6 * bs_e
         rng = np.random.default_rng(1234 + rank)
         prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
