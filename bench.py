@@ -266,7 +266,8 @@ def main():
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
                         draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
-                        world=world, allow_shards=not args.no_shards, disk_budget=int(args.disk_gb * 1e9))
+                        world=world, allow_shards=not args.no_shards, disk_budget=int(args.disk_gb * 1e9),
+                        kv_host_modes=(False, True) if world == 1 else (False,))
     log(f"plan: bs {plan.bs_decoding} draft {plan.draft_kv}/{plan.draft_cached} pinned {len(plan.pinned_layers)} "
         f"streamed {len(plan.stream_layers)} (disk {len(plan.disk_layers)}) sharded {len(plan.shard_layers)} "
         f"link {link / 1e9:.1f} GB/s")
@@ -292,7 +293,8 @@ def main():
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
-                        bs_draft=plan.bs_draft, draft_kv=plan.draft_kv, draft_cached=plan.draft_cached)
+                        bs_draft=plan.bs_draft, draft_kv=plan.draft_kv, draft_cached=plan.draft_cached,
+                        kv_host=plan.kv_host)
     eng.synthetic_context(s, args.ctx, max_new, seed=rank)
     eng.first_draft(s)
     setup_s = time.perf_counter() - t_setup
@@ -449,11 +451,14 @@ def main():
         per_slot = PagedKVCache.bytes_needed(tgt, 1, g_len) + PagedKVCache.bytes_needed(drf, 1, g_len)
         headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
         bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
+        e_kv_host, e_draft_kv, e_bs_draft = False, "cached", None
+        if plan.kv_host:  # tiny HBM budget: the decode plan's host-KV pool and re-prefill draft
+            bs_e, e_kv_host, e_draft_kv, e_bs_draft = plan.bs_decoding, True, plan.draft_kv, plan.bs_draft
         S_e = args.e2e_seqs or 6 * bs_e
         rng = np.random.default_rng(1234 + rank)
         prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
         pol = Policy(bs_prefill=min(S_e, 2 * bs_e), bs_decoding=min(bs_e, (S_e + 1) // 2),
-                     bs_draft=min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
+                     bs_draft=e_bs_draft or min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
         torch.cuda.synchronize(device)
         g0 = time.perf_counter()
         admit = args.e2e_admit or None
@@ -468,14 +473,15 @@ def main():
         log(f"generate: {S_e} prompts through {2 * pol.bs_decoding} slots")
 
         eng.round = logged_round
-        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv="cached", max_admit=admit)
+        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=e_draft_kv, max_admit=admit,
+                            kv_host=e_kv_host)
         g_wall = time.perf_counter() - g0
         eng.round = round0
         assert all(len(t) == args.e2e_new for t in toks)
         gs = eng.last_session
         gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
                "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
-               "policy": list(pol.as_tuple()), "draft_kv": "cached",
+               "policy": list(pol.as_tuple()), "draft_kv": e_draft_kv, "target_kv_host": e_kv_host,
                "refill": gs.refill, "slots": gs.n_seq, "max_admit_per_round": admit,
                "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
                        "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "
@@ -510,6 +516,7 @@ def main():
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "hbm_sharded_layers": len(plan.shard_layers), "disk_layers": len(plan.disk_layers),
+                   "target_kv": "host DRAM (one batch staged per layer)" if plan.kv_host else "HBM",
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
                    "streamed_bytes_per_round": int(streamed / steps * world),

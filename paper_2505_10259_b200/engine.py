@@ -32,7 +32,7 @@ import torch
 from . import native
 from .acceptance import forced_counts, input_uniforms
 from .domain import Policy
-from .kvcache import PagedKVCache
+from .kvcache import HostPagedKVCache, PagedKVCache
 from .models import DraftModel, ForwardBatch, TargetModel
 from .trace import SimResult, Tracer, busy
 
@@ -104,7 +104,7 @@ class DecodeSession:
     def __init__(self, engine: "Engine", n_seq: int, bs_decoding: int, max_len: int, n_cand: int,
                  mode: str, seed: int, temperature: float, forced_p: float | None, bs_draft: int,
                  draft_kv: str = "cached", draft_cached: int | None = None, prompts: list | None = None,
-                 max_new: int = 0, max_admit: int | None = None):
+                 max_new: int = 0, max_admit: int | None = None, kv_host: bool = False):
         self.e = engine
         self.n_seq = n_seq
         self.n_cand = n_cand
@@ -120,7 +120,11 @@ class DecodeSession:
         self.draft_kv = draft_kv
         self.batches = [_Batch(0, min(bs_decoding, n_seq)), _Batch(min(bs_decoding, n_seq), n_seq)]
         dev = engine.device
-        self.tkv = PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size)
+        # target KV in HBM, or (kv_host, for tiny HBM budgets) in pinned host DRAM
+        # with one batch's pages staged per layer (kvcache.HostPagedKVCache)
+        self.tkv = (HostPagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size,
+                                     window_seqs=max(b.n for b in self.batches))
+                    if kv_host else PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size))
         # Draft KV policy (planner choice):
         #   cached    one persistent draft KV row per sequence;
         #   reprefill the paper's draft (costmodel.py:53-57,
@@ -261,9 +265,9 @@ class Engine:
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
                     bs_draft: int | None = None, draft_kv: str = "cached",
                     draft_cached: int | None = None, prompts: list | None = None,
-                    max_new: int = 0, max_admit: int | None = None) -> DecodeSession:
+                    max_new: int = 0, max_admit: int | None = None, kv_host: bool = False) -> DecodeSession:
         return DecodeSession(self, n_seq, bs_decoding, max_len, n_cand, mode, seed, temperature, forced_p,
-                             bs_draft or bs_decoding, draft_kv, draft_cached, prompts, max_new, max_admit)
+                             bs_draft or bs_decoding, draft_kv, draft_cached, prompts, max_new, max_admit, kv_host)
 
     def _bt(self, kv: PagedKVCache, rows, stream) -> torch.Tensor:
         """Block-table rows of an arbitrary slot list, staged to the device."""
@@ -294,7 +298,12 @@ class Engine:
             cur.append(i)
             cur_tok += int(L)
         groups.append(cur)
-        models = [(self.target, s.tkv, self.tgt_stream, groups, np.arange(s.n_seq))]
+        if isinstance(s.tkv, HostPagedKVCache):  # one target pass per batch: the KV window holds one batch
+            models = [(self.target, s.tkv, self.tgt_stream,
+                       [[i for i in g if b.lo <= i < b.hi] for g in groups if any(b.lo <= i < b.hi for i in g)],
+                       np.arange(s.n_seq), b) for b in s.batches if b.n]
+        else:
+            models = [(self.target, s.tkv, self.tgt_stream, groups, np.arange(s.n_seq), None)]
         if s.any_reprefill:  # the re-prefilling draft only needs the prompt tokens
             seqs = np.concatenate([np.full(L, i) for i, L in enumerate(lens)])
             pos = np.concatenate([np.arange(L) for L in lens])
@@ -305,8 +314,12 @@ class Engine:
         dgroups = [[i for i in g if s.drow[i] >= 0] for g in groups]
         dgroups = [g for g in dgroups if g]
         if dgroups:
-            models.append((self.draft, s.dkv, self.drf_stream, dgroups, s.drow))
-        for model, kv, stream, mgroups, rowmap in models:
+            models.append((self.draft, s.dkv, self.drf_stream, dgroups, s.drow, None))
+        first = torch.empty(s.n_seq, dtype=torch.int32, device=self.device)
+        first_h = None
+        for model, kv, stream, mgroups, rowmap, window in models:
+            if window is not None:
+                kv.set_window(window.lo, window.hi)
             chunks = []
             row0 = 0
             last = []
@@ -320,9 +333,11 @@ class Engine:
                 T = len(toks)
                 o = 0
                 r0, r1 = int(rowmap[g[0]]), int(rowmap[g[-1]])
+                bt = (self._bt(kv, rowmap[g], stream) if isinstance(kv, HostPagedKVCache)
+                      else kv.block_table[r0:r1 + 1])  # host KV: window-relative pages
                 fb = ForwardBatch(meta[o:o + T], meta[o + T:o + 2 * T], meta[o + 2 * T:o + 3 * T],
                                   meta[o + 3 * T:o + 3 * T + len(g) + 1], meta[o + 3 * T + len(g) + 1:],
-                                  kv.block_table[r0:r1 + 1], len(g), int(lens[g].max()), None, row0)
+                                  bt, len(g), int(lens[g].max()), None, row0)
                 last.extend(row0 + qs[1:] - 1)
                 chunks.append(fb)
                 row0 += T
@@ -330,17 +345,18 @@ class Engine:
             chunks[0].last_rows = lr
             if model is self.target:
                 logits = model.forward(chunks, kv, stream)
-                first = torch.empty(s.n_seq, dtype=torch.int32, device=self.device)
+                lo = 0 if window is None else window.lo  # logits rows = this pass's sequences
                 with torch.cuda.stream(stream):
                     for bi, b in enumerate(s.batches):
-                        if b.n == 0:
+                        if b.n == 0 or (window is not None and b is not window):
                             continue
                         u = None
                         if s.mode == "sample":
                             u = self._up(input_uniforms(s.seed, -2, bi, 3, b.n), stream, torch.float32)
-                        native.sample_tokens(logits[b.lo:b.hi], first[b.lo:b.hi], uniforms=u,
+                        native.sample_tokens(logits[b.lo - lo:b.hi - lo], first[b.lo:b.hi], uniforms=u,
                                              temperature=s.temperature, stream=stream)
-                    first_h = first.to("cpu", non_blocking=True)
+                    if window is None or window is s.batches[-1] or s.batches[-1].n == 0:
+                        first_h = first.to("cpu", non_blocking=True)
             else:
                 model.forward(chunks, kv, stream, want_logits=False)
         self.tgt_stream.synchronize()
@@ -363,6 +379,9 @@ class Engine:
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
         for kv in (s.tkv, s.dkv):
+            if isinstance(kv, HostPagedKVCache):
+                kv.fill_random(g, self.device)
+                continue
             kv.k.normal_(0.0, 1.0, generator=g)
             kv.v.normal_(0.0, 1.0, generator=g)
         rng = np.random.default_rng(seed)
@@ -527,6 +546,7 @@ class Engine:
         act = s.dlist[bi]
         new = s.pending_new[bi]
         na, nn = act.size, new.size
+        s.tkv.set_window(s.batches[bi].lo, s.batches[bi].hi)  # host-resident KV: this batch's pages
         T = na * (n + 1)
         ctx = s.ctx[act]
         pos = ctx[:, None] + np.arange(n + 1)[None, :]
@@ -759,7 +779,8 @@ class Engine:
     def generate(self, prompts: list, max_new_tokens: int, policy: Policy | None = None, seed: int = 0,
                  mode: str = "greedy", temperature: float = 1.0, forced_p: float | None = None,
                  draft_kv: str = "cached", draft_cached: int | None = None,
-                 refill: bool | None = None, max_admit: int | None = None) -> list[list[int]]:
+                 refill: bool | None = None, max_admit: int | None = None,
+                 kv_host: bool = False) -> list[list[int]]:
         """prompts (token id lists) → committed continuations, max_new_tokens each.
 
         With more prompts than the two batches hold (or ``refill=True``), the
@@ -778,12 +799,12 @@ class Engine:
             s = self.new_session(slots, min(policy.bs_decoding, slots), max_len, policy.n_cand, mode, seed,
                                  temperature, forced_p, policy.bs_draft, draft_kv, draft_cached,
                                  prompts=[np.asarray(p, np.int32) for p in prompts], max_new=max_new_tokens,
-                                 max_admit=max_admit)
+                                 max_admit=max_admit, kv_host=kv_host)
             self.decode(s)
             self.last_session = s
             return [o[:max_new_tokens] for o in s.out]
         s = self.new_session(S, policy.bs_decoding, max_len, policy.n_cand, mode, seed, temperature, forced_p,
-                             policy.bs_draft, draft_kv, draft_cached)
+                             policy.bs_draft, draft_kv, draft_cached, kv_host=kv_host)
         self.prefill(s, prompts, max_new_tokens, policy.bs_prefill)
         if (s.remaining > 0).any():
             self.first_draft(s)

@@ -128,7 +128,7 @@ class CausalLM:
         for li, L in enumerate(self.w.layers):
             if hook:
                 hook(li, "attn_start", stream)
-            kc, vc = kv.layer(li)
+            kc, vc = kv.layer(li, stream)
             base = None
             wqkv, wo = L.wqkv, L.wo
             if wqkv is None:  # attention weights stream with the layer: wait before QKV
@@ -157,6 +157,7 @@ class CausalLM:
                     self._moe(L, base, xn[:T], h[:T], out, T, stream)
                 else:
                     self._mlp(base, xn[:T], h[:T], out, T, stream)
+            kv.release(li, stream)  # host-resident KV: write the layer's window back
             self._ffn_release(li, stream)
             if hook:
                 hook(li, "ffn_end", stream)

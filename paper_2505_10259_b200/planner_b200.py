@@ -22,7 +22,7 @@ import math
 from .acceptance import AcceptanceModel, expected_accepted
 from .config import ModelArch
 from .errors import InfeasiblePlan
-from .kvcache import PagedKVCache
+from .kvcache import HostPagedKVCache, PagedKVCache
 from .weights import attn_elems, ffn_offsets, unit_layout
 
 GB = 1e9
@@ -75,6 +75,7 @@ class OffloadPlan:
     t_nvlink_s: float = 0.0
     disk_layers: tuple[int, ...] = ()   # f4: streamed layers kept on disk (subset of stream_layers)
     t_disk_s: float = 0.0
+    kv_host: bool = False               # target KV in pinned host DRAM, one batch staged per layer
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -129,7 +130,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,
-                 world: int = 1, allow_shards: bool = True, disk_budget: int = 0) -> OffloadPlan:
+                 world: int = 1, allow_shards: bool = True, disk_budget: int = 0,
+                 kv_host_modes=(False,)) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
@@ -147,13 +149,21 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
 
     ``disk_budget`` > 0 (§8 f4, placement.py:241-243): streamed units beyond
     host DRAM (less two pinned staging units) live on disk and are read once
-    per pass, so the pass also costs disk bytes / disk_bytes_per_s."""
+    per pass, so the pass also costs disk bytes / disk_bytes_per_s.
+
+    ``kv_host_modes`` containing True lets the target KV live in host DRAM (the
+    reference's CPU-resident KV, placement.py:120-130): HBM keeps a 2-slot
+    window of one batch's per-layer KV, host DRAM the pool, and every pass also
+    moves the verified batch's KV host → GPU (the write-back uses the other
+    link direction)."""
     e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
+    draft_w = resident_bytes(draft, True)
     best = None
     cands = bs_candidates or [b for b in range(8, 2049, 8)]
     attn_layer = attn_elems(target) * 2
-    for stream_attn, mode in [(sa, m) for sa in stream_attn_modes for m in draft_kv_modes]:
+    for stream_attn, mode, kv_host in [(sa, m, kh) for sa in stream_attn_modes for m in draft_kv_modes
+                                        for kh in kv_host_modes]:
         # unit = bytes of one streamed (or pinned) layer; with stream_attn the
         # attention projections travel with the FFN and leave the resident set
         layer_bytes = unit_layout(target, stream_attn)[1]
@@ -168,12 +178,24 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
             else:
                 kcs = [bs if mode == "cached" else 0]
             for kc in kcs:
-                bs_draft = bs if mode == "cached" else min(bs, max_draft_chunk)
-                draft_rows = 2 * kc + (bs_draft if kc < bs else 0)
-                kv = (PagedKVCache.bytes_needed(target, 2 * bs, max_len, page_size)
-                      + PagedKVCache.bytes_needed(draft, draft_rows, max_len, page_size))
-                ws = workspace_bytes(target, draft, bs, n_cand, None if kc == bs else max(bs_draft * max_len, kc))
-                free = hbm_budget - fixed - kv - ws
+                # re-prefill scratch chunk: max_draft_chunk sequences; with host-resident
+                # KV (tiny HBM budgets) the largest of it, ½ and ¼ that fits
+                chunks = [bs] if mode == "cached" else sorted(
+                    {min(bs, max_draft_chunk >> k) for k in range(3 if kv_host else 1)}, reverse=True)
+                for bs_draft in chunks:
+                    draft_rows = 2 * kc + (bs_draft if kc < bs else 0)
+                    tkv_bytes = PagedKVCache.bytes_needed(target, 2 * bs, max_len, page_size)
+                    kv_link = 0  # KV bytes the verified batch moves host → GPU per pass
+                    host_kv = 0
+                    if kv_host:
+                        host_kv = tkv_bytes
+                        kv_link = tkv_bytes // 2
+                        tkv_bytes = HostPagedKVCache.window_bytes_needed(target, bs, max_len, page_size)
+                    kv = tkv_bytes + PagedKVCache.bytes_needed(draft, draft_rows, max_len, page_size)
+                    ws = workspace_bytes(target, draft, bs, n_cand, None if kc == bs else max(bs_draft * max_len, kc))
+                    free = hbm_budget - fixed - kv - ws
+                    if free >= 0:
+                        break
                 if free < 0:
                     continue
                 L = target.n_layer
@@ -181,6 +203,13 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                 eff = rates.tensor_flops * rates.tensor_efficiency
                 t_base = (verify_flops(target, bs, n_cand, ctx_len)
                           + draft_flops(draft, bs, n_cand, ctx_len, "mixed", kc)) / eff
+                # each draft chunk's decode steps stream the draft's weights from HBM
+                # (weight-bound at these row counts).  The re-fit tensor efficiency was
+                # measured with max_draft_chunk-sized chunks and absorbs their passes;
+                # the smaller chunks of host-KV plans pay the extra passes explicitly
+                if bs_draft < min(bs, max_draft_chunk) and kc < bs:
+                    extra = -(-(bs - kc) // bs_draft) - -(-(bs - kc) // max_draft_chunk)
+                    t_base += n_cand * extra * draft_w / rates.hbm_bytes_per_s
                 p0 = min(L, int(free // layer_bytes), cap)
                 for n_sh in (range(0, L - p0 + 1) if (world > 1 and allow_shards) else (0,)):
                     room = free - n_sh * layer_bytes / world
@@ -189,6 +218,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                     pinned = min(L - n_sh, int(room // layer_bytes), cap)
                     streamed = L - pinned - n_sh
                     n_disk = 0
+                    if host_kv and streamed * host_unit + host_kv > host_budget:
+                        continue
                     if streamed * host_unit > host_budget:
                         if disk_budget <= 0 or world > 1:
                             continue
@@ -196,7 +227,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                         n_disk = streamed - n_host
                         if n_disk * host_unit > disk_budget:
                             continue
-                    S = streamed * host_unit // world         # this rank's link bytes per pass
+                    S = streamed * host_unit // world + kv_link  # this rank's link bytes per pass
                     t_stream = max(S / rates.h2d_bytes_per_s, n_disk * host_unit / rates.disk_bytes_per_s)
                     t_nvl = ((streamed + n_sh) * layer_bytes * (world - 1) / world / rates.nvlink_bytes_per_s
                              if world > 1 else 0.0)
@@ -206,11 +237,11 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                     tps = bs * e_tok / t_round
                     if best is None or tps > best[0] * 1.001:
                         best = (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round,
-                                stream_attn, fixed, layer_bytes, kc, n_sh, t_nvl, host_unit, n_disk)
+                                stream_attn, fixed, layer_bytes, kc, n_sh, t_nvl, host_unit, n_disk, kv_host)
     if best is None:
         raise InfeasiblePlan("no batch size fits the HBM and host budgets")
     (tps, bs, mode, bs_draft, pinned, streamed, kv, ws, S, t_stream, t_comp, t_round, sa, fixed, layer_bytes, kc,
-     n_sh, t_nvl, host_unit, n_disk) = best
+     n_sh, t_nvl, host_unit, n_disk, kv_host) = best
     # pin the first layers (ascending order, placement.py:220-231); among the
     # rest, host-streamed layers are spread evenly between the sharded ones so
     # the PCIe link keeps a layer in flight while NVLink gathers the others
@@ -226,7 +257,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                         "shards": int(n_sh * layer_bytes / world)},
                        streamed * host_unit, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
                        kc if mode == "mixed" else 0, shard_l, world, t_nvl, disk_l,
-                       n_disk * host_unit / rates.disk_bytes_per_s)
+                       n_disk * host_unit / rates.disk_bytes_per_s, kv_host)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

@@ -321,3 +321,20 @@ def test_trace_causality_ffn_after_its_load(pair, codec):
             assert f.start >= load.end - 1e-5, (layer, f, load)
             checked += 1
     assert checked >= 4
+
+
+@pytest.mark.parametrize("draft_kv,refill", [("cached", False), ("reprefill", False), ("cached", True)])
+def test_host_resident_kv_matches(pair, draft_kv, refill):
+    """Target KV in pinned host DRAM (tiny-HBM budgets): each pass stages one
+    batch's pages per layer into a 2-slot HBM window and writes them back —
+    the same greedy tokens as HBM-resident KV (classic prefill per batch, or
+    slot refill with prefill inside the verify passes)."""
+    tw, dw = pair
+    prompts = tiny.prompts(13 if refill else 8, seed=41)
+    pol = Policy(8, 4, 4, 4)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 3})
+    ref = eng.generate(prompts, 12, pol, draft_kv=draft_kv, refill=refill)
+    got = eng.generate(prompts, 12, pol, draft_kv=draft_kv, refill=refill, kv_host=True)
+    s = eng.last_session
+    assert type(s.tkv).__name__ == "HostPagedKVCache" and s.tkv.bytes_h2d > 0
+    assert got == ref
