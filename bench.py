@@ -436,57 +436,63 @@ def main():
     # ---- generate(): the paper's end-to-end tokens/s (prefill included) ----
     gen = None
     if not args.no_e2e_generate:
-        del s
-        torch.cuda.empty_cache()
-        # Its own slot pool: with prefill inside every round the generate workload is
-        # tensor-bound, not link-bound, so the draft keeps a KV row per slot (no
-        # per-round context re-prefill) and HBM left after the engine's weights
-        # and window sets the slot count (headroom for the prefill activations).
-        from paper_2505_10259_b200.kvcache import PagedKVCache
+        try:
+            del s
+            torch.cuda.empty_cache()
+            # Its own slot pool: with prefill inside every round the generate workload is
+            # tensor-bound, not link-bound, so the draft keeps a KV row per slot (no
+            # per-round context re-prefill) and HBM left after the engine's weights
+            # and window sets the slot count (headroom for the prefill activations).
+            from paper_2505_10259_b200.kvcache import PagedKVCache
 
-        free_now, _ = torch.cuda.mem_get_info(device)
-        # the HBM budget (configs[1]: 24 GB cap) bounds the pool, not just the device's free memory
-        free_now = min(free_now // share, hbm - torch.cuda.memory_reserved(device))
-        g_len = args.ctx + args.e2e_new + args.n_cand + 2
-        per_slot = PagedKVCache.bytes_needed(tgt, 1, g_len) + PagedKVCache.bytes_needed(drf, 1, g_len)
-        headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
-        bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
-        e_kv_host, e_draft_kv, e_bs_draft = False, "cached", None
-        if plan.kv_host:  # tiny HBM budget: the decode plan's host-KV pool and re-prefill draft
-            bs_e, e_kv_host, e_draft_kv, e_bs_draft = plan.bs_decoding, True, plan.draft_kv, plan.bs_draft
-        S_e = args.e2e_seqs or 6 * bs_e
-        rng = np.random.default_rng(1234 + rank)
-        prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
-        pol = Policy(bs_prefill=min(S_e, 2 * bs_e), bs_decoding=min(bs_e, (S_e + 1) // 2),
-                     bs_draft=e_bs_draft or min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
-        torch.cuda.synchronize(device)
-        g0 = time.perf_counter()
-        admit = args.e2e_admit or None
-        round0 = eng.round
+            free_now, _ = torch.cuda.mem_get_info(device)
+            # the HBM budget (configs[1]: 24 GB cap) bounds the pool, not just the device's free memory
+            free_now = min(free_now // share, hbm - torch.cuda.memory_reserved(device))
+            g_len = args.ctx + args.e2e_new + args.n_cand + 2
+            per_slot = PagedKVCache.bytes_needed(tgt, 1, g_len) + PagedKVCache.bytes_needed(drf, 1, g_len)
+            headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
+            bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
+            e_kv_host, e_draft_kv, e_bs_draft = False, "cached", None
+            if plan.kv_host:  # tiny HBM budget: the decode plan's host-KV pool and re-prefill draft
+                bs_e, e_kv_host, e_draft_kv, e_bs_draft = plan.bs_decoding, True, plan.draft_kv, plan.bs_draft
+                eng.prefill_chunk_tokens = 2048  # prefill activations must fit beside the capped plan
+            S_e = args.e2e_seqs or 6 * bs_e
+            rng = np.random.default_rng(1234 + rank)
+            prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
+            pol = Policy(bs_prefill=min(S_e, 2 * bs_e), bs_decoding=min(bs_e, (S_e + 1) // 2),
+                         bs_draft=e_bs_draft or min(bs_e, (S_e + 1) // 2), n_cand=args.n_cand)
+            torch.cuda.synchronize(device)
+            g0 = time.perf_counter()
+            admit = args.e2e_admit or None
+            round0 = eng.round
 
-        def logged_round(sess, _r=round0):  # progress of the long generate leg on stderr
-            c = _r(sess)
-            if sess.rounds % 10 == 0 or sess.rounds <= 3:
-                log(f"generate: round {sess.rounds}, queue {len(sess.queue)}, active {int(sess.active.sum())}")
-            return c
+            def logged_round(sess, _r=round0):  # progress of the long generate leg on stderr
+                c = _r(sess)
+                if sess.rounds % 10 == 0 or sess.rounds <= 3:
+                    log(f"generate: round {sess.rounds}, queue {len(sess.queue)}, active {int(sess.active.sum())}")
+                return c
 
-        log(f"generate: {S_e} prompts through {2 * pol.bs_decoding} slots")
+            log(f"generate: {S_e} prompts through {2 * pol.bs_decoding} slots")
 
-        eng.round = logged_round
-        toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=e_draft_kv, max_admit=admit,
-                            kv_host=e_kv_host)
-        g_wall = time.perf_counter() - g0
-        eng.round = round0
-        assert all(len(t) == args.e2e_new for t in toks)
-        gs = eng.last_session
-        gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
-               "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
-               "policy": list(pol.as_tuple()), "draft_kv": e_draft_kv, "target_kv_host": e_kv_host,
-               "refill": gs.refill, "slots": gs.n_seq, "max_admit_per_round": admit,
-               "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
-                       "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "
-                       "verify pass), so every round streams the layers once for prefill and decode alike; "
-                       "paper's e2e definition (prefill included)"}
+            eng.round = logged_round
+            toks = eng.generate(prompts, args.e2e_new, pol, forced_p=args.p, draft_kv=e_draft_kv, max_admit=admit,
+                                kv_host=e_kv_host)
+            g_wall = time.perf_counter() - g0
+            eng.round = round0
+            assert all(len(t) == args.e2e_new for t in toks)
+            gs = eng.last_session
+            gen = {"value": S_e * args.e2e_new / g_wall, "unit": "tokens/s", "sequences": S_e,
+                   "prompt_tokens": args.ctx, "new_tokens": args.e2e_new, "wall_s": g_wall, "rounds": gs.rounds,
+                   "policy": list(pol.as_tuple()), "draft_kv": e_draft_kv, "target_kv_host": e_kv_host,
+                   "refill": gs.refill, "slots": gs.n_seq, "max_admit_per_round": admit,
+                   "note": "Engine.generate(): host token ids in, host token lists out; the prompts stream through "
+                           "the 2·bs_decoding slots with slot refill (each admitted prompt is prefilled inside a "
+                           "verify pass), so every round streams the layers once for prefill and decode alike; "
+                           "paper's e2e definition (prefill included)"}
+        except torch.OutOfMemoryError as exc:  # the decode result above stands; report the leg's failure
+            gen = {"error": f"generate() leg out of HBM: {str(exc).splitlines()[0]}"}
+            eng.__dict__.pop("round", None)  # drop the logging wrapper (instance attribute)
+            torch.cuda.empty_cache()
 
     if args.trace_out and rank == 0:
         from paper_2505_10259_b200.trace import SimResult, busy, export_chrome

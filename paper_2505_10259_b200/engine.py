@@ -193,6 +193,7 @@ class DecodeSession:
 
 class Engine:
     FRESH_CHUNK = 64  # sequences per draft context prefill of freshly admitted slots
+    prefill_chunk_tokens = 16384  # prompt tokens per chunk of a verify pass that prefills (activation workspace)
 
     def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 16,
                  trace: bool = True):
@@ -533,7 +534,7 @@ class Engine:
                 native.sample_tokens(logits, out_tok, stream=st)
 
     # ----------------------------------------------------------------- verify
-    def _verify(self, s: DecodeSession, bi: int, rnd: int, chunk_tokens: int = 16384) -> None:
+    def _verify(self, s: DecodeSession, bi: int, rnd: int) -> None:
         """Verify batch ``bi``: the drafted slots (``s.dlist[bi]``, n_cand+1
         query tokens each) and, with slot refill, prefill the prompts admitted
         into its free slots (``s.pending_new[bi]``) in the same layer pass —
@@ -584,6 +585,7 @@ class Engine:
             last.append(np.arange(T, dtype=np.int32))
         row0 = T
         lo = 0
+        chunk_tokens = self.prefill_chunk_tokens
         while lo < nn:  # admitted prompts, ≤ chunk_tokens per chunk
             hi, tok = lo, 0
             while hi < nn and (hi == lo or tok + len(s.prompts[s.slot_prompt[new[hi]]]) <= chunk_tokens):
