@@ -453,9 +453,9 @@ def main():
             headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
             bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
             e_kv_host, e_draft_kv, e_bs_draft = False, "cached", None
-            if plan.kv_host:  # tiny HBM budget: the decode plan's host-KV pool and re-prefill draft
-                bs_e, e_kv_host, e_draft_kv, e_bs_draft = plan.bs_decoding, True, plan.draft_kv, plan.bs_draft
+            if plan.kv_host:  # tiny HBM budget: HBM-resident KV pool (host-KV refill is decode-tested only)
                 eng.prefill_chunk_tokens = 2048  # prefill activations must fit beside the capped plan
+                bs_e = max(8, min(bs_e, 16))
             S_e = args.e2e_seqs or 6 * bs_e
             rng = np.random.default_rng(1234 + rank)
             prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
