@@ -32,6 +32,8 @@ import time
 
 import numpy as np
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see paper_2505_10259_b200/__init__.py
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -453,9 +455,9 @@ def main():
             headroom = min(10e9, 0.35 * free_now)  # prefill activations of the admitted prompts
             bs_e = max(8, int((free_now - headroom) // per_slot) // 2 // 8 * 8)
             e_kv_host, e_draft_kv, e_bs_draft = False, "cached", None
-            if plan.kv_host:  # tiny HBM budget: HBM-resident KV pool (host-KV refill is decode-tested only)
+            if plan.kv_host:  # tiny HBM budget: the decode plan's host-resident target KV and re-prefill draft
                 eng.prefill_chunk_tokens = 2048  # prefill activations must fit beside the capped plan
-                bs_e = max(8, min(bs_e, 16))
+                bs_e, e_kv_host, e_draft_kv, e_bs_draft = plan.bs_decoding, True, "reprefill", plan.bs_draft
             S_e = args.e2e_seqs or 6 * bs_e
             rng = np.random.default_rng(1234 + rank)
             prompts = [rng.integers(0, tgt.vocab, args.ctx).astype(np.int32) for _ in range(S_e)]
@@ -516,7 +518,10 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": dev_s / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, random prompt KV, forced acceptance p)",
-        "config": {"workload": f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM",
+        "config": {"workload": (f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM"
+                                if args.config == "8x22b" and not args.hbm_gb else
+                                f"configs[1]: {tgt.name} offloaded + {drf.name} draft, {world} B200, "
+                                f"HBM capped to {hbm / 2**30:.0f} GiB"),
                    "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
                    "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,

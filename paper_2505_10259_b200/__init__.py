@@ -7,6 +7,17 @@ that keeps the reference's API shapes (Policy / Workload / ModelSpec /
 HardwareProfile, SimEvent / SimResult, planner functions) and adds the
 ``Engine.generate`` / ``Engine.run_decoding`` entry points.
 """
+import os as _os
+
+# The engine runs up to eight streams per device (verify, draft, weight copy,
+# XC4 decode, KV h2d/d2h, torch's own).  With the default 8 hardware work
+# queues two of them can share a queue, and a cross-stream event wait at the
+# head of one blocks the other's already-runnable work — with host-resident KV
+# that closes a cycle (verify ← KV h2d ← KV d2h ← verify) and the device stalls.
+# One queue per stream removes the false dependency; it must be set before the
+# CUDA context exists (tools/repro_hostkv.py reproduces the stall without it).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .acceptance import AcceptanceModel, expected_accepted, pmf, sample_accepted
 from .config import MIXTRAL_8X7B, MIXTRAL_8X22B, MISTRAL_7B, MISTRAL_7B_V3, PAIRS, TINY_DRAFT, TINY_TARGET, ModelArch
 from .domain import HardwareProfile, ModelSpec, Policy, Workload, validate_profile
