@@ -120,3 +120,12 @@ def test_disk_tier_file_round_trip(tmp_path):
             d._read(mv, off, lo, hi)
         assert np.array_equal(out, t.numpy()) and refs[li].nbytes == n
     d.close()
+
+
+def test_package_sets_one_work_queue_per_stream():
+    """Importing the package reserves a hardware work queue per stream before the
+    CUDA context exists (the host-KV + refill stall, DESIGN.md robustness)."""
+    import os
+
+    import paper_2505_10259_b200  # noqa: F401
+    assert int(os.environ["CUDA_DEVICE_MAX_CONNECTIONS"]) >= 16
