@@ -314,6 +314,7 @@ def main():
     bytes0 = st.bytes_issued if st else 0
     raw0 = st.raw_bytes_issued if st else 0
     nvl0 = st.nvlink_bytes_issued if st else 0
+    kvh0 = getattr(s.tkv, "bytes_h2d", 0)  # host-resident target KV: window pages cross the same link
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     if eng.tracer.enabled:
@@ -342,6 +343,9 @@ def main():
     streamed = (st.bytes_issued - bytes0) if st else 0       # bytes over this rank's link
     streamed_raw = (st.raw_bytes_issued - raw0) if st else 0  # layer bytes they delivered
     nvl = (st.nvlink_bytes_issued - nvl0) if st else 0       # bytes this rank received from HBM shards
+    kv_link = getattr(s.tkv, "bytes_h2d", 0) - kvh0          # host KV window pages (0 with HBM KV)
+    streamed += kv_link
+    streamed_raw += kv_link
     launches = dict(native.launches)
     if world > 1:
         rdev = device if args.dist_backend == "nccl" else "cpu"
@@ -531,13 +535,15 @@ def main():
                    "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
                    "streamed_bytes_per_round": int(streamed / steps * world),
+                   "kv_h2d_bytes_per_round": int(kv_link / steps * world),
                    "streamed_layer_bytes_per_round": len(plan.stream_layers) * layer_bytes,
                    "host_pinned_bytes": store.bytes if store is not None else 0, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
                    "parallelism": f"dp{world} (independent prompt shards)", "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "h2d", "achieved": achieved_link / 1e9, "peak": link / 1e9, "unit": "GB/s",
                      "frac": achieved_link / link, "traffic": None,
                      "note": "dominant 'kernel' = copy-engine stream of the streamed layer units (XC4-encoded "
-                             "bytes when codec=xc4); peak = pinned 1 GiB H2D measured in this run"},
+                             "bytes when codec=xc4) plus, with host-resident target KV, the KV window pages; peak = "
+                             "pinned 1 GiB H2D measured in this run"},
         "roofline_tokens_per_s": roof, "frac_of_roofline": value / roof if roof else None,
         "nvlink": ({"received_bytes_per_round": int((nvl + streamed_raw * (world - 1)) / steps),
                     "achieved_GBps": (nvl + streamed_raw * (world - 1)) / dev_s / 1e9,
