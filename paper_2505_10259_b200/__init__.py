@@ -16,7 +16,15 @@ import os as _os
 # that closes a cycle (verify ← KV h2d ← KV d2h ← verify) and the device stalls.
 # One queue per stream removes the false dependency; it must be set before the
 # CUDA context exists (tools/repro_hostkv.py reproduces the stall without it).
-_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+if "CUDA_DEVICE_MAX_CONNECTIONS" not in _os.environ:
+    _os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
+    import sys as _sys
+    _torch = _sys.modules.get("torch")
+    if _torch is not None and _torch.cuda.is_initialized():
+        import warnings as _warnings
+        _warnings.warn("paper_2505_10259_b200 imported after the CUDA context was created: set "
+                       "CUDA_DEVICE_MAX_CONNECTIONS=32 in the environment (host-resident KV can stall with 8 "
+                       "hardware work queues)", RuntimeWarning, stacklevel=2)
 
 from .acceptance import AcceptanceModel, expected_accepted, pmf, sample_accepted
 from .config import MIXTRAL_8X7B, MIXTRAL_8X22B, MISTRAL_7B, MISTRAL_7B_V3, PAIRS, TINY_DRAFT, TINY_TARGET, ModelArch
