@@ -12,10 +12,10 @@ import os as _os
 # The engine runs up to eight streams per device (verify, draft, weight copy,
 # XC4 decode, KV h2d/d2h, torch's own).  With the default 8 hardware work
 # queues two of them can share a queue, and a cross-stream event wait at the
-# head of one blocks the other's already-runnable work — with host-resident KV
-# that closes a cycle (verify ← KV h2d ← KV d2h ← verify) and the device stalls.
-# One queue per stream removes the false dependency; it must be set before the
-# CUDA context exists (tools/repro_hostkv.py reproduces the stall without it).
+# head of one can block the other's runnable work.  One queue per stream rules
+# that false dependency out (mitigation for the intermittent host-KV + refill
+# stall, DESIGN.md robustness notes; cause unconfirmed).  Must be set before
+# the CUDA context exists.
 if "CUDA_DEVICE_MAX_CONNECTIONS" not in _os.environ:
     _os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"
     import sys as _sys

@@ -124,7 +124,7 @@ def test_disk_tier_file_round_trip(tmp_path):
 
 def test_package_sets_one_work_queue_per_stream():
     """Importing the package reserves a hardware work queue per stream before the
-    CUDA context exists (the host-KV + refill stall, DESIGN.md robustness)."""
+    CUDA context exists (mitigation for the host-KV + refill stall)."""
     import os
 
     import paper_2505_10259_b200  # noqa: F401

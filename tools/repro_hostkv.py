@@ -1,9 +1,9 @@
 #!/usr/bin/env python
-"""Regression check for the host-resident-KV + slot-refill stall (DESIGN.md,
-robustness): 8 layers of the 8x7B target at a 24 GiB cap, N prompts through 192
-slots with target KV in host DRAM.  With CUDA_DEVICE_MAX_CONNECTIONS=8 (the
-CUDA default) it stalled at the barrier of round ~11 — hardware work-queue
-false dependency between the engine's streams; the package now sets 32.
+"""Regression check for the intermittent host-resident-KV + slot-refill stall
+(DESIGN.md robustness notes): 8 layers of the 8x7B target at a 24 GiB cap, N
+prompts through 192 slots with target KV in host DRAM.  Stalled once at the
+barrier of round 11; 13 later runs (5 with CUDA_DEVICE_MAX_CONNECTIONS=8)
+completed.  Cause unconfirmed.
 
     python tools/repro_hostkv.py 576
 """
