@@ -577,27 +577,37 @@ __device__ __forceinline__ TileInfo tile_info(int t, const int32_t* __restrict__
   const int kbs = (num_kb + k_split - 1) / k_split;
   ti.kb0 = ti.ks * kbs;
   ti.kb1 = min(num_kb, ti.kb0 + kbs);
-  raster_tile(t, m_tiles, n_tiles, mt, nt);
   ti.expert = 0;
-  ti.row0 = mt * tileM;
   ti.row_end = M;
-  ti.n0 = nt * BNc;
-  ti.valid = ti.row0 < M;
-  if (offs != nullptr) {
-    int before = 0;
-    ti.valid = false;
-    for (int e = 0; e < E; ++e) {
-      const int lo = offs[e], hi = offs[e + 1];
-      const int nt_e = (hi - lo + tileM - 1) / tileM;
-      if (mt < before + nt_e) {
-        ti.expert = e;
-        ti.row0 = lo + (mt - before) * tileM;
-        ti.row_end = hi;
-        ti.valid = true;
-        break;
-      }
-      before += nt_e;
+  if (offs == nullptr) {
+    raster_tile(t, m_tiles, n_tiles, mt, nt);
+    ti.row0 = mt * tileM;
+    ti.n0 = nt * BNc;
+    ti.valid = ti.row0 < M;
+    return ti;
+  }
+  // grouped: the raster runs expert by expert (bands of ≤ 16 of the expert's own
+  // m-tiles), so an expert's weight tiles are read once by every m-tile that needs
+  // them instead of once per band the expert straddles (a global band raster read
+  // 2.07× the weight bytes at bs 472: profiles/ncu_gemm_persistent_r1.md)
+  ti.valid = false;
+  ti.row0 = M;
+  ti.n0 = 0;
+  int base = 0;
+  for (int e = 0; e < E; ++e) {
+    const int lo = offs[e], hi = offs[e + 1];
+    const int nt_e = (hi - lo + tileM - 1) / tileM;
+    const int span = nt_e * n_tiles;
+    if (t < base + span) {
+      raster_tile(t - base, nt_e, n_tiles, mt, nt);
+      ti.expert = e;
+      ti.row0 = lo + mt * tileM;
+      ti.row_end = hi;
+      ti.n0 = nt * BNc;
+      ti.valid = true;
+      break;
     }
+    base += span;
   }
   return ti;
 }

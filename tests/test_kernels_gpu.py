@@ -227,8 +227,8 @@ def test_gemm_swiglu(M, I, K, gemm_variant):
 
 @pytest.mark.parametrize("counts", [[0, 3, 130, 0, 1, 255, 256, 7], [320] * 8, [1, 0, 0, 0, 0, 0, 0, 0],
                                     [1000, 24, 0, 0, 513, 2, 2, 9]])
-def test_gemm_grouped(counts, gemm_variant):
-    E, N, K = len(counts), 256, 384
+def test_gemm_grouped(counts, gemm_variant, N=256):
+    E, K = len(counts), 384
     rows = sum(counts)
     g = torch.Generator(device=DEV).manual_seed(rows)
     a = torch.randn(rows, K, device=DEV, generator=g).to(torch.bfloat16)
@@ -242,6 +242,13 @@ def test_gemm_grouped(counts, gemm_variant):
     for e in range(E):
         ref[o[e]:o[e + 1]] = (a[o[e]:o[e + 1]].float() @ b[e].float().T) * w[o[e]:o[e + 1], None]
     _bf16_close(out, ref)
+
+
+@pytest.mark.parametrize("counts", [[2200, 130, 0, 700], [0, 4100, 1, 129]])
+def test_gemm_grouped_expert_bands(counts, gemm_variant):
+    """Experts with more m-tiles than one raster band (> 16) and many n-tiles:
+    the expert-major tile walk covers every (expert, m-tile, n-tile) once."""
+    test_gemm_grouped(counts, gemm_variant, N=1024)
 
 
 # ----------------------------------------------------------------- K8 ---
