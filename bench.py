@@ -32,10 +32,12 @@ import time
 
 import numpy as np
 
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see paper_2505_10259_b200/__init__.py
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+import paper_2505_10259_b200  # noqa: E402
+
+paper_2505_10259_b200.reserve_work_queues(32)  # one hardware queue per engine stream (DESIGN.md robustness notes)
 
 
 def parse():

@@ -145,19 +145,22 @@ size_t so_gemm_workspace_bytes(int M, int N, int K);
 int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
                     const void* aux, void* workspace, size_t ws_bytes, void* stream);
 
-/* Tile variant of the GEMMs (process-wide; for tests and benchmarks):
- * 0 = auto (persistent kernels with double-buffered TMEM accumulators:
- * CTA-pair 256×256 cta_group::2 tiles for M ≥ 1024 and N % 256 == 0, else
- * 1-CTA 128×{128,256}), 1 = persistent 1-CTA only, 2 = persistent CTA-pair
- * wherever legal, 3 = the auto choice with one tile per CTA (non-persistent). */
-int so_gemm_set_variant(int variant);
-
 /* Grouped (MoE) GEMM: rows [offs[e], offs[e+1]) of A use expert e's weight
  * B + e·N·K.  max_rows bounds offs[E] (no host sync: the tile schedule is
  * derived on device from offs). */
 int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_offsets,
                          int E, int max_rows, int N, int K, void* C, int ldc,
                          int epilogue, const void* aux, void* stream);
+/* The general GEMM entry the three above specialise: dense (expert_offsets ==
+ * NULL, optional split-K workspace) or grouped (M = max_rows), with the tile
+ * variant an explicit argument — 0 = auto (persistent kernels with
+ * double-buffered TMEM accumulators: CTA-pair 256×256 cta_group::2 tiles for
+ * dense M ≥ 1024 with N % 256 == 0, else 1-CTA 128×{128,256}), 1 = persistent
+ * 1-CTA only, 2 = persistent CTA-pair wherever legal, 3 = the auto choice with
+ * one tile per CTA (non-persistent, no split-K).  No process-wide state. */
+int so_gemm_bf16_v(const void* A, const void* B, const int32_t* expert_offsets, int E, int M, int N, int K,
+                   void* C, int ldc, int epilogue, const void* aux, void* workspace, size_t ws_bytes,
+                   int variant, void* stream);
 
 /* ---- K8: auxiliary ------------------------------------------------------- */
 int so_embed(const int32_t* tokens, const void* table, int T, int H, void* out, void* stream);
@@ -179,10 +182,44 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* q_start, const int32_t* kv_before,
                   int bs, int max_q, int hq, int hkv, int dh, int page_size,
                   float scale, void* out, void* stream);
-/* K/V tile staging (process-wide; tests and benchmarks): 0 = TMA boxes issued
- * by one thread where the page size allows (pages of ≤ 32 slots dividing 32,
- * or multiples of 32), else cp.async; 1 = cp.async by every thread. */
-int so_attn_set_variant(int variant);
+/* Same with the K/V tile staging an explicit argument: 0 = TMA boxes issued by
+ * one thread where the page size allows (pages of ≤ 32 slots dividing 32, or
+ * multiples of 32), else cp.async (so_attn_paged's choice); 1 = cp.async by
+ * every thread. */
+int so_attn_paged_v(const void* q, const void* k_cache, const void* v_cache,
+                    const int32_t* block_table, int max_pages,
+                    const int32_t* q_start, const int32_t* kv_before,
+                    int bs, int max_q, int hq, int hkv, int dh, int page_size,
+                    float scale, void* out, int variant, void* stream);
+
+/* ---- Canonical-order arithmetic (parity mode, tiny shapes) ----------------
+ * The same ops, operands, epilogues and bf16 rounding points as the product
+ * kernels above (so_gemm_bf16 / so_gemm_grouped_bf16, so_rmsnorm,
+ * so_rope_kv_append, so_attn_paged, so_router_top2), computed by CUDA cores
+ * with every float op a single correctly rounded IEEE op in a fixed order
+ * (sequential fma dot products, det_exp, IEEE sqrt/div; csrc/canon.cu header).
+ * oracle/csrc/canon_oracle.c restates them, so a model run through these
+ * entry points reproduces the CPU oracle's logits and tokens bit for bit —
+ * the "bit-exact accepted tokens on the tiny config" target (
+ * the verify pass it serves is modeled at costmodel.py:60-76).  One thread per
+ * output element: for parity tests, not throughput.
+ * so_canon_gemm: expert_offsets == NULL → dense C = epi(A·Bᵀ); else grouped as
+ * so_gemm_grouped_bf16 with M = max_rows.
+ * so_canon_rope_kv_append: rope_table [table_rows, dh] fp32 holds cos(p·f_i)
+ * in columns [0, dh/2) and sin(p·f_i) in [dh/2, dh) for position p (every
+ * position must be < table_rows; the kernel traps otherwise). */
+int so_canon_gemm(const void* A, const void* B, const int32_t* expert_offsets, int E, int M, int N, int K,
+                  void* C, int ldc, int epilogue, const void* aux, void* stream);
+int so_canon_rmsnorm(const void* x, const void* w, int T, int H, float eps, void* out, void* stream);
+int so_canon_rope_kv_append(const void* qkv, const int32_t* positions, const int32_t* slot_mapping, int T,
+                            int hq, int hkv, int dh, const float* rope_table, int table_rows, int page_size,
+                            void* q_out, void* k_cache, void* v_cache, void* stream);
+int so_canon_attn_paged(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
+                        int max_pages, const int32_t* q_start, const int32_t* kv_before, int bs, int max_q,
+                        int hq, int hkv, int dh, int page_size, float scale, void* out, void* stream);
+int so_canon_router_top2(const void* x, const void* w_gate, int T, int H, int E, int32_t* topk_idx,
+                         float* topk_w, int32_t* expert_offsets, int32_t* perm_token, float* row_weight,
+                         int32_t* token_rows, void* x_perm, void* workspace, void* stream);
 
 /* ---- K1: layer streamer -------------------------------------------------
  * Pinned host → HBM window slot, `chunk`-byte cudaMemcpyAsync pieces on the

@@ -19,8 +19,9 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import accept_ref
-from .model_ref import KV, Arch, forward
+from . import accept_ref, canon_ref
+from .model_ref import KV, Arch
+from .model_ref import forward as _forward_np
 
 
 def uniforms(seed: int, rnd: int, batch: int, kind: int, shape) -> np.ndarray:
@@ -36,11 +37,22 @@ def forced_counts(seed: int, rnd: int, batch: int, p: float, n_cand: int, size: 
 def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_new: int, n_cand: int,
              bs_decoding: int, mode: str = "greedy", seed: int = 0, forced_p: float | None = None,
              temperature: float = 1.0, mirror: bool = True, record: list | None = None,
-             margins: list | None = None):
+             margins: list | None = None, arith: str = "numpy"):
     """Returns (committed token lists, rounds).  ``margins`` (optional, filled
     per sequence) receives the top-1 − top-2 logit gap of the target row that
-    produced each committed token: a GPU/oracle divergence is legitimate only
-    where that gap is inside the bf16 noise of the two computations."""
+    produced each committed token.  ``arith="canonical"`` evaluates both models
+    in the canonical float order (canon_ref) — the order the B200 parity mode
+    reproduces bit for bit, so its tokens must equal these exactly;
+    ``"numpy"`` is the NumPy restatement (``mirror`` = bf16 rounding points)."""
+    if arith == "canonical":
+        def forward(arch, W, kv, seqs, toks, starts, _mirror, rows):
+            return canon_ref.forward(arch, W, kv, seqs, toks, starts, rows)
+
+        new_kv = canon_ref.KV16
+    elif arith == "numpy":
+        forward, new_kv = _forward_np, KV
+    else:
+        raise ValueError(f"arith must be 'numpy' or 'canonical', got {arith!r}")
     S = len(prompts)
     gap = [[] for _ in range(S)]
 
@@ -51,7 +63,7 @@ def generate(tarch: Arch, tW: dict, darch: Arch, dW: dict, prompts: list, max_ne
     assert 1 <= S <= 2 * bs_decoding
     batches = [list(range(0, min(bs_decoding, S))), list(range(bs_decoding, S))]
     max_len = max(len(p) for p in prompts) + max_new + n_cand + 2
-    tkv, dkv = KV(tarch, S, max_len), KV(darch, S, max_len)
+    tkv, dkv = new_kv(tarch, S, max_len), new_kv(darch, S, max_len)
     all_seq = list(range(S))
     starts0 = [0] * S
     tl = forward(tarch, tW, tkv, all_seq, [np.asarray(p) for p in prompts], starts0, mirror, "last")

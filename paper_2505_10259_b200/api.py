@@ -25,7 +25,8 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  seed: int = 0, trace: bool = True, page_size: int = 16, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
                  shared_store: SharedHostStore | None = None, stream_attn: bool = False,
-                 codec: str = "none", shard_layers=None, disk_layers=None, disk_path: str | None = None) -> Engine:
+                 codec: str = "none", shard_layers=None, disk_layers=None, disk_path: str | None = None,
+                 arith: str = "tensor") -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
@@ -37,7 +38,9 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     ``shard_layers`` (world > 1): layers kept 1/N per GPU in
     HBM and rebuilt each pass by an NVLink all-gather instead of the host link.
     ``disk_layers`` (§8 f4): streamed layers kept in a file at ``disk_path``
-    (default: a temporary file) and staged through pinned DRAM each pass."""
+    (default: a temporary file) and staged through pinned DRAM each pass.
+    ``arith="canonical"`` runs both models through the parity-mode kernels
+    (fixed IEEE order, bit-identical to the CPU oracle; tiny shapes only)."""
     if codec not in ("none", "xc4"):
         raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
@@ -61,7 +64,9 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
         disk = DiskTier(disk_path)
     enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
     if target_weights is not None:
-        tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc)
+        store = host_store or HostStore()
+        tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc,
+                            host_alloc=store.alloc)
     elif shared_store is not None:
         sink = shared_store.write_coded if enc is not None else shared_store.write_slice
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=sink,
@@ -86,6 +91,9 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                              shards=tw.shard_ffn, disk=disk) if (host or tw.shard_ffn) else None
     if disk is not None:
         weakref.finalize(streamer, disk.close)
-    target = TargetModel(tw, dev, streamer)
-    draft = DraftModel(dw, dev)
-    return Engine(target, draft, device=dev, page_size=page_size, trace=trace)
+    target = TargetModel(tw, dev, streamer, arith=arith)
+    draft = DraftModel(dw, dev, arith=arith)
+    eng = Engine(target, draft, device=dev, page_size=page_size, trace=trace)
+    # host-resident KV pools (DecodeSession kv_host) come from the same exact-size page-locked store
+    eng.host_alloc = (host_store or HostStore()).alloc if shared_store is None else None
+    return eng

@@ -427,8 +427,6 @@ int cache_map(CUtensorMap* m, const void* base, int dh, int box_rows) {
   return r == CUDA_SUCCESS ? SO_OK : SO_E_DRIVER;
 }
 
-int g_attn_variant = 0;  // 0 = TMA staging where the page size allows it, 1 = cp.async staging
-
 template <int DH, bool TMA>
 int launch(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
            const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
@@ -438,20 +436,10 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
   const size_t smem = (TMA ? 1024 : 0) + (size_t)kStages * 2 * Tile<DH, TMA>::kBytes + 2 * kStages * sizeof(uint64_t) +
                       (size_t)max_pages * sizeof(int32_t);
   auto kern = attn_paged_kernel<DH, TMA>;
-  {
-    // raised when a longer block table needs more smem; the verify and the draft
-    // streams launch this kernel from two host threads, so check-and-raise is atomic
-    static std::mutex mu;
-    static size_t attr_bytes = 0;
-    std::lock_guard<std::mutex> lock(mu);
-    if (smem > attr_bytes) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess)  // all of L1/smem as shared memory: 3 × 64 KB tiles per SM
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return (int)e;
-      attr_bytes = smem;
-    }
-  }
+  // raised when a longer block table needs more smem (per kernel and device, under a lock:
+  // the verify and the draft streams launch from two host threads); carveout 100 = all of
+  // L1/smem as shared memory, 3 × 64 KB tiles per SM
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, 100)) return rc;
   CUtensorMap mk, mv;
   memset(&mk, 0, sizeof(mk));
   memset(&mv, 0, sizeof(mv));
@@ -475,35 +463,39 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
 template <int DH>
 int launch_dh(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
               const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
-              cudaStream_t st) {
+              int variant, cudaStream_t st) {
   // TMA boxes cover whole pages (≤ 32 rows) or 32-row halves of larger pages
   const bool tma_ok = (page_size <= kKeys ? kKeys % page_size == 0 : page_size % kKeys == 0) &&
                       (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0;
-  if (g_attn_variant == 0 && tma_ok)
+  if (variant == 0 && tma_ok)
     return launch<DH, true>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
   return launch<DH, false>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
 }
 
 }  // namespace
 
-extern "C" int so_attn_paged(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
-                             int max_pages, const int32_t* q_start, const int32_t* kv_before, int bs, int max_q,
-                             int hq, int hkv, int dh, int page_size, float scale, void* out, void* stream) {
+extern "C" int so_attn_paged_v(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
+                               int max_pages, const int32_t* q_start, const int32_t* kv_before, int bs, int max_q,
+                               int hq, int hkv, int dh, int page_size, float scale, void* out, int variant,
+                               void* stream) {
   SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
   SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
-  SO_REQUIRE(page_size >= 1, SO_E_SHAPE);
+  SO_REQUIRE(page_size >= 1 && (variant == 0 || variant == 1), SO_E_SHAPE);
   SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (bs == 0) return SO_OK;
   cudaStream_t st = as_stream(stream);
-  if (dh == 128) return launch_dh<128>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
-                                    page_size, scale, out, st);
-  if (dh == 64) return launch_dh<64>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
-                                  page_size, scale, out, st);
+  if (dh == 128)
+    return launch_dh<128>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+                          page_size, scale, out, variant, st);
+  if (dh == 64)
+    return launch_dh<64>(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv,
+                         page_size, scale, out, variant, st);
   return SO_E_UNSUPPORTED;
 }
 
-extern "C" int so_attn_set_variant(int variant) {
-  SO_REQUIRE(variant == 0 || variant == 1, SO_E_SHAPE);
-  g_attn_variant = variant;
-  return SO_OK;
+extern "C" int so_attn_paged(const void* q, const void* k_cache, const void* v_cache, const int32_t* block_table,
+                             int max_pages, const int32_t* q_start, const int32_t* kv_before, int bs, int max_q,
+                             int hq, int hkv, int dh, int page_size, float scale, void* out, void* stream) {
+  return so_attn_paged_v(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv, dh,
+                         page_size, scale, out, 0, stream);
 }

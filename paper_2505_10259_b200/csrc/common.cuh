@@ -3,6 +3,11 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/specoffload_b200.h"
 
 #define SO_CHECK_LAUNCH()                                   \
@@ -52,4 +57,41 @@ __device__ __forceinline__ int4 pack8(const float* f) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   return v;
+}
+
+// Raise `kern`'s dynamic shared-memory limit to at least `bytes` on the current
+// device (and, optionally, its smem carveout).  The verify and the draft
+// streams launch the same kernels from two host threads and a process may
+// drive several devices, so the bookkeeping is per (kernel, device) under one
+// lock; a launch that needs no raise only takes the uncontended lock.
+inline int ensure_smem_attr(const void* kern, size_t bytes, int carveout = -1) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> raised;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = raised[{kern, dev}];
+  if (bytes <= have) return 0;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && carveout >= 0) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  if (e != cudaSuccess) return (int)e;
+  have = bytes;
+  return 0;
+}
+
+// SM count of the current device (cached per device).
+inline int device_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (n <= 0) n = 148;
+  cache[dev] = n;
+  return n;
 }

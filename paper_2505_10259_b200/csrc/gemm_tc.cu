@@ -890,35 +890,22 @@ int make_map_3d(CUtensorMap* m, const void* base, uint64_t groups, uint64_t rows
   return r == CUDA_SUCCESS ? SO_OK : SO_E_DRIVER;
 }
 
-int g_sm_count = 0;
-int sm_count() {
-  if (g_sm_count == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sm_count <= 0) g_sm_count = 148;
-  }
-  return g_sm_count;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int BN, int EPI>
 int launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const int32_t* offs, int E, int m_tiles, int M,
               int N, int K, void* C, int ldc, const void* aux, cudaStream_t st) {
   using CF = Cfg<BN>;
   auto kern = gemm_tc_kernel<BN, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem);
-    if (e != cudaSuccess) return (int)e;
-    attr_set = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), CF::kSmem)) return rc;
   const int n_tiles = (N + BN - 1) / BN;
   kern<<<m_tiles * n_tiles, kThreads, CF::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, m_tiles, n_tiles);
   SO_CHECK_LAUNCH();
   return SO_OK;
 }
 
-int g_variant = 0;  // 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where legal, 3 = one tile per CTA
+// Tile variant, an explicit argument of every launch (no process state):
+// 0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair tiles where legal, 3 = one tile per CTA
 
 // persistent launch: one CTA (pair) per SM (pair), never more than the tiles
 template <int CG, int BN, int EPI>
@@ -926,12 +913,7 @@ int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_
                       int M, int N, int K, void* C, int ldc, const void* aux, cudaStream_t st, int k_split = 1) {
   using CF = CfgP<CG, BN>;
   auto kern = gemm_tcp_kernel<CG, BN, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem);
-    if (e != cudaSuccess) return (int)e;
-    attr_set = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), CF::kSmem)) return rc;
   const int n_tiles = (N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * k_split;
   int units = sm_count() / CG;
@@ -961,21 +943,16 @@ int launch_persistent(const CUtensorMap& ma, const CUtensorMap& mb, const int32_
 
 template <int EPI>
 int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
-                const void* aux, cudaStream_t st) {
+                const void* aux, int variant, cudaStream_t st) {
   CUtensorMap ma, mb;
   int rc = make_map_2d(&ma, A, (uint64_t)M, (uint64_t)K, 128);
   if (rc) return rc;
   rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
   if (rc) return rc;
   const int pair_tiles = offs ? (M + 255) / 256 + E : (M + 255) / 256;
-  if (g_variant != 3) return launch_persistent<2, 256, EPI>(ma, mb, offs, E, pair_tiles, M, N, K, C, ldc, aux, st);
+  if (variant != 3) return launch_persistent<2, 256, EPI>(ma, mb, offs, E, pair_tiles, M, N, K, C, ldc, aux, st);
   auto kern = gemm_tc2_kernel<EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg2::kSmem);
-    if (e != cudaSuccess) return (int)e;
-    attr_set = true;
-  }
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), Cfg2::kSmem)) return rc;
   const int n_tiles = N / 256;
   kern<<<2 * pair_tiles * n_tiles, kThreads, Cfg2::kSmem, st>>>(ma, mb, offs, E, M, N, K, C, ldc, aux, pair_tiles,
                                                                  n_tiles);
@@ -985,13 +962,13 @@ int launch_pair(const void* A, const void* B, const int32_t* offs, int E, int M,
 
 template <int EPI>
 int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C, int ldc,
-               const void* aux, cudaStream_t st) {
+               const void* aux, int variant, cudaStream_t st) {
   // CTA-pair 256×256 tiles cut the per-SM operand stream by a third; 1-CTA
   // 128-row tiles pad less when M is small or split into experts (~560 rows
   // each at bs 248: measured 0.58 vs 0.51 of peak, profiles/gemm_bench_r1.json).
   const bool pair_ok = (N % 256) == 0;
-  if (pair_ok && (g_variant == 2 || ((g_variant == 0 || g_variant == 3) && offs == nullptr && M >= 1024)))
-    return launch_pair<EPI>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+  if (pair_ok && (variant == 2 || ((variant == 0 || variant == 3) && offs == nullptr && M >= 1024)))
+    return launch_pair<EPI>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
   const int m_tiles = offs ? (M + BM - 1) / BM + E : (M + BM - 1) / BM;
   // prefer the wide tile unless it leaves most SMs idle
   bool wide = (long)m_tiles * ((N + 255) / 256) >= sm_count() || EPI == SO_EPI_SWIGLU && (N % 256) == 0;
@@ -1002,17 +979,17 @@ int launch_epi(const void* A, const void* B, const int32_t* offs, int E, int M, 
   if (wide) {
     rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 256);
     if (rc) return rc;
-    if (g_variant != 3) return launch_persistent<1, 256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
+    if (variant != 3) return launch_persistent<1, 256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
     return launch_bn<256, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
   }
   rc = make_map_3d(&mb, B, (uint64_t)E, (uint64_t)N, (uint64_t)K, 128);
   if (rc) return rc;
-  if (g_variant != 3) return launch_persistent<1, 128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
+  if (variant != 3) return launch_persistent<1, 128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
   return launch_bn<128, EPI>(ma, mb, offs, E, m_tiles, M, N, K, C, ldc, aux, st);
 }
 
 int gemm_dispatch(const void* A, const void* B, const int32_t* offs, int E, int M, int N, int K, void* C,
-                  int ldc, int epi, const void* aux, cudaStream_t st) {
+                  int ldc, int epi, const void* aux, int variant, cudaStream_t st) {
   SO_REQUIRE(A && B && C, SO_E_NULLPTR);
   SO_REQUIRE(M >= 0 && N > 0 && K > 0 && E >= 1, SO_E_SHAPE);
   SO_REQUIRE(K % BK == 0 && N % 32 == 0, SO_E_SHAPE);
@@ -1021,20 +998,22 @@ int gemm_dispatch(const void* A, const void* B, const int32_t* offs, int E, int 
   else if (epi == SO_EPI_F32) SO_REQUIRE(ldc % 4 == 0 && ldc >= N, SO_E_SHAPE);
   else SO_REQUIRE(ldc % 8 == 0 && ldc >= N, SO_E_SHAPE);
   if (epi == SO_EPI_BF16_RESID || epi == SO_EPI_BF16_ROWSCALE) SO_REQUIRE(aux != nullptr, SO_E_NULLPTR);
+  SO_REQUIRE(variant >= 0 && variant <= 3, SO_E_SHAPE);
   if (M == 0) return SO_OK;
   switch (epi) {
-    case SO_EPI_BF16: return launch_epi<SO_EPI_BF16>(A, B, offs, E, M, N, K, C, ldc, aux, st);
-    case SO_EPI_F32: return launch_epi<SO_EPI_F32>(A, B, offs, E, M, N, K, C, ldc, aux, st);
-    case SO_EPI_BF16_RESID: return launch_epi<SO_EPI_BF16_RESID>(A, B, offs, E, M, N, K, C, ldc, aux, st);
-    case SO_EPI_SWIGLU: return launch_epi<SO_EPI_SWIGLU>(A, B, offs, E, M, N, K, C, ldc, aux, st);
-    case SO_EPI_BF16_ROWSCALE: return launch_epi<SO_EPI_BF16_ROWSCALE>(A, B, offs, E, M, N, K, C, ldc, aux, st);
+    case SO_EPI_BF16: return launch_epi<SO_EPI_BF16>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
+    case SO_EPI_F32: return launch_epi<SO_EPI_F32>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
+    case SO_EPI_BF16_RESID: return launch_epi<SO_EPI_BF16_RESID>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
+    case SO_EPI_SWIGLU: return launch_epi<SO_EPI_SWIGLU>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
+    case SO_EPI_BF16_ROWSCALE:
+      return launch_epi<SO_EPI_BF16_ROWSCALE>(A, B, offs, E, M, N, K, C, ldc, aux, variant, st);
     default: return SO_E_UNSUPPORTED;
   }
 }
 
 // Split-K choice for a dense GEMM with few output tiles (0 = not worth it)
-int splitk_factor(int M, int N, int K) {
-  if (M > 256 || g_variant == 3) return 0;
+int splitk_factor(int M, int N, int K, int variant = 0) {
+  if (M > 256 || variant == 3) return 0;
   const int tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
   const int sms = sm_count();
   if (2 * tiles >= sms) return 0;
@@ -1071,15 +1050,18 @@ int launch_splitk(const void* A, const void* B, int M, int N, int K, void* C, in
 }  // namespace
 
 extern "C" size_t so_gemm_workspace_bytes(int M, int N, int K) {
-  const int ks = (M > 0 && N > 0 && K >= BK) ? splitk_factor(M, N, K) : 0;
+  const int ks = (M > 0 && N > 0 && K >= BK) ? splitk_factor(M, N, K, 0) : 0;
   return ks ? (size_t)ks * M * N * sizeof(float) : 0;
 }
 
-extern "C" int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
-                               const void* aux, void* workspace, size_t ws_bytes, void* stream) {
-  const int ks = (M > 0 && N > 0 && K >= BK && K % BK == 0 && N % 128 == 0) ? splitk_factor(M, N, K) : 0;
+extern "C" int so_gemm_bf16_v(const void* A, const void* B, const int32_t* expert_offsets, int E, int M, int N,
+                              int K, void* C, int ldc, int epilogue, const void* aux, void* workspace, size_t ws_bytes,
+                              int variant, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (expert_offsets != nullptr) return gemm_dispatch(A, B, expert_offsets, E, M, N, K, C, ldc, epilogue, aux, variant, st);
+  const int ks = (M > 0 && N > 0 && K >= BK && K % BK == 0 && N % 128 == 0) ? splitk_factor(M, N, K, variant) : 0;
   if (ks == 0 || workspace == nullptr || ws_bytes < (size_t)ks * M * N * sizeof(float))
-    return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, as_stream(stream));
+    return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, variant, st);
   SO_REQUIRE(A && B && C, SO_E_NULLPTR);
   SO_REQUIRE(aligned16(A) && aligned16(B) && aligned16(C) && aligned16(workspace), SO_E_ALIGN);
   if (epilogue == SO_EPI_SWIGLU) SO_REQUIRE(ldc % 8 == 0 && ldc >= N / 2, SO_E_SHAPE);
@@ -1087,7 +1069,6 @@ extern "C" int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K
   else SO_REQUIRE(ldc % 8 == 0 && ldc >= N, SO_E_SHAPE);
   if (epilogue == SO_EPI_BF16_RESID || epilogue == SO_EPI_BF16_ROWSCALE) SO_REQUIRE(aux != nullptr, SO_E_NULLPTR);
   float* ws = reinterpret_cast<float*>(workspace);
-  cudaStream_t st = as_stream(stream);
   switch (epilogue) {
     case SO_EPI_BF16: return launch_splitk<SO_EPI_BF16>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
     case SO_EPI_F32: return launch_splitk<SO_EPI_F32>(A, B, M, N, K, C, ldc, aux, ks, ws, st);
@@ -1098,22 +1079,22 @@ extern "C" int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K
   }
 }
 
+extern "C" int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
+                               const void* aux, void* workspace, size_t ws_bytes, void* stream) {
+  return so_gemm_bf16_v(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, workspace, ws_bytes, 0, stream);
+}
+
 extern "C" int so_gemm_bf16(const void* A, const void* B, int M, int N, int K, void* C, int ldc, int epilogue,
                             const void* aux, void* stream) {
-  return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, as_stream(stream));
+  return gemm_dispatch(A, B, nullptr, 1, M, N, K, C, ldc, epilogue, aux, 0, as_stream(stream));
 }
 
 extern "C" int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_offsets, int E,
                                     int max_rows, int N, int K, void* C, int ldc, int epilogue,
                                     const void* aux, void* stream) {
   SO_REQUIRE(expert_offsets != nullptr, SO_E_NULLPTR);
-  return gemm_dispatch(A, B, expert_offsets, E, max_rows, N, K, C, ldc, epilogue, aux, as_stream(stream));
+  return gemm_dispatch(A, B, expert_offsets, E, max_rows, N, K, C, ldc, epilogue, aux, 0, as_stream(stream));
 }
 
 extern "C" int so_device_sm_count(void) { return sm_count(); }
 
-extern "C" int so_gemm_set_variant(int variant) {
-  SO_REQUIRE(variant >= 0 && variant <= 3, SO_E_SHAPE);
-  g_variant = variant;
-  return SO_OK;
-}

@@ -215,13 +215,7 @@ extern "C" int so_rope_kv_append(const void* qkv, const int32_t* positions, cons
              SO_E_SHAPE);
   SO_REQUIRE(aligned16(qkv) && aligned16(q_out) && aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (T == 0) return SO_OK;
-  static int ctas = 0;
-  if (ctas == 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = 16 * sms;  // 64 warps per SM, grid-stride over the tokens
-  }
+  const int ctas = 16 * device_sm_count();  // 64 warps per SM, grid-stride over the tokens
   const int need = (T + kRopeWarps - 1) / kRopeWarps;
   rope_append_kernel<<<need < ctas ? need : ctas, 32 * kRopeWarps, 0, as_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(qkv), positions, slot_mapping, T, hq, hkv, dh, rope_theta, page_size,

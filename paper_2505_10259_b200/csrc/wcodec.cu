@@ -599,13 +599,7 @@ inline int launch_decode(const so_xc4_header* h, uint32_t f, const uint8_t* fram
   const FrameGeom g = frame_geom(m, bits_of(h));
   uint32_t t[4];
   table_words(h, t);
-  static int ctas = 0;  // 8 resident CTAs (64 warps) per SM, grid-stride over the rest
-  if (ctas == 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = 8 * sms;
-  }
+  const int ctas = 8 * device_sm_count();  // 8 resident CTAs (64 warps) per SM, grid-stride over the rest
   const uint32_t need = (m + kBlock * kWarpsPerCta - 1) / (kBlock * kWarpsPerCta);
   const uint32_t grid = need < (uint32_t)ctas ? need : (uint32_t)ctas;
   uint16_t* out = reinterpret_cast<uint16_t*>(dst_unit) + e_begin;

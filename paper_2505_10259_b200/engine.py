@@ -123,7 +123,7 @@ class DecodeSession:
         # target KV in HBM, or (kv_host, for tiny HBM budgets) in pinned host DRAM
         # with one batch's pages staged per layer (kvcache.HostPagedKVCache)
         self.tkv = (HostPagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size,
-                                     window_seqs=max(b.n for b in self.batches))
+                                     window_seqs=max(b.n for b in self.batches), host_alloc=engine.host_alloc)
                     if kv_host else PagedKVCache(engine.target.arch, n_seq, max_len, dev, engine.page_size))
         # Draft KV policy (planner choice):
         #   cached    one persistent draft KV row per sequence;
@@ -205,6 +205,7 @@ class Engine:
         # the verify stream gets the higher priority: each layer's expert GEMMs
         # must release its window slot promptly or the copy engine idles, while
         # the draft's (re-)prefill work only has to finish by the barrier
+        self.host_alloc = None   # pinned-host allocator for host-resident KV pools (None: torch's)
         self.tgt_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.drf_stream = torch.cuda.Stream(device=self.device, priority=0)
         self.tracer = Tracer(trace)
@@ -360,6 +361,7 @@ class Engine:
                         first_h = first.to("cpu", non_blocking=True)
             else:
                 model.forward(chunks, kv, stream, want_logits=False)
+        s.tkv.join(self.tgt_stream)
         self.tgt_stream.synchronize()
         self.drf_stream.synchronize()
         first_np = first_h.numpy()
@@ -751,9 +753,12 @@ class Engine:
             if err:
                 raise err[0]
             self._tev[1].record(self.drf_stream)
-        # barrier (simulator.py:209-211): device-side join, then the host reads counts
+        # barrier (simulator.py:209-211): device-side join, then the host reads counts.
+        # Host-resident KV: the last layers' write-backs (d2h stream) join too, so
+        # no DMA into the pinned pool outlives the round and its time is counted.
         self._join.record(self.drf_stream)
         self._join.wait(self.tgt_stream)
+        s.tkv.join(self.tgt_stream)
         bev = self.tracer.mark(self.tgt_stream)
         self.tracer.add("GPU_TARGET", "barrier", bev, bev, rnd=rnd)
         native.stream_synchronize(self.tgt_stream)

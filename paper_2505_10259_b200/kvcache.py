@@ -56,6 +56,9 @@ class PagedKVCache:
     def set_window(self, lo_seq: int, hi_seq: int) -> None:
         """All sequences are always resident."""
 
+    def join(self, stream) -> None:
+        """Make ``stream`` wait for every copy this cache issued (HBM pools: none)."""
+
 
 class HostPagedKVCache(PagedKVCache):
     """Target KV in pinned host DRAM, one verified batch's pages staged per layer.
@@ -157,6 +160,11 @@ class HostPagedKVCache(PagedKVCache):
         for win, pool in ((self.wk[w], self.k), (self.wv[w], self.v)):
             self._native.memcpy_async(pool[li, self.base].data_ptr(), win.data_ptr(), n, self.d2h)
         self.written[w].record(self.d2h)
+
+    def join(self, stream) -> None:
+        """``stream`` waits for both window slots' last write-back (d2h stream)."""
+        for ev in self.written:
+            ev.wait(stream)
 
     def fill_random(self, g: torch.Generator, device) -> None:
         """Synthetic prompt KV (decode benchmarks), generated on the GPU per layer."""

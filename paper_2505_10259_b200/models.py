@@ -88,13 +88,29 @@ class ForwardBatch:
 class CausalLM:
     """Shared forward of the target and the draft."""
 
-    def __init__(self, weights: ModelWeights, device, streamer=None):
+    ARITH = ("tensor", "canonical")
+
+    def __init__(self, weights: ModelWeights, device, streamer=None, arith: str = "tensor"):
+        """``arith="tensor"``: the product kernels (tcgen05 GEMMs, mma.sync
+        attention).  ``"canonical"``: the parity mode — the same ops at the
+        same bf16 rounding points in a fixed IEEE order (csrc/canon.cu) that
+        the CPU oracle reproduces bit for bit; CUDA-core code for tiny shapes."""
+        if arith not in self.ARITH:
+            raise ValueError(f"arith must be one of {self.ARITH}, got {arith!r}")
         self.w = weights
         self.arch: ModelArch = weights.arch
         self.device = torch.device(device)
         self.streamer = streamer
         self.ws = Workspace(device)
         self.hooks = None  # optional callback(layer, phase, stream) used by the tracer
+        self.arith = arith
+        canon = arith == "canonical"
+        self._gemm = native.canon_gemm if canon else native.gemm
+        self._gemm_grouped = native.canon_gemm_grouped if canon else native.gemm_grouped
+        self._rmsnorm = native.canon_rmsnorm if canon else native.rmsnorm
+        self._attn = native.canon_attn_paged if canon else native.attn_paged
+        self._router = native.canon_router_top2 if canon else native.router_top2
+        self._rope_table = None  # canonical RoPE: host-computed cos/sin rows, grown to the KV capacity
 
     def spec(self):
         return self.arch.spec()
@@ -140,14 +156,13 @@ class CausalLM:
                 T = c.T
                 x = xa[c.row0:c.row0 + T]
                 out = x  # in place (see above)
-                native.rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
-                native.gemm(xn[:T], wqkv, qkv[:T], native.EPI_BF16, None, stream)
-                native.rope_kv_append(qkv[:T], c.positions, c.slots, hq, hkv, dh, a.rope_theta, kv.page_size,
-                                      q[:T], kc, vc, stream)
-                native.attn_paged(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
-                                  kv.page_size, scale, att[:T], stream)
-                native.gemm(att[:T], wo, h[:T], native.EPI_BF16_RESID, x, stream)
-                native.rmsnorm(h[:T], L.ffn_norm, xn[:T], a.eps, stream)
+                self._rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
+                self._gemm(xn[:T], wqkv, qkv[:T], native.EPI_BF16, None, stream)
+                self._rope(kv, qkv[:T], c.positions, c.slots, q[:T], kc, vc, stream)
+                self._attn(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
+                           kv.page_size, scale, att[:T], stream)
+                self._gemm(att[:T], wo, h[:T], native.EPI_BF16_RESID, x, stream)
+                self._rmsnorm(h[:T], L.ffn_norm, xn[:T], a.eps, stream)
                 if ci == 0:
                     if base is None:
                         base = self._ffn_acquire(li, L, stream)
@@ -173,11 +188,23 @@ class CausalLM:
             x = rows
         R = x.shape[0]
         xf = ws.get("xf", (R, H), torch.bfloat16)
-        native.rmsnorm(x, self.w.final_norm, xf, a.eps, stream)
+        self._rmsnorm(x, self.w.final_norm, xf, a.eps, stream)
         if logits_out is None:
             logits_out = ws.get("logits", (R, a.vocab), torch.float32)
-        native.gemm(xf, self.w.lm_head, logits_out, native.EPI_F32, None, stream)
+        self._gemm(xf, self.w.lm_head, logits_out, native.EPI_F32, None, stream)
         return logits_out
+
+    def _rope(self, kv, qkv, positions, slots, q, kc, vc, stream):
+        a = self.arch
+        if self.arith == "tensor":
+            native.rope_kv_append(qkv, positions, slots, a.n_head, a.n_kv_head, a.head_dim, a.rope_theta,
+                                  kv.page_size, q, kc, vc, stream)
+            return
+        rows = kv.pages_per_seq * kv.page_size  # every position a sequence of this cache can hold
+        if self._rope_table is None or self._rope_table.shape[0] < rows:
+            self._rope_table = torch.from_numpy(rope_table(a.head_dim, a.rope_theta, rows)).to(self.device)
+        native.canon_rope_kv_append(qkv, positions, slots, a.n_head, a.n_kv_head, a.head_dim, self._rope_table,
+                                    kv.page_size, q, kc, vc, stream)
 
     # ------------------------------------------------------------------
     def _ffn_acquire(self, li, L, stream) -> int:
@@ -201,10 +228,10 @@ class CausalLM:
         act = ws.get("act", (rows, I), torch.bfloat16)
         y = ws.get("y", (rows, H), torch.bfloat16)
         rws = ws.get("router_ws", (native.router_workspace_bytes(T, E),), torch.uint8)
-        native.router_top2(xn, L.router, offs, perm, roww, trows, xperm, rws, stream=stream)
+        self._router(xn, L.router, offs, perm, roww, trows, xperm, rws, stream=stream)
         gu_elems, _, _ = ffn_offsets(a)
-        native.gemm_grouped(xperm, base, offs, E, 2 * I, act, native.EPI_SWIGLU, None, stream)
-        native.gemm_grouped(act, base + 2 * gu_elems, offs, E, H, y, native.EPI_BF16_ROWSCALE, roww, stream)
+        self._gemm_grouped(xperm, base, offs, E, 2 * I, act, native.EPI_SWIGLU, None, stream)
+        self._gemm_grouped(act, base + 2 * gu_elems, offs, E, H, y, native.EPI_BF16_ROWSCALE, roww, stream)
         native.moe_combine(y, trows, h, out, stream)
 
     def _mlp(self, base, xn, h, out, T, stream):
@@ -214,8 +241,19 @@ class CausalLM:
         gu_elems, _, _ = ffn_offsets(a)
         gu = _raw_bf16(base, (2 * I, H), self.device)
         dn = _raw_bf16(base + 2 * gu_elems, (H, I), self.device)
-        native.gemm(xn, gu, act, native.EPI_SWIGLU, None, stream)
-        native.gemm(act, dn, out, native.EPI_BF16_RESID, h, stream)
+        self._gemm(xn, gu, act, native.EPI_SWIGLU, None, stream)
+        self._gemm(act, dn, out, native.EPI_BF16_RESID, h, stream)
+
+
+def rope_table(dh: int, theta: float, rows: int):
+    """cos/sin rows of the canonical RoPE: [rows, dh] fp32, cos(p·f_i) in columns
+    [0, dh/2), sin(p·f_i) in [dh/2, dh), f_i = θ^(−2i/dh) — evaluated in float64
+    on the host and rounded once (setup-time constants of the parity mode)."""
+    import numpy as np
+
+    inv = 1.0 / theta ** (np.arange(0, dh, 2, dtype=np.float64) / dh)
+    ang = np.arange(rows, dtype=np.float64)[:, None] * inv[None, :]
+    return np.concatenate([np.cos(ang), np.sin(ang)], axis=1).astype(np.float32)
 
 
 class _RawView:

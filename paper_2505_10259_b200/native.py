@@ -33,8 +33,6 @@ _SIGNATURES = {
     "so_status_string": (ctypes.c_char_p, [c_int]),
     "so_device_sm_count": (c_int, []),
     "so_set_device": (c_int, [c_int]),
-    "so_gemm_set_variant": (c_int, [c_int]),
-    "so_attn_set_variant": (c_int, [c_int]),
     "so_accept_greedy": (c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_accept_sample": (c_int, [_P, _P, _P, _P, _P, _P, c_float, c_int, c_int, c_int, _P, _P, _P]),
     "so_sample_tokens": (c_int, [_P, c_int64, _P, c_float, c_int, c_int, _P, c_int64, _P, c_int64, _P]),
@@ -45,11 +43,20 @@ _SIGNATURES = {
     "so_gemm_workspace_bytes": (c_size_t, [c_int, c_int, c_int]),
     "so_gemm_bf16_ex": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, _P]),
     "so_gemm_grouped_bf16": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
+    "so_gemm_bf16_v": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, c_int, _P]),
     "so_embed": (c_int, [_P, _P, c_int, c_int, _P, _P]),
     "so_rmsnorm": (c_int, [_P, _P, c_int, c_int, c_float, _P, _P]),
     "so_rope_kv_append": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_float, c_int, _P, _P, _P, _P]),
     "so_attn_paged": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
                               c_float, _P, _P]),
+    "so_attn_paged_v": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
+                                c_float, _P, c_int, _P]),
+    "so_canon_gemm": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
+    "so_canon_rmsnorm": (c_int, [_P, _P, c_int, c_int, c_float, _P, _P]),
+    "so_canon_rope_kv_append": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, _P, _P]),
+    "so_canon_attn_paged": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
+                                    c_float, _P, _P]),
+    "so_canon_router_top2": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "so_stream_layer": (c_int, [_P, _P, c_size_t, c_size_t, _P, _P]),
     "so_event_create": (c_int, [c_int, ctypes.POINTER(c_void_p)]),
     "so_event_destroy": (c_int, [_P]),
@@ -73,8 +80,7 @@ _SIGNATURES = {
 }
 
 _PLUMBING = {"so_event_create", "so_event_destroy", "so_event_record", "so_stream_wait_event", "so_event_synchronize",
-             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device", "so_gemm_set_variant",
-             "so_attn_set_variant"}
+             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device"}
 
 
 def library_path() -> str:
@@ -104,7 +110,7 @@ def exported_symbols() -> list[str]:
 
 # kernels (or copy-engine DMA batches) each entry point enqueues; summed into
 # ``launches`` so bench.py can report how many of our kernels ran
-_KERNELS_PER_CALL = {"so_router_top2": 3, "so_stream_layer": 0, "so_xc4_encode": 5}
+_KERNELS_PER_CALL = {"so_router_top2": 3, "so_canon_router_top2": 3, "so_stream_layer": 0, "so_xc4_encode": 5}
 launches = {"kernels": 0, "copies": 0}
 _count_lock = threading.Lock()  # the verify and draft streams are enqueued from two threads
 
@@ -113,16 +119,6 @@ def reset_launch_counter() -> None:
     with _count_lock:
         launches["kernels"] = 0
         launches["copies"] = 0
-
-
-def gemm_set_variant(variant: int) -> None:
-    """0 = auto, 1 = 1-CTA tiles only, 2 = CTA-pair (cta_group::2) tiles wherever legal."""
-    _check(lib().so_gemm_set_variant(variant), "so_gemm_set_variant")
-
-
-def attn_set_variant(variant: int) -> None:
-    """0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging."""
-    _check(lib().so_attn_set_variant(variant), "so_attn_set_variant")
 
 
 def set_device(index: int) -> None:
@@ -241,28 +237,30 @@ def _gemm_workspace(M: int, N: int, K: int, stream: int, device) -> tuple[int, i
     return ws.data_ptr(), ws.numel()
 
 
-def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None):
-    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (skinny shapes: split-K over the SMs)."""
+def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
+    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (skinny shapes: split-K over the SMs).
+    ``variant``: tile choice (0 = auto; see so_gemm_bf16_v) — tests and benchmarks only."""
     M, K = a.shape
     N = b.shape[-2]
     assert b.shape[-1] == K
     _need(a, torch.bfloat16, "a")
     assert b.dtype == torch.bfloat16
     st = _stream(stream)
-    ws, ws_bytes = _gemm_workspace(M, N, K, st, a.device)
-    _check(lib().so_gemm_bf16_ex(_ptr(a), _ptr(b), M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux), ws,
-                                 ws_bytes, st), "so_gemm_bf16")
+    ws, ws_bytes = _gemm_workspace(M, N, K, st, a.device) if variant != 3 else (0, 0)
+    _check(lib().so_gemm_bf16_v(_ptr(a), _ptr(b), None, 1, M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux), ws,
+                                ws_bytes, variant, st), "so_gemm_bf16")
     if ws:
         with _count_lock:
             launches["kernels"] += 1  # the split-K reduce
 
 
-def gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None, stream=None):
+def gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None, stream=None,
+                 variant: int = 0):
     """Grouped expert GEMM; ``b_ptr`` addresses [E, N, K] bf16 weights (e.g. a window slot)."""
     rows, K = a.shape
     _need(a, torch.bfloat16, "a")
-    _check(lib().so_gemm_grouped_bf16(_ptr(a), b_ptr, _ptr(expert_offsets), E, rows, N, K, _ptr(out),
-                                      out.stride(0), epilogue, _ptr(aux), _stream(stream)), "so_gemm_grouped_bf16")
+    _check(lib().so_gemm_bf16_v(_ptr(a), b_ptr, _ptr(expert_offsets), E, rows, N, K, _ptr(out), out.stride(0),
+                                epilogue, _ptr(aux), None, 0, variant, _stream(stream)), "so_gemm_grouped_bf16")
 
 
 # ---------------------------------------------------------------- K8 ---
@@ -288,11 +286,62 @@ def rope_kv_append(qkv, positions, slots, hq, hkv, dh, theta, page_size, q_out, 
 # ---------------------------------------------------------------- K6 ---
 
 def attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, hkv, dh, page_size, scale, out,
-               stream=None):
+               stream=None, variant: int = 0):
+    """``variant`` 0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging."""
     bs = kv_before.numel()
-    _check(lib().so_attn_paged(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
-                               _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,
-                               _ptr(out), _stream(stream)), "so_attn_paged")
+    _check(lib().so_attn_paged_v(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
+                                 _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,
+                                 _ptr(out), variant, _stream(stream)), "so_attn_paged")
+
+
+# ------------------------------------------- canonical-order arithmetic ---
+# Parity mode (csrc/canon.cu): the same ops as the kernels above in a fixed
+# IEEE evaluation order that oracle/csrc/canon_oracle.c restates bit for bit.
+
+def canon_gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None):
+    M, K = a.shape
+    N = b.shape[-2]
+    _check(lib().so_canon_gemm(_ptr(a), _ptr(b), None, 0, M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux),
+                               _stream(stream)), "so_canon_gemm")
+
+
+def canon_gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None,
+                       stream=None):
+    rows, K = a.shape
+    _check(lib().so_canon_gemm(_ptr(a), b_ptr, _ptr(expert_offsets), E, rows, N, K, _ptr(out), out.stride(0),
+                               epilogue, _ptr(aux), _stream(stream)), "so_canon_gemm")
+
+
+def canon_rmsnorm(x, w, out, eps, stream=None):
+    T, H = x.shape
+    _check(lib().so_canon_rmsnorm(_ptr(x), _ptr(w), T, H, eps, _ptr(out), _stream(stream)), "so_canon_rmsnorm")
+
+
+def canon_rope_kv_append(qkv, positions, slots, hq, hkv, dh, table, page_size, q_out, k_cache, v_cache,
+                         stream=None):
+    """``table`` [rows, dh] fp32: cos(p·f_i) in columns [0, dh/2), sin in [dh/2, dh)."""
+    T = qkv.shape[0]
+    _need(table, torch.float32, "table")
+    _check(lib().so_canon_rope_kv_append(_ptr(qkv), _ptr(positions), _ptr(slots), T, hq, hkv, dh, _ptr(table),
+                                         table.shape[0], page_size, _ptr(q_out), _ptr(k_cache), _ptr(v_cache),
+                                         _stream(stream)), "so_canon_rope_kv_append")
+
+
+def canon_attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, hkv, dh, page_size, scale,
+                     out, stream=None):
+    bs = kv_before.numel()
+    _check(lib().so_canon_attn_paged(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
+                                     _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,
+                                     _ptr(out), _stream(stream)), "so_canon_attn_paged")
+
+
+def canon_router_top2(x, w_gate, expert_offsets, perm_token, row_weight, token_rows, x_perm, workspace,
+                      topk_idx=None, topk_w=None, stream=None):
+    T, H = x.shape
+    E = w_gate.shape[0]
+    _check(lib().so_canon_router_top2(_ptr(x), _ptr(w_gate), T, H, E, _ptr(topk_idx), _ptr(topk_w),
+                                      _ptr(expert_offsets), _ptr(perm_token), _ptr(row_weight), _ptr(token_rows),
+                                      _ptr(x_perm), _ptr(workspace), _stream(stream)), "so_canon_router_top2")
 
 
 # ------------------------------------------------------ stream plumbing ---

@@ -102,9 +102,12 @@ class ModelWeights:
 
 
 def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset(),
-                 stream_attn: bool = False, encoder=None) -> ModelWeights:
+                 stream_attn: bool = False, encoder=None, host_alloc=None) -> ModelWeights:
     """Build device weights from logical (HF-shaped) arrays — numpy or torch.
-    With ``encoder`` (codec.Encoder) the streamed units are kept XC4-encoded."""
+    With ``encoder`` (codec.Encoder) the streamed units are kept XC4-encoded.
+    Streamed units go to ``host_alloc(nbytes)`` (e.g. HostStore.alloc: exact-size
+    page-locked mmaps) — torch's pinned allocator would round each unit up to a
+    power of two and cache it (8 GiB per 5 GB 8x22B layer)."""
     dev = torch.device(device)
     layers = []
     host = {}
@@ -117,9 +120,15 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
                 packed = torch.cat([wqkv.reshape(-1), wo.reshape(-1), packed])
                 wqkv = wo = None
             if encoder is not None:
-                host[li] = codec.encode_to_host(packed.to(dev), encoder)
+                host[li] = codec.encode_to_host(packed.to(dev), encoder, host_alloc)
+            elif dev.type != "cuda":
+                host[li] = packed
+            elif host_alloc is not None:
+                buf = host_alloc(packed.numel() * 2).view(torch.bfloat16)[: packed.numel()]
+                buf.copy_(packed)
+                host[li] = buf
             else:
-                host[li] = packed.pin_memory() if dev.type == "cuda" else packed
+                host[li] = packed.pin_memory()
             ffn = None
         else:
             ffn = packed.to(dev)

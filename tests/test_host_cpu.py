@@ -122,10 +122,18 @@ def test_disk_tier_file_round_trip(tmp_path):
     d.close()
 
 
-def test_package_sets_one_work_queue_per_stream():
-    """Importing the package reserves a hardware work queue per stream before the
-    CUDA context exists (mitigation for the host-KV + refill stall)."""
+def test_import_changes_no_process_state_and_work_queues_are_explicit():
+    """Importing the package leaves CUDA_DEVICE_MAX_CONNECTIONS alone (other
+    frameworks pin it); reserve_work_queues() sets it only when unset and only
+    before the CUDA context exists."""
     import os
+    import subprocess
+    import sys
 
-    import paper_2505_10259_b200  # noqa: F401
-    assert int(os.environ["CUDA_DEVICE_MAX_CONNECTIONS"]) >= 16
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    code = ("import os, paper_2505_10259_b200 as p; assert 'CUDA_DEVICE_MAX_CONNECTIONS' not in os.environ; "
+            "assert p.reserve_work_queues(32); assert os.environ['CUDA_DEVICE_MAX_CONNECTIONS'] == '32'; "
+            "assert not p.reserve_work_queues(16); assert os.environ['CUDA_DEVICE_MAX_CONNECTIONS'] == '32'")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -176,10 +176,9 @@ def test_moe_combine():
 @pytest.fixture(params=[1, 2, 3], ids=["cta1", "cta_pair", "one_tile_per_cta"])
 def gemm_variant(request):
     """Run each GEMM test on the persistent 1-CTA tiles, the persistent cta_group::2
-    pair tiles, and the non-persistent one-tile-per-CTA kernels."""
-    native.gemm_set_variant(request.param)
-    yield request.param
-    native.gemm_set_variant(0)
+    pair tiles, and the non-persistent one-tile-per-CTA kernels (an explicit
+    per-call argument: the library keeps no variant state)."""
+    return request.param
 
 
 def _bf16_close(got, want, rel=1.5e-2):
@@ -198,14 +197,14 @@ def test_gemm_dense(M, N, K, gemm_variant):
     b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
     ref = a.float() @ b.float().T
     out = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
-    native.gemm(a, b, out)
+    native.gemm(a, b, out, variant=gemm_variant)
     _bf16_close(out, ref)
     out32 = torch.empty(M, N, dtype=torch.float32, device=DEV)
-    native.gemm(a, b, out32, native.EPI_F32)
+    native.gemm(a, b, out32, native.EPI_F32, variant=gemm_variant)
     torch.testing.assert_close(out32, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
     r = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
     outr = torch.empty_like(out)
-    native.gemm(a, b, outr, native.EPI_BF16_RESID, r)
+    native.gemm(a, b, outr, native.EPI_BF16_RESID, r, variant=gemm_variant)
     _bf16_close(outr, ref.to(torch.bfloat16).float() + r.float())
 
 
@@ -219,7 +218,7 @@ def test_gemm_swiglu(M, I, K, gemm_variant):
 
     b = interleave_gate_up(wg, wu).contiguous()
     out = torch.empty(M, I, dtype=torch.bfloat16, device=DEV)
-    native.gemm(a, b, out, native.EPI_SWIGLU)
+    native.gemm(a, b, out, native.EPI_SWIGLU, variant=gemm_variant)
     gate = a.float() @ wg.float().T
     up = a.float() @ wu.float().T
     _bf16_close(out, torch.nn.functional.silu(gate) * up)
@@ -236,7 +235,7 @@ def test_gemm_grouped(counts, gemm_variant, N=256):
     offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=DEV)
     w = torch.rand(rows, device=DEV, generator=g)
     out = torch.zeros(rows, N, dtype=torch.bfloat16, device=DEV)
-    native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, native.EPI_BF16_ROWSCALE, w)
+    native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, native.EPI_BF16_ROWSCALE, w, variant=gemm_variant)
     ref = torch.zeros(rows, N, device=DEV)
     o = offs.cpu().numpy()
     for e in range(E):
@@ -326,14 +325,10 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
 ])
 @pytest.mark.parametrize("attn_variant", [0, 1], ids=["tma", "cp_async"])
 def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
-    native.attn_set_variant(attn_variant)
-    try:
-        _check_attn(dh, hq, hkv, qlens, kvbs, ps)
-    finally:
-        native.attn_set_variant(0)
+    _check_attn(dh, hq, hkv, qlens, kvbs, ps, attn_variant)
 
 
-def _check_attn(dh, hq, hkv, qlens, kvbs, ps):
+def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):
     bs = len(qlens)
     max_len = max(q + k for q, k in zip(qlens, kvbs))
     pps = (max_len + ps - 1) // ps + 1
@@ -357,7 +352,7 @@ def _check_attn(dh, hq, hkv, qlens, kvbs, ps):
     T = sum(qlens)
     q = torch.randn(T, hq * dh, device=DEV, generator=g).to(torch.bfloat16)
     out = torch.empty(T, hq * dh, dtype=torch.bfloat16, device=DEV)
-    native.attn_paged(q, kc, vc, bt, qs, kvb, max(qlens), hq, hkv, dh, ps, 1 / math.sqrt(dh), out)
+    native.attn_paged(q, kc, vc, bt, qs, kvb, max(qlens), hq, hkv, dh, ps, 1 / math.sqrt(dh), out, variant=variant)
     ref = _attn_ref(q, kc, vc, bt.long().cpu().numpy(), qs.cpu().numpy(), kvb.cpu().numpy(), hq, hkv, dh, ps)
     # P is rounded to bf16 for the PV product: |err| ≤ 2e-2 absolute on O(1) outputs
     torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=2e-2)
@@ -374,14 +369,14 @@ def test_gemm_splitk_skinny(M, N, K):
     b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
     ref = a.float() @ b.float().T
     out = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
-    native.gemm(a, b, out)
+    native.gemm(a, b, out, variant=gemm_variant)
     _bf16_close(out, ref)
     out32 = torch.empty(M, N, dtype=torch.float32, device=DEV)
-    native.gemm(a, b, out32, native.EPI_F32)
+    native.gemm(a, b, out32, native.EPI_F32, variant=gemm_variant)
     torch.testing.assert_close(out32, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
     r = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
     outr = torch.empty_like(out)
-    native.gemm(a, b, outr, native.EPI_BF16_RESID, r)
+    native.gemm(a, b, outr, native.EPI_BF16_RESID, r, variant=gemm_variant)
     _bf16_close(outr, ref.to(torch.bfloat16).float() + r.float())
     from paper_2505_10259_b200.weights import interleave_gate_up
 

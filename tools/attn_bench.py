@@ -24,7 +24,7 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 
 
-def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20):
+def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20, variant=0):
     dev = "cuda:0"
     q_len = n + 1
     max_len = ctx + q_len
@@ -38,7 +38,8 @@ def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20):
     kvb = torch.full((bs,), ctx, dtype=torch.int32, device=dev)
     q = torch.randn(bs * q_len, hq * dh, device=dev, generator=g).to(torch.bfloat16)
     out = torch.empty_like(q)
-    f = lambda: native.attn_paged(q, kc, vc, bt, qs, kvb, q_len, hq, hkv, dh, ps, 1 / math.sqrt(dh), out)  # noqa
+    f = lambda: native.attn_paged(q, kc, vc, bt, qs, kvb, q_len, hq, hkv, dh, ps, 1 / math.sqrt(dh), out,
+                                      variant=variant)  # noqa
     for _ in range(3):
         f()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -55,8 +56,7 @@ def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20):
 
 if __name__ == "__main__":
     for variant, label in ((1, "cp_async"), (0, "tma")):
-        native.attn_set_variant(variant)
-        for r in [run(), run(bs=128, n=4), run(bs=248, n=8, ctx=2000), run(bs=472, n=8, ctx=520),
-                  run(bs=64, n=519, ctx=1, hq=32, hkv=8)]:
+        for r in [run(variant=variant), run(bs=128, n=4, variant=variant), run(bs=248, n=8, ctx=2000, variant=variant),
+                  run(bs=472, n=8, ctx=520, variant=variant), run(bs=64, n=519, ctx=1, hq=32, hkv=8, variant=variant)]:
             r["staging"] = label
             print(json.dumps(r))

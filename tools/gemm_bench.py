@@ -75,24 +75,22 @@ def main():
             cnt = np.full(E, M // E)
             cnt[: M - cnt.sum()] += 1
             offs = torch.tensor(np.concatenate([[0], np.cumsum(cnt)]), dtype=torch.int32, device=DEV)
-            fn = lambda: native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, epi, aux)  # noqa: E731
+            fn = lambda v: native.gemm_grouped(a, b.data_ptr(), offs, E, N, out, epi, aux, variant=v)  # noqa: E731
         else:
-            fn = lambda: native.gemm(a, b, out, epi, aux)  # noqa: E731
+            fn = lambda v: native.gemm(a, b, out, epi, aux, variant=v)  # noqa: E731
         flops = 2.0 * M * N * K
         res = {"shape": name, "M": M, "N": N, "K": K}
         variants = ((3, "tile_per_cta_auto"), (0, "persistent_auto"), (1, "cta1"), (2, "cta_pair"))
         best = {}
         for _ in range(3):  # interleaved trials, best of 3 (clocks drift under the power cap)
             for variant, label in variants:
-                native.gemm_set_variant(variant)
-                t = timed(fn, reps=20)
+                t = timed(lambda: fn(variant), reps=20)
                 best[label] = min(best.get(label, t), t)
         wbytes = max(E, 1) * N * K * 2  # weight bytes each launch streams (decode steps are bound by these)
         for _, label in variants:
             t = best[label]
             res[label] = {"ms": t * 1e3, "tflops": flops / t / 1e12, "frac_of_peak": flops / t / 1e12 / PEAK,
                           "weight_GBps": wbytes / t / 1e9}
-        native.gemm_set_variant(0)
         rows.append(res)
         print(json.dumps(res), flush=True)
         del a, b, out, aux

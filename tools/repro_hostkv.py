@@ -10,6 +10,9 @@ completed.  Cause unconfirmed.
 import os, sys, time, faulthandler
 sys.path.insert(0, os.getcwd())
 faulthandler.dump_traceback_later(90, repeat=True)
+import paper_2505_10259_b200
+if os.environ.get("SO_WORK_QUEUES", "32") != "default":
+    paper_2505_10259_b200.reserve_work_queues(int(os.environ.get("SO_WORK_QUEUES", "32")))
 import numpy as np, torch
 from paper_2505_10259_b200 import PAIRS, Policy
 from paper_2505_10259_b200.api import build_engine
