@@ -63,6 +63,10 @@ int so_event_synchronize(void* event);
 int so_event_elapsed_ms(void* start, void* end, float* ms);
 int so_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 int so_stream_synchronize(void* stream);
+/* Non-blocking probes (0 = complete, 600 = cudaErrorNotReady) for stall
+ * diagnostics (tools/stall_probe.py). */
+int so_stream_query(void* stream);
+int so_event_query(void* event);
 /* Small transfer (KBs) between pinned host memory and HBM done by SMs over
  * UVA, so per-round metadata never queues behind layer copies on the copy
  * engine. */

@@ -101,3 +101,18 @@ PAIRS = {
     "8x7b": (MIXTRAL_8X7B, MISTRAL_7B),
     "8x22b": (MIXTRAL_8X22B, MISTRAL_7B_V3),
 }
+
+
+def arch_for_spec(spec) -> ModelArch | None:
+    """The architecture whose byte accounting is ``spec`` (any object with the
+    reference ModelSpec's fields), or None for a shape this package does not
+    know.  Matches on the byte fields, preferring an equal name (Mistral-7B
+    and its v0.3 vocabulary differ only in the embedding bytes anyway)."""
+    if isinstance(spec, ModelArch):
+        return spec
+    keys = ("n_layer", "attn_bytes_per_layer", "ffn_bytes_per_layer", "other_bytes", "kv_bytes_per_token_per_layer")
+    want = tuple(getattr(spec, k, None) for k in keys)
+    hits = [a for a in (MIXTRAL_8X22B, MIXTRAL_8X7B, MISTRAL_7B_V3, MISTRAL_7B, TINY_TARGET, TINY_DRAFT)
+            if tuple(getattr(a.spec(), k) for k in keys) == want]
+    named = [a for a in hits if a.name == getattr(spec, "name", None)]
+    return (named or hits or [None])[0]

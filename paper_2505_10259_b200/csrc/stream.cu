@@ -76,6 +76,15 @@ extern "C" int so_memcpy_async(void* dst, const void* src, size_t bytes, void* s
 
 extern "C" int so_stream_synchronize(void* stream) { return (int)cudaStreamSynchronize(as_stream(stream)); }
 
+// Non-blocking status probes (0 = all work done, 600 = cudaErrorNotReady):
+// diagnostics of a stalled pipeline read which stream / event is pending.
+extern "C" int so_stream_query(void* stream) { return (int)cudaStreamQuery(as_stream(stream)); }
+
+extern "C" int so_event_query(void* event) {
+  SO_REQUIRE(event, SO_E_NULLPTR);
+  return (int)cudaEventQuery(reinterpret_cast<cudaEvent_t>(event));
+}
+
 // Small host↔device transfers executed by SMs over UVA (zero-copy) instead of
 // the copy engine.  The H2D copy engine is busy streaming 4.8 GB layers whose
 // copies are gated on the verify's slot releases; a metadata copy queued

@@ -206,6 +206,10 @@ class Engine:
         # must release its window slot promptly or the copy engine idles, while
         # the draft's (re-)prefill work only has to finish by the barrier
         self.host_alloc = None   # pinned-host allocator for host-resident KV pools (None: torch's)
+        # acceptance probability generate(policy=None) plans with (the reference ships none:
+        # presets.py:16-19 — typical well-matched drafts measure 0.6-0.9)
+        self.acceptance_p = 0.7
+        self.last_policy = None
         self.tgt_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.drf_stream = torch.cuda.Stream(device=self.device, priority=0)
         self.tracer = Tracer(trace)
@@ -240,7 +244,8 @@ class Engine:
         if st is not None and self.tracer.enabled and self.tracer.t0 is not None:
             for k, layer, a, b in st.copy_marks:
                 if a is not None and b is not None:
-                    self.tracer.add("IO_C2G", "ffn_load", a, b, None, layer, None)
+                    rnd, bi = st.use_tags.pop(k, (None, None))
+                    self.tracer.add("IO_C2G", "ffn_load", a, b, bi, layer, rnd)
             st.copy_marks.clear()
         return self.tracer.resolve()
 
@@ -609,7 +614,11 @@ class Engine:
             lo = hi
         if len(chunks) > 1 or nn:
             chunks[0].last_rows = self._up(np.concatenate(last), st)
+        if self.target.streamer is not None:
+            self.target.streamer.pass_tag = (rnd, bi)
         logits = self.target.forward(chunks, s.tkv, st)
+        if self.target.streamer is not None:
+            self.target.streamer.pass_tag = None
         ev1 = tr.mark(st)
         if na:
             out_tok = self.target.ws.get("acc_tok", (na, n + 1), torch.int32)
@@ -795,9 +804,10 @@ class Engine:
         finish: no straggler rounds and no separate prefill
         pass; otherwise every prompt is prefilled layer-major first."""
         S = len(prompts)
-        if policy is None:
-            policy = Policy(bs_prefill=min(S, 2 * ((S + 1) // 2)), bs_decoding=(S + 1) // 2,
-                            bs_draft=(S + 1) // 2, n_cand=4)
+        if policy is None:  # the reference's planner picks it (planner.py:161-184)
+            p = forced_p if forced_p is not None else self.acceptance_p
+            policy = self.plan_policy(S, max(len(q) for q in prompts), max_new_tokens, p)
+            self.last_policy = policy
         max_len = max(len(p) for p in prompts) + max_new_tokens + policy.n_cand + 2
         if refill is None:
             refill = S > 2 * policy.bs_decoding
@@ -818,6 +828,45 @@ class Engine:
             self.decode(s)
         self.last_session = s
         return [o[:max_new_tokens] for o in s.out]
+
+    def b200_profile(self, l_input: int):
+        """``self.hw``, or a B200 HardwareProfile of this device for the pair
+        (presets.b200_profile): HBM = the device's total, host = MemAvailable,
+        the streamed units' encoded/raw ratio when they are XC4-coded."""
+        if self.hw is not None:
+            return self.hw
+        from .presets import b200_profile
+
+        _, total = torch.cuda.mem_get_info(self.device)
+        host = 0
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable"):
+                    host = int(line.split()[1]) * 1024
+        st = self.target.streamer
+        ratio = 1.0
+        if st is not None and st.coded and st.host:
+            units = [u for u in st.host.values() if hasattr(u, "ratio")]
+            ratio = max((u.ratio for u in units), default=1.0)
+        return b200_profile(self.target.arch, self.draft.arch, ctx=l_input, gpu_mem=total, cpu_mem=max(host, 1),
+                            stream_ratio=ratio)
+
+    def plan_policy(self, n_prompts: int, l_input: int, max_new: int, acceptance_p: float, space=None):
+        """``planner.search`` over ``space`` (default: a grid sized to the
+        prompt count) for this pair on ``b200_profile``; returns the best Policy."""
+        from .domain import Workload
+        from .planner import SearchSpace, search
+
+        if space is None:
+            half = max(1, (n_prompts + 1) // 2)
+            bs = sorted({min(half, b) for b in (8, 16, 32, 64, 128, 256, 384, 512)})
+            space = SearchSpace(bs_prefill_values=tuple(sorted({min(n_prompts, 2 * b) for b in bs})),
+                                bs_decoding_values=tuple(bs),
+                                bs_draft_values=tuple(sorted({min(half, b) for b in (8, 16, 32, 64)})),
+                                n_cand_values=(2, 4, 6, 8))
+        wl = Workload(total_sequences=n_prompts, l_input=l_input, max_new_tokens=max_new,
+                      acceptance_p=float(acceptance_p))
+        return search(space, wl, self.b200_profile(l_input), self.target.spec(), self.draft.spec()).best
 
     def run_decoding(self, policy, workload, plan=None, seed: int = 0, acceptance="greedy", prompts=None,
                      max_rounds: int | None = None, draft_kv: str = "cached",

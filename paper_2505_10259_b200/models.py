@@ -272,9 +272,132 @@ def _raw_bf16(ptr: int, shape, device) -> _RawView:
     return _RawView(ptr, shape)
 
 
+class SeqState:
+    """Decoding state of a set of sequences — the ``state`` argument of the
+    model protocol: a paged KV cache, the cache row of each
+    sequence, its committed context length (KV positions [0, ctx) are valid)
+    and its last committed token (position ctx, KV not yet written).
+
+    One state per model: the target's and the draft's rows may differ (the
+    engine gives re-prefilled draft sequences scratch rows)."""
+
+    def __init__(self, kv: PagedKVCache, rows, ctx, t_last, stream: torch.cuda.Stream | None = None):
+        import numpy as np
+
+        self.kv = kv
+        self.rows = np.asarray(rows, np.int64)
+        self.ctx = np.asarray(ctx, np.int64).copy()
+        self.t_last = np.asarray(t_last, np.int32).copy()
+        self.stream = stream
+        if not (self.rows.shape == self.ctx.shape == self.t_last.shape):
+            raise ValueError("rows, ctx and t_last need one entry per sequence")
+
+    @property
+    def bs(self) -> int:
+        return int(self.rows.size)
+
+    def advance(self, counts, tokens) -> None:
+        """Commit ``counts[i]`` tokens ``tokens[i, :counts[i]]`` (accept/reject
+        output, acceptance.py:1-6): the context grows by the count and the last
+        committed token becomes the new t_last.  KV written beyond the new
+        context is stale and is overwritten by the next step at that position."""
+        import numpy as np
+
+        counts = np.asarray(counts, np.int64)
+        tokens = np.asarray(tokens)
+        for i, c in enumerate(counts):
+            if c > 0:
+                self.ctx[i] += c
+                self.t_last[i] = tokens[i, c - 1]
+
+
+def _dev_i32(a, device) -> torch.Tensor:
+    import numpy as np
+
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.int32))).to(device, non_blocking=False)
+
+
+def _step_batch(kv, rows, positions, tokens_dev, device, max_q: int) -> ForwardBatch:
+    """ForwardBatch of ``max_q`` consecutive positions per sequence starting at
+    ``positions[:, 0]`` (verify: t_last + n_cand drafts; draft step: one)."""
+    import numpy as np
+
+    n_seq = rows.size
+    slots = kv.slots(np.broadcast_to(rows[:, None], positions.shape), positions)
+    qs = np.arange(n_seq + 1) * max_q
+    bt = kv.block_table[torch.from_numpy(rows).to(device)]
+    return ForwardBatch(tokens_dev, _dev_i32(positions.ravel(), device), _dev_i32(slots.ravel(), device),
+                        _dev_i32(qs, device), _dev_i32(positions[:, 0], device), bt, n_seq, max_q)
+
+
 class TargetModel(CausalLM):
     """Mixtral-style MoE verifier; FFN layers come through the streamer."""
+
+    def verify(self, state: SeqState, draft_tokens) -> torch.Tensor:
+        """Target logits of t_last and the drafted tokens: ``draft_tokens``
+        [bs, n_cand] → fp32 logits [bs, n_cand + 1, V] (row j scores the token
+        after position ctx + j).  Appends the n_cand + 1
+        positions to the KV cache; the accept/reject step decides how many of
+        them the context keeps (``SeqState.advance``)."""
+        import numpy as np
+
+        dev = self.device
+        st = state.stream or torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st):  # metadata copies ordered before the kernels that read them
+            d = torch.as_tensor(draft_tokens, dtype=torch.int32).to(dev)
+            bs, n = d.shape
+            if bs != state.bs:
+                raise ValueError(f"draft_tokens has {bs} rows, the state {state.bs} sequences")
+            toks = torch.cat([_dev_i32(state.t_last, dev)[:, None], d], dim=1).contiguous()
+            pos = state.ctx[:, None] + np.arange(n + 1)[None, :]
+            fb = _step_batch(state.kv, state.rows, pos, toks.view(-1), dev, n + 1)
+            out = torch.empty((bs * (n + 1), self.arch.vocab), dtype=torch.float32, device=dev)
+            self.forward(fb, state.kv, st, logits_out=out)
+        return out.view(bs, n + 1, self.arch.vocab)
 
 
 class DraftModel(CausalLM):
     """Mistral-style dense drafter, fully HBM-resident."""
+
+    def draft(self, state: SeqState, n_cand: int, bs_draft: int | None = None, uniforms=None,
+              temperature: float = 1.0):
+        """``n_cand`` draft tokens per sequence from cached-KV decode steps, in
+        chunks of ``bs_draft`` sequences (costmodel.py:53-57): tokens
+        [bs, n_cand] int32, greedy; with ``uniforms`` [bs, n_cand] (inverse-CDF
+        sampling at ``temperature``) also the draft distributions
+        [bs, n_cand, V] fp32 the sampling accept step needs.  A last step
+        writes the KV of d_n, so after ``advance`` the cache holds every
+        committed position (no rollback copies)."""
+        import numpy as np
+
+        from . import native
+
+        dev = self.device
+        st = state.stream or torch.cuda.current_stream(dev)
+        bs = state.bs
+        step = bs_draft or bs
+        V = self.arch.vocab
+        with torch.cuda.stream(st):
+            tokens = torch.empty((bs, n_cand), dtype=torch.int32, device=dev)
+            probs = torch.empty((bs, n_cand, V), dtype=torch.float32, device=dev) if uniforms is not None else None
+            u = None if uniforms is None else torch.as_tensor(uniforms, dtype=torch.float32).to(dev).contiguous()
+            logits = torch.empty((step, V), dtype=torch.float32, device=dev)
+            for lo in range(0, bs, step):
+                hi = min(bs, lo + step)
+                rows = state.rows[lo:hi]
+                cur = _dev_i32(state.t_last[lo:hi], dev)
+                for j in range(n_cand + 1):
+                    pos = state.ctx[lo:hi, None] + j
+                    fb = _step_batch(state.kv, rows, pos, cur, dev, 1)
+                    if j == n_cand:
+                        self.forward(fb, state.kv, st, want_logits=False)  # KV of d_n only
+                        break
+                    lg = self.forward(fb, state.kv, st, logits_out=logits[:hi - lo])
+                    out = tokens[lo:hi, j]
+                    if u is None:
+                        native.sample_tokens(lg, out, stream=st)
+                    else:
+                        native.sample_tokens(lg, out, uniforms=u[lo:hi, j].contiguous(), out_probs=probs[lo:hi, j],
+                                             temperature=temperature, stream=st)
+                    cur = out.contiguous()
+        return tokens if probs is None else (tokens, probs)

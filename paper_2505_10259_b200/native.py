@@ -66,6 +66,8 @@ _SIGNATURES = {
     "so_event_elapsed_ms": (c_int, [_P, _P, ctypes.POINTER(c_float)]),
     "so_memcpy_async": (c_int, [_P, _P, c_size_t, _P]),
     "so_stream_synchronize": (c_int, [_P]),
+    "so_stream_query": (c_int, [_P]),
+    "so_event_query": (c_int, [_P]),
     "so_copy_sm": (c_int, [_P, _P, c_size_t, _P]),
     "so_build_verify_tokens": (c_int, [_P, _P, c_int, c_int, c_int, _P, _P, _P]),
     "so_gather_i32": (c_int, [_P, _P, c_int, _P, _P]),
@@ -80,7 +82,8 @@ _SIGNATURES = {
 }
 
 _PLUMBING = {"so_event_create", "so_event_destroy", "so_event_record", "so_stream_wait_event", "so_event_synchronize",
-             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device"}
+             "so_event_elapsed_ms", "so_memcpy_async", "so_stream_synchronize", "so_set_device",
+             "so_stream_query", "so_event_query"}
 
 
 def library_path() -> str:
@@ -372,6 +375,10 @@ class Event:
     def synchronize(self) -> None:
         _check(lib().so_event_synchronize(self.handle), "so_event_synchronize")
 
+    def query(self) -> int:
+        """0 = the last record completed, 600 = pending (never blocks)."""
+        return int(lib().so_event_query(self.handle))
+
     def elapsed_ms(self, end: "Event") -> float:
         ms = c_float()
         _check(lib().so_event_elapsed_ms(self.handle, end.handle, ctypes.byref(ms)), "so_event_elapsed_ms")
@@ -381,6 +388,11 @@ class Event:
         if _lib is not None and getattr(self, "handle", None):
             _lib.so_event_destroy(self.handle)
             self.handle = None
+
+
+def stream_query(stream) -> int:
+    """0 = the stream is idle, 600 = work pending; other values are sticky errors."""
+    return int(lib().so_stream_query(_sp(stream)))
 
 
 def memcpy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream) -> None:

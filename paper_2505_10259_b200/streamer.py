@@ -405,6 +405,11 @@ class LayerStreamer:
         self.nvlink_bytes_issued = 0  # bytes this rank receives in the all-gathers
         self.trace = trace
         self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
+        # (round, batch) of the pass that consumed each use: the engine sets
+        # pass_tag before a verify pass, so a load's trace event carries the
+        # round of its ffn_gpu (the reference's causality check keys on it)
+        self.pass_tag: tuple | None = None
+        self.use_tags: dict[int, tuple] = {}
         if disk is not None:
             disk.start([li for li in self.streamed if isinstance(host.get(li), DiskRef)])
 
@@ -493,6 +498,8 @@ class LayerStreamer:
             return self.resident[layer].data_ptr()
         k = self.k_use
         assert self.streamed[k % len(self.streamed)] == layer, "layers must be consumed in pass order"
+        if self.trace and self.pass_tag is not None:
+            self.use_tags[k] = self.pass_tag
         self._ensure_issued(k + self.n_slots - 1)
         self.loaded[k % self.n_slots].wait(stream)
         return self.slots[k % self.n_slots].data_ptr()
