@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--p", type=float, default=0.8)
     ap.add_argument("--ctx", type=int, default=503)
     ap.add_argument("--bs", type=int, default=0, help="per-batch size (0 = planner)")
-    ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget (0 = MemAvailable − 14 GB)")
+    ap.add_argument("--host-gb", type=float, default=193.0,
+                    help="pinned host budget for streamed units, GB (default 193: 55 XC4 8x22B units on the "
+                         "pool's 196 GiB boxes; lowered to MemAvailable − 12 GB only if the box has less)")
     ap.add_argument("--hbm-gb", type=float, default=0.0, help="HBM budget (0 = device; 8x7b config: 24 GiB cap)")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill", "mixed"), default="auto",
@@ -71,6 +73,7 @@ def parse():
                     help="disk tier budget (§8 f4): streamed units beyond the host budget go to a file")
     ap.add_argument("--disk-path", default="", help="file of the disk tier (default: a temporary file)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-run logits check")
     ap.add_argument("--no-e2e-generate", action="store_true",
                     help="skip the generate() leg (host prompts → prefill → decode → host tokens)")
     ap.add_argument("--e2e-seqs", type=int, default=0,
@@ -161,6 +164,63 @@ def pair(cfg, layers: int = 0):
     return t, d
 
 
+def reference_cpu_work(cfg: str) -> dict:
+    """The reference's own CPU work on this box: its
+    planner ``search`` over the C5 grid at four HBM budgets, its
+    ``simulate_decoding`` of the best policy, and its ``predict_throughput``
+    on the B200 HardwareProfile preset (a model prediction, not a
+    measurement).  Runs the unmodified specpipe installed in baseline/_ref
+    (``__graft_entry__.build`` installs it when /root/reference is present)."""
+    import dataclasses
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "specpipe")):
+        return {"unavailable": "specpipe not installed in baseline/_ref"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import specpipe
+    from specpipe import planner as SP
+    from specpipe import simulator as SS
+
+    from paper_2505_10259_b200 import presets
+
+    name = {"8x22b": "b200_8x22b", "8x7b": "b200_8x7b_24g", "tiny": "b200_tiny"}[cfg]
+    hw_o, t_o, d_o = presets.preset(name)
+    hw = specpipe.HardwareProfile(**hw_o.to_dict())
+    t = specpipe.ModelSpec(**dataclasses.asdict(t_o))
+    d = specpipe.ModelSpec(**dataclasses.asdict(d_o))
+    space = SP.SearchSpace(bs_prefill_values=(64, 128, 256), bs_decoding_values=(32, 64, 128, 256, 384, 512, 640),
+                           bs_draft_values=(16, 32, 64), n_cand_values=(2, 3, 4, 5, 6, 7, 8))
+    wl = specpipe.Workload(total_sequences=2048, l_input=503, max_new_tokens=16, acceptance_p=0.8)
+    out = {"package": f"specpipe {getattr(specpipe, '__version__', '')} (unmodified, baseline/_ref)",
+           "preset": name, "grid_points": len(space.policies()), "search": []}
+    best = None
+    for gib in (24, 48, 96, None):
+        h = hw if gib is None else dataclasses.replace(hw, gpu_mem_capacity=gib * 2**30)
+        t0 = time.perf_counter()
+        try:
+            rk = SP.search(space, wl, h, t, d)
+            res = {"feasible": len(rk.entries), "best": list(rk.best.as_tuple()),
+                   "predicted_tokens_per_s": rk.entries[0][1].throughput}
+            if gib is None:
+                best = rk.best
+        except specpipe.errors.SpecPipeError as exc:
+            res = {"feasible": 0, "error": type(exc).__name__}
+        res.update(hbm_gib=gib or round(hw.gpu_mem_capacity / 2**30, 1), seconds=time.perf_counter() - t0)
+        out["search"].append(res)
+    if best is not None:
+        t0 = time.perf_counter()
+        sim = SS.simulate_decoding(best, SP.rotation_workload(wl, best), hw, t, d, seed=0)
+        out["simulate_decoding"] = {"policy": list(best.as_tuple()), "seconds": time.perf_counter() - t0,
+                                    "events": len(sim.trace), "simulated_tokens_per_s": sim.throughput}
+        bd = SP.predict_throughput(best, wl, hw, t, d)
+        out["predict_throughput"] = {"policy": list(best.as_tuple()), "tokens_per_s": bd.throughput,
+                                     "t_target_per_round_s": bd.t_target_per_round,
+                                     "note": "the reference's cost model on the B200 preset (CPU attention, "
+                                             "no prefetch-ahead): a prediction, not a measurement"}
+    return out
+
+
 def run_reference(args, rank: int) -> None:
     """--impl reference: the CPU port of the path (oracle) on the host cores."""
     if rank != 0:
@@ -168,21 +228,32 @@ def run_reference(args, rank: int) -> None:
     from oracle import cpu_baseline
 
     tgt, drf = pair(args.config)
-    vals = []
+    vals, samples = [], []
     cache: dict = {}  # weights built once; every step times the sampled forward passes
     for i in range(args.warmup + args.steps):
         r = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4, seed=i, cache=cache)
         if i >= args.warmup:
             vals.append(r.tokens_per_s)
+            samples.append(r.t_sample)
     v = float(np.mean(vals))
+    step_s = float(np.mean(samples))
     line = {"impl": "reference", "metric": METRIC, "value": v,
             "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": r.t_round * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config} offloaded spec-decode round, n_cand {args.n_cand}, p {args.p}, "
                                    f"ctx {args.ctx}", "sample_seqs": 4},
+            "step": {"executed": "1 full-shape target layer verify (4 seqs × (n_cand+1) tokens, ctx "
+                                 f"{args.ctx}) + 1 full-shape draft layer step, NumPy fp32 on {r.cores} cores",
+                     "executed_s": step_s, "extrapolated_round_s": r.t_round,
+                     "value_is": "tokens/s of a full round extrapolated from the executed sample "
+                                 "(4·E[k] committed tokens / extrapolated round time)"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r.cores, "kind": "port", "sample": r.sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        line["reference_cpu_work"] = reference_cpu_work(args.config)
+    except Exception as exc:  # the arm's line must still print
+        line["reference_cpu_work"] = {"error": str(exc)[:200]}
     print(json.dumps(line))
 
 
@@ -206,6 +277,10 @@ def main():
 
         tgt, drf = pair(args.config)  # full-depth shapes
         cpu = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4)
+        try:
+            ref_work = reference_cpu_work(args.config)
+        except Exception as exc:
+            ref_work = {"error": str(exc)[:200]}
 
     import torch
     import torch.distributed as dist
@@ -213,7 +288,7 @@ def main():
     from paper_2505_10259_b200 import Policy, native
     from paper_2505_10259_b200.acceptance import AcceptanceModel, expected_accepted
     from paper_2505_10259_b200.api import build_engine
-    from paper_2505_10259_b200.planner_b200 import plan_offload, roofline_tokens_per_s, verify_flops
+    from paper_2505_10259_b200.planner_b200 import draft_flops, plan_offload, roofline_tokens_per_s, verify_flops
     from paper_2505_10259_b200.streamer import HostStore
     from paper_2505_10259_b200.weights import ffn_offsets, unit_layout
 
@@ -223,6 +298,9 @@ def main():
     share = -(-min(world, int(os.environ.get("LOCAL_WORLD_SIZE", world))) // n_dev)  # ranks per GPU
     if world > 1:
         if args.dist_backend == "nccl":
+            # communicator lines (rank, nranks, NVLS / P2P transport) on stderr for the driver's rank check
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group("gloo")
@@ -238,7 +316,11 @@ def main():
         # enforce the cap (configs[1]: "HBM capped to 24 GB") on the allocator itself
         torch.cuda.set_per_process_memory_fraction(min(1.0, hbm / total), device)
     # one host copy of the streamed layers serves every rank (SharedHostStore)
-    host = int(args.host_gb * 1e9) if args.host_gb else max(0, mem_available() - int(14e9))
+    # deterministic plan input: a fixed host budget (the plan, hence the headline, must not
+    # depend on free host RAM at launch); reduced only on a box that cannot hold it
+    host_req = int(args.host_gb * 1e9)
+    host = min(host_req, max(0, mem_available() - int(12e9)))
+    host_src = "requested" if host == host_req else f"reduced from {host_req} to MemAvailable − 12 GB"
     if world > 1:  # every rank must build the same plan: agree on the smallest measured budgets / rates
         agree = torch.tensor([float(link), float(hbm), float(host)], dtype=torch.float64,
                              device=device if args.dist_backend == "nccl" else "cpu")
@@ -364,7 +446,10 @@ def main():
     layer_bytes = ffn_offsets(tgt)[2]
     achieved_link = streamed / dev_s if dev_s > 0 else 0.0
     e_tok = expected_accepted(AcceptanceModel(args.p, args.n_cand))
-    F = verify_flops(tgt, bs, args.n_cand, args.ctx)
+    # compute term: the verify pass plus the concurrent draft work of the round
+    F_verify = verify_flops(tgt, bs, args.n_cand, args.ctx)
+    F_draft = draft_flops(drf, bs, args.n_cand, args.ctx, plan.draft_kv, plan.draft_cached)
+    F = F_verify + F_draft
     # north-star roofline: committed tokens over max(link bytes / B_h2d, compute at peak), per round
     roof = roofline_tokens_per_s(bs * e_tok * world, streamed / steps, F, link, peaks["bf16_tflops_sustained"] * 1e12)
     if world > 1:  # the NVLink all-gathers are a third bound
@@ -374,6 +459,21 @@ def main():
         roof = bs * e_tok * world / t_roof
     roof_raw = roofline_tokens_per_s(bs * e_tok * world, streamed_raw / steps, F, link,
                                      peaks["bf16_tflops_sustained"] * 1e12)
+
+    # ---- numerics of the headline path (forced acceptance hides them): a few sequences'
+    # verify logits through the product path vs a PyTorch fp32 restatement over the same
+    # streamed weights and KV (tools/fp32_ref.py) ----
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            from tools.fp32_ref import parity_report
+
+            t_p = time.perf_counter()
+            parity = parity_report(eng, s, n_seq=2)
+            parity["seconds"] = time.perf_counter() - t_p
+        except Exception as exc:  # the headline must still print
+            parity = {"error": f"{type(exc).__name__}: {str(exc)[:300]}"}
+        log(f"parity: {parity}")
 
     # ---- tensor-core kernel sample: MoE gate_up grouped GEMM at this round's shape ----
     kern = {}
@@ -539,13 +639,22 @@ def main():
                    "streamed_bytes_per_round": int(streamed / steps * world),
                    "kv_h2d_bytes_per_round": int(kv_link / steps * world),
                    "streamed_layer_bytes_per_round": len(plan.stream_layers) * layer_bytes,
-                   "host_pinned_bytes": store.bytes if store is not None else 0, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
+                   "host_pinned_bytes": store.bytes if store is not None else 0,
+                   "host_budget_bytes": host, "host_budget": host_src, "l2": "inputs ≫ L2 (≈180 GB streamed per step)",
                    "parallelism": f"dp{world} (independent prompt shards)", "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "h2d", "achieved": achieved_link / 1e9, "peak": link / 1e9, "unit": "GB/s",
                      "frac": achieved_link / link, "traffic": None,
+                     "peak_source": "pinned 1 GiB host→device cudaMemcpyAsync, best of 5, measured in this run "
+                                    "(MEASURED_PEAKS.json carries no host-link figure)",
                      "note": "dominant 'kernel' = copy-engine stream of the streamed layer units (XC4-encoded "
-                             "bytes when codec=xc4) plus, with host-resident target KV, the KV window pages; peak = "
-                             "pinned 1 GiB H2D measured in this run"},
+                             "bytes when codec=xc4) plus, with host-resident target KV, the KV window pages"},
+        "roofline_raw": {"bound": "h2d", "achieved": streamed_raw / dev_s / 1e9, "peak": link / 1e9, "unit": "GB/s",
+                         "frac": streamed_raw / dev_s / link,
+                         "note": "the same rounds counted in the reference's raw ffn_bytes (uncompressed bf16 layer "
+                                 "bytes delivered per second): > 1 because XC4 moves ≈0.70 of them over the link"},
+        "compute": {"flops_per_round": F, "verify_flops": F_verify, "draft_flops": F_draft,
+                    "t_at_sustained_peak_s": F / (peaks["bf16_tflops_sustained"] * 1e12),
+                    "t_link_s": streamed / steps / link},
         "roofline_tokens_per_s": roof, "frac_of_roofline": value / roof if roof else None,
         "nvlink": ({"received_bytes_per_round": int((nvl + streamed_raw * (world - 1)) / steps),
                     "achieved_GBps": (nvl + streamed_raw * (world - 1)) / dev_s / 1e9,
@@ -569,9 +678,13 @@ def main():
     }
     if gen is not None:
         line["e2e_generate"] = gen
+    if parity is not None:
+        line["parity"] = parity
     if cpu is not None:
         line["cpu_baseline"] = {"value": cpu.tokens_per_s, "unit": "tokens/s", "cores": cpu.cores, "kind": "port",
-                                "sample": cpu.sample}
+                                "sample": cpu.sample, "executed_s": cpu.t_sample,
+                                "extrapolated_round_s": cpu.t_round}
+        line["reference_cpu_work"] = ref_work
     print(json.dumps(line))
 
 

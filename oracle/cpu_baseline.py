@@ -28,12 +28,12 @@ def _arch(a, n_layer=1) -> Arch:
 
 
 def _weights(a: Arch, seed: int) -> dict:
-    """Cheap-to-build weights of the right shapes (values only matter for routing)."""
+    """Random weights of the benchmark's distribution (N(0, 0.02²))."""
     rng = np.random.default_rng(seed)
     H, I, E, dh = a.hidden, a.inter, a.n_expert, a.head_dim
 
     def filled(*shape):
-        return np.full(shape, 0.0078125, np.float32)
+        return rng.standard_normal(shape, dtype=np.float32) * np.float32(0.02)
 
     L = {"attn_norm": np.ones(H, np.float32), "ffn_norm": np.ones(H, np.float32),
          "wq": filled(a.n_head * dh, H), "wk": filled(a.n_kv_head * dh, H), "wv": filled(a.n_kv_head * dh, H),
@@ -49,12 +49,13 @@ def _weights(a: Arch, seed: int) -> dict:
 
 @dataclasses.dataclass
 class CpuSample:
-    tokens_per_s: float
+    tokens_per_s: float     # extrapolated: sample_seqs·E[k] per extrapolated round
     t_target_layer: float
     t_draft_layer: float
-    t_round: float
+    t_round: float          # extrapolated round time (not executed)
     sample: str
     cores: int
+    t_sample: float = 0.0   # wall time of the work actually executed (one step of the reference arm)
 
 
 def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4, seed: int = 0,
@@ -86,4 +87,4 @@ def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4
     sample = (f"1 target layer ({target.name if hasattr(target, 'name') else 'target'}) verify of {sample_seqs} seqs × "
               f"{n_cand + 1} tokens at ctx {ctx} + 1 draft layer decode step, NumPy fp32 on {cores} cores, "
               f"extrapolated to {target.n_layer}+{n_cand + 1}×{draft.n_layer} layers per round, E[k]={e:.4f}")
-    return CpuSample(sample_seqs * e / t_round, t_t, t_d, t_round, sample, cores)
+    return CpuSample(sample_seqs * e / t_round, t_t, t_d, t_round, sample, cores, t_t + t_d)

@@ -325,7 +325,7 @@ def _step_batch(kv, rows, positions, tokens_dev, device, max_q: int) -> ForwardB
     n_seq = rows.size
     slots = kv.slots(np.broadcast_to(rows[:, None], positions.shape), positions)
     qs = np.arange(n_seq + 1) * max_q
-    bt = kv.block_table[torch.from_numpy(rows).to(device)]
+    bt = _dev_i32(kv._bt_host[rows], device)  # window-relative pages for host-resident KV
     return ForwardBatch(tokens_dev, _dev_i32(positions.ravel(), device), _dev_i32(slots.ravel(), device),
                         _dev_i32(qs, device), _dev_i32(positions[:, 0], device), bt, n_seq, max_q)
 
@@ -343,6 +343,7 @@ class TargetModel(CausalLM):
 
         dev = self.device
         st = state.stream or torch.cuda.current_stream(dev)
+        state.kv.set_window(int(state.rows.min()), int(state.rows.max()) + 1)  # host-resident KV: the pass's pages
         with torch.cuda.stream(st):  # metadata copies ordered before the kernels that read them
             d = torch.as_tensor(draft_tokens, dtype=torch.int32).to(dev)
             bs, n = d.shape

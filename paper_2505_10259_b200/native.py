@@ -44,6 +44,8 @@ _SIGNATURES = {
     "so_gemm_bf16_ex": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, _P]),
     "so_gemm_grouped_bf16": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
     "so_gemm_bf16_v": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, c_int, _P]),
+    "so_gemv_workspace_bytes": (c_size_t, [c_int, c_int, c_int]),
+    "so_gemv_bf16": (c_int, [_P, _P, c_int, c_int, c_int, _P, c_int, c_int, _P, _P, c_size_t, _P]),
     "so_embed": (c_int, [_P, _P, c_int, c_int, _P, _P]),
     "so_rmsnorm": (c_int, [_P, _P, c_int, c_int, c_float, _P, _P]),
     "so_rope_kv_append": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_float, c_int, _P, _P, _P, _P]),
@@ -235,7 +237,8 @@ def _gemm_workspace(M: int, N: int, K: int, stream: int, device) -> tuple[int, i
     with _splitk_lock:
         ws = _splitk_ws.get(stream)
         if ws is None or ws.numel() < need:
-            ws = torch.empty(max(need, 16 << 20), dtype=torch.uint8, device=device)
+            # zero-filled once: the decode-step kernel's per-tile arrival counters (left zero by every launch)
+            ws = torch.zeros(max(need, 16 << 20), dtype=torch.uint8, device=device)
             _splitk_ws[stream] = ws
     return ws.data_ptr(), ws.numel()
 
@@ -252,9 +255,10 @@ def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
     ws, ws_bytes = _gemm_workspace(M, N, K, st, a.device) if variant != 3 else (0, 0)
     _check(lib().so_gemm_bf16_v(_ptr(a), _ptr(b), None, 1, M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux), ws,
                                 ws_bytes, variant, st), "so_gemm_bf16")
-    if ws:
+    gemv = variant in (0, 4) and epilogue != EPI_BF16_ROWSCALE and lib().so_gemv_workspace_bytes(M, N, K) > 0
+    if ws and not gemv:
         with _count_lock:
-            launches["kernels"] += 1  # the split-K reduce
+            launches["kernels"] += 1  # the split-K reduce (the decode-step kernel reduces in place)
 
 
 def gemm_grouped(a, b_ptr: int, expert_offsets, E: int, N: int, out, epilogue=EPI_BF16, aux=None, stream=None,

@@ -384,3 +384,63 @@ def test_gemm_splitk_skinny(M, N, K):
     outs = torch.empty(M, N // 2, dtype=torch.bfloat16, device=DEV)
     native.gemm(a, interleave_gate_up(wg, wu).contiguous(), outs, native.EPI_SWIGLU)
     _bf16_close(outs, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T))
+
+
+# ------------------------------------------------------------- K5b decode steps ---
+
+@pytest.mark.parametrize("M,N,K,epi", [
+    (64, 6144, 4096, 0),          # Mistral-7B QKV decode step
+    (64, 4096, 4096, 2),          # O + residual
+    (64, 28672, 4096, 3),         # gate_up SwiGLU
+    (64, 4096, 14336, 2),         # down + residual (tiles split over many CTAs)
+    (112, 4096, 14336, 2),
+    (128, 32768, 4096, 1),        # LM head (fp32 logits)
+    (1, 128, 64, 0),              # one row, one tile, one k-block
+    (17, 384, 192, 3),            # ragged rows, 3 tiles of 3 k-blocks
+    (33, 1024, 640, 1),
+    (100, 256, 8192, 0),          # two tiles, long K: every CTA a slice of one tile
+])
+def test_gemv_decode_step(M, N, K, epi):
+    """The stream-K decode-step kernel (so_gemv_bf16, variant 4) against fp32
+    torch; run twice: bitwise deterministic, and the per-tile arrival counters
+    are left zero by the first launch (the second is just as correct)."""
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ref = a.float() @ b.float().T
+    aux = None
+    if epi == native.EPI_SWIGLU:
+        from paper_2505_10259_b200.weights import SWIGLU_BLOCK
+
+        blk = ref.view(M, N // (2 * SWIGLU_BLOCK), 2, SWIGLU_BLOCK)
+        ref = (torch.nn.functional.silu(blk[:, :, 0]) * blk[:, :, 1]).reshape(M, N // 2)
+    elif epi == native.EPI_BF16_RESID:
+        aux = torch.randn(M, N, device=DEV, generator=g).to(torch.bfloat16)
+        ref = ref.to(torch.bfloat16).float() + aux.float()
+    cols = N // 2 if epi == native.EPI_SWIGLU else N
+    dt = torch.float32 if epi == native.EPI_F32 else torch.bfloat16
+    outs = []
+    for _ in range(2):
+        out = torch.full((M, cols), float("nan"), dtype=dt, device=DEV)
+        native.gemm(a, b, out, epi, aux, variant=4)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    if epi == native.EPI_F32:
+        torch.testing.assert_close(outs[0], ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+    else:
+        _bf16_close(outs[0], ref)
+
+
+def test_gemv_is_the_auto_choice_for_decode_steps():
+    """Auto (variant 0) routes M ≤ 128 dense GEMMs to the decode-step kernel and
+    larger M to the tiled kernels: same results either way within bf16."""
+    g = torch.Generator(device=DEV).manual_seed(3)
+    a = torch.randn(48, 4096, device=DEV, generator=g).to(torch.bfloat16)
+    b = (torch.randn(4096, 4096, device=DEV, generator=g) / 64).to(torch.bfloat16)
+    o0 = torch.empty(48, 4096, dtype=torch.bfloat16, device=DEV)
+    o4 = torch.empty_like(o0)
+    native.gemm(a, b, o0)
+    native.gemm(a, b, o4, variant=4)
+    torch.cuda.synchronize()
+    assert torch.equal(o0, o4)

@@ -216,3 +216,17 @@ def test_rng_free_and_deterministic():
     b = P.search(P.SearchSpace((16,), (16, 32, 64), (8, 16), (2, 4, 8)), WL, hw, t, d)
     assert [(p.as_tuple(), x.throughput) for p, x in a.entries] == [(p.as_tuple(), x.throughput) for p, x in b.entries]
     assert np.isfinite([x.throughput for _, x in a.entries]).all()
+
+
+def test_bench_reference_cpu_work_runs_the_unmodified_reference():
+    """bench.py's reference_cpu_work: the reference's own search / simulate /
+    predict on the B200 preset, from the baseline/_ref install."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not os.path.isdir(os.path.join(root, "baseline", "_ref", "specpipe")):
+        pytest.skip("baseline/_ref not installed (run __graft_entry__.build())")
+    import bench
+
+    out = bench.reference_cpu_work("8x22b")
+    assert "unavailable" not in out and out["grid_points"] > 100
+    assert [r["hbm_gib"] for r in out["search"]][:3] == [24, 48, 96]
+    assert out["simulate_decoding"]["events"] > 0 and out["predict_throughput"]["tokens_per_s"] > 0
