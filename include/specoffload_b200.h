@@ -201,15 +201,24 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* q_start, const int32_t* kv_before,
                   int bs, int max_q, int hq, int hkv, int dh, int page_size,
                   float scale, void* out, void* stream);
-/* Same with the K/V tile staging an explicit argument: 0 = TMA boxes issued by
- * one thread where the page size allows (pages of ≤ 32 slots dividing 32, or
+/* Same with the kernel an explicit argument: 0 = TMA boxes issued by one
+ * thread where the page size allows (pages of ≤ 32 slots dividing 32, or
  * multiples of 32), else cp.async (so_attn_paged's choice); 1 = cp.async by
- * every thread. */
+ * every thread; 2 = K6b, the tcgen05 kernel (so_attn_paged_tc). */
 int so_attn_paged_v(const void* q, const void* k_cache, const void* v_cache,
                     const int32_t* block_table, int max_pages,
                     const int32_t* q_start, const int32_t* kv_before,
                     int bs, int max_q, int hq, int hkv, int dh, int page_size,
                     float scale, void* out, int variant, void* stream);
+/* K6b — the same attention on the tcgen05 tensor cores: persistent CTAs over
+ * (sequence, kv head, 128 query rows) units, S = Q·Kᵀ and P·V accumulated in
+ * TMEM, TMA-staged K/V tiles of 64 keys, one query row per softmax thread.
+ * dh = 128, hq/hkv ≤ 128, page_size ≥ 8 dividing 64 or a multiple of 64. */
+int so_attn_paged_tc(const void* q, const void* k_cache, const void* v_cache,
+                     const int32_t* block_table, int max_pages,
+                     const int32_t* q_start, const int32_t* kv_before,
+                     int bs, int max_q, int hq, int hkv, int dh, int page_size,
+                     float scale, void* out, void* stream);
 
 /* ---- Canonical-order arithmetic (parity mode, tiny shapes) ----------------
  * The same ops, operands, epilogues and bf16 rounding points as the product

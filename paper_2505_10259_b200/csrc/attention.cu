@@ -480,7 +480,10 @@ extern "C" int so_attn_paged_v(const void* q, const void* k_cache, const void* v
                                void* stream) {
   SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
   SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
-  SO_REQUIRE(page_size >= 1 && (variant == 0 || variant == 1), SO_E_SHAPE);
+  SO_REQUIRE(page_size >= 1 && variant >= 0 && variant <= 2, SO_E_SHAPE);
+  if (variant == 2)
+    return so_attn_paged_tc(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv, dh,
+                            page_size, scale, out, stream);
   SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);
   if (bs == 0) return SO_OK;
   cudaStream_t st = as_stream(stream);

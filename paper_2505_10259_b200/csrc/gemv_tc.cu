@@ -224,10 +224,21 @@ __global__ void __launch_bounds__(kGThreads, 1)
           __threadfence();
           // fixed contributor order 0..last-first: the sum does not depend on arrival order
           const float* base = partials + (size_t)tile * max_contrib * NT * kWRows;
-          for (int m = 0; m < NT; ++m) {
-            float s = 0.f;
-            for (int j = 0; j <= last - first; ++j) s += __ldcg(base + ((size_t)j * NT + m) * kWRows + row);
-            accv[m] = s;
+          // 16 token columns per step, every contributor's loads issued before the adds (L2 latency overlapped)
+          for (int m0 = 0; m0 < NT; m0 += 16) {
+            float s16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) s16[i] = 0.f;
+            for (int j = 0; j <= last - first; ++j) {
+              const float* src = base + ((size_t)j * NT + m0) * kWRows + row;
+              float v16[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v16[i] = __ldcg(src + (size_t)i * kWRows);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) s16[i] += v16[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) accv[m0 + i] = s16[i];
           }
           store_row<EPI>(row, n, M, NT, accv, C, ldc, aux, swap);
         }

@@ -51,6 +51,8 @@ _SIGNATURES = {
     "so_rope_kv_append": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_float, c_int, _P, _P, _P, _P]),
     "so_attn_paged": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
                               c_float, _P, _P]),
+    "so_attn_paged_tc": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
+                                 c_float, _P, _P]),
     "so_attn_paged_v": (c_int, [_P, _P, _P, _P, c_int, _P, _P, c_int, c_int, c_int, c_int, c_int, c_int,
                                 c_float, _P, c_int, _P]),
     "so_canon_gemm": (c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, _P, c_int, c_int, _P, _P]),
@@ -294,7 +296,8 @@ def rope_kv_append(qkv, positions, slots, hq, hkv, dh, theta, page_size, q_out, 
 
 def attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, hkv, dh, page_size, scale, out,
                stream=None, variant: int = 0):
-    """``variant`` 0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging."""
+    """``variant`` 0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging,
+    2 = the tcgen05 kernel (S and O in TMEM)."""
     bs = kv_before.numel()
     _check(lib().so_attn_paged_v(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
                                  _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,

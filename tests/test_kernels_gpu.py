@@ -323,9 +323,22 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
     (128, 32, 8, [9, 1, 40], [300, 31, 0], 8),               # small pages: 4 TMA boxes per tile
     (64, 4, 2, [5, 3], [20, 7], 5),                          # odd pages: cp.async staging only
 ])
-@pytest.mark.parametrize("attn_variant", [0, 1], ids=["tma", "cp_async"])
+@pytest.mark.parametrize("attn_variant", [0, 1, 2], ids=["tma", "cp_async", "tcgen05"])
 def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
+    if attn_variant == 2 and (dh != 128 or not (ps >= 8 and (64 % ps == 0 if ps <= 64 else ps % 64 == 0))):
+        pytest.skip("K6b covers dh 128 with pages dividing 64 (or multiples of 64)")
     _check_attn(dh, hq, hkv, qlens, kvbs, ps, attn_variant)
+
+
+@pytest.mark.parametrize("qlens,kvbs,hq", [
+    ([9] * 40, [503 + i for i in range(40)], 48),          # verify batch, 8x22B heads (G 6: 21 positions per unit)
+    ([520, 300, 64], [0, 0, 0], 32),                          # draft re-prefill, Mistral heads (G 4)
+    ([1, 2, 130], [1000, 64, 7], 32),                         # mixed, many units per CTA
+])
+def test_attn_tcgen05_larger(qlens, kvbs, hq):
+    """K6b over more units than SMs (persistent CTAs carry the ring, TMEM and
+    barrier phases across units) at the path's head shapes."""
+    _check_attn(128, hq, 8, qlens, kvbs, 16, 2)
 
 
 def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):

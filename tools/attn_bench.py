@@ -50,12 +50,14 @@ def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20, variant=0):
     b.synchronize()
     t = a.elapsed_time(b) / reps * 1e-3
     kv_bytes = bs * (ctx + q_len) * hkv * dh * 2 * 2
-    return {"bs": bs, "n_cand": n, "ctx": ctx, "us": t * 1e6, "kv_MB": kv_bytes / 1e6,
-            "GBps": kv_bytes / t / 1e9, "frac_of_hbm_peak": kv_bytes / t / 1e9 / PEAK}
+    # causal FLOPs: QKᵀ and PV over the keys each query row sees (ctx + j + 1)
+    flops = 4.0 * bs * hq * dh * sum(ctx + j + 1 for j in range(q_len))
+    return {"bs": bs, "n_cand": n, "ctx": ctx, "hq": hq, "us": t * 1e6, "kv_MB": kv_bytes / 1e6,
+            "GBps": kv_bytes / t / 1e9, "frac_of_hbm_peak": kv_bytes / t / 1e9 / PEAK, "tflops": flops / t / 1e12}
 
 
 if __name__ == "__main__":
-    for variant, label in ((1, "cp_async"), (0, "tma")):
+    for variant, label in ((1, "cp_async"), (0, "tma"), (2, "tcgen05")):
         for r in [run(variant=variant), run(bs=128, n=4, variant=variant), run(bs=248, n=8, ctx=2000, variant=variant),
                   run(bs=472, n=8, ctx=520, variant=variant), run(bs=64, n=519, ctx=1, hq=32, hkv=8, variant=variant)]:
             r["staging"] = label
