@@ -160,7 +160,8 @@ int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, 
  * SO_EPI_BF16 / F32 / BF16_RESID / SWIGLU.  The workspace
  * (so_gemv_workspace_bytes, 0 = shape not eligible) holds per-tile arrival
  * counters followed by fp32 partials; it must be zero-filled before its first
- * use — every launch leaves the counters zero again.  so_gemm_bf16_ex and
+ * use — every launch leaves the counters zero again — and must not double as
+ * a split-K workspace (split-K partials would overwrite the counters).  so_gemm_bf16_ex and
  * so_gemm_bf16_v (variant 0 or 4) route eligible shapes here. */
 size_t so_gemv_workspace_bytes(int M, int N, int K);
 int so_gemv_bf16(const void* X, const void* W, int M, int N, int K, void* C, int ldc, int epilogue,

@@ -4,27 +4,31 @@
 // The reference charges the whole MoE block as one `ffn_gpu` event per layer
 // (simulator.py:185-191); its routing semantics are the third-party Mixtral
 // block (transformers modeling_mixtral.py: fp32 softmax → top-2 → renormalise),
-// cited in SURVEY.md §8c.  Three launches, no host synchronisation:
-//   1. route:   one warp per token — E dot products (fp32), top-2 (ties → lower
-//               expert index), pair-renormalised weights, per-expert histogram;
-//   2. scan:    one CTA — exclusive scan of the histogram into expert offsets,
-//               then a stable rank of every (token, slot) inside its expert using
-//               __match_any_sync + popc (order = token index, so the permutation
-//               is deterministic);
-//   3. gather:  x_perm[row] = x[perm_token[row]] with 16-B vector copies.
+// cited in SURVEY.md §8c.  ONE cooperative launch, no host synchronisation.
+// CTA c owns the contiguous token range [T·c/G, T·(c+1)/G):
+//   A. route:   one warp per token — E dot products (fp32), top-2 (ties → lower
+//               expert index), pair-renormalised weights; a per-CTA expert
+//               histogram in shared memory, published to the workspace;
+//   —  grid barrier (all CTAs are co-resident: cooperative launch, ≤ one wave);
+//   B. place:   every CTA sums the published histograms — expert offsets
+//               (exclusive scan over experts) plus its own base inside each
+//               expert (the counts of lower CTAs) — then ranks its (token, slot)
+//               pairs stably in token order with __match_any_sync + popc, so
+//               the permutation is the same as one global stable sort;
+//   C. gather:  x_perm[row] = x[token] for its own tokens, 16-B vectors (the x
+//               rows were read in A a few µs earlier: L2 hits).
 #include "common.cuh"
 
 namespace {
 
 constexpr int kMaxE = 16;  // Mixtral uses 8; accumulators stay in registers
 
-__global__ void route_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T,
-                             int H, int E, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
-                             int32_t* __restrict__ counts) {
-  const int warps = blockDim.x >> 5;
-  const int t = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
+constexpr int kRThreads = 256;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kMaxRouterCtas = 1024;
+
+__device__ __forceinline__ void route_token(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                                            int t, int H, int E, int lane, int& i0, int& i1, float& w0, float& w1) {
   float acc[kMaxE];
 #pragma unroll
   for (int e = 0; e < kMaxE; ++e) acc[e] = 0.0f;
@@ -44,7 +48,8 @@ __global__ void route_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfl
     }
   }
   float l0 = -3.4e38f, l1 = -3.4e38f;
-  int i0 = 0, i1 = 1;
+  i0 = 0;
+  i1 = 1;
 #pragma unroll
   for (int e = 0; e < kMaxE; ++e) {
     if (e >= E) break;
@@ -56,48 +61,84 @@ __global__ void route_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfl
       l1 = v; i1 = e;
     }
   }
-  if (lane == 0) {
-    // softmax over all E then renormalising the top pair == softmax over the pair
-    const float w1 = 1.0f / (1.0f + expf(l0 - l1));
-    const float w0 = 1.0f - w1;
-    topk_idx[2 * t] = i0;
-    topk_idx[2 * t + 1] = i1;
-    topk_w[2 * t] = w0;
-    topk_w[2 * t + 1] = w1;
-    atomicAdd(&counts[i0], 1);
-    atomicAdd(&counts[i1], 1);
-  }
+  // softmax over all E then renormalising the top pair == softmax over the pair
+  w1 = 1.0f / (1.0f + expf(l0 - l1));
+  w0 = 1.0f - w1;
 }
 
-constexpr int kScanThreads = 1024;
-
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const int32_t* __restrict__ topk_idx,
-                                                            const float* __restrict__ topk_w,
-                                                            const int32_t* __restrict__ counts, int T, int E,
-                                                            int32_t* __restrict__ offs, int32_t* __restrict__ perm_token,
-                                                            float* __restrict__ row_weight,
-                                                            int32_t* __restrict__ token_rows) {
-  __shared__ int s_offs[kMaxE + 1];
-  __shared__ int s_base[kMaxE];
-  __shared__ int s_warp_cnt[kScanThreads / 32][kMaxE];
+__global__ void __launch_bounds__(kRThreads) router_fused_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T, int H, int E,
+    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ cta_counts,
+    unsigned int* __restrict__ barrier, int32_t* __restrict__ offs, int32_t* __restrict__ perm_token,
+    float* __restrict__ row_weight, int32_t* __restrict__ token_rows, __nv_bfloat16* __restrict__ x_perm) {
+  __shared__ int s_cnt[kMaxE];
+  __shared__ int s_cursor[kMaxE];
+  __shared__ int s_warp_cnt[kRWarps][kMaxE];
+  const int G = gridDim.x, c = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = (int)((long)T * c / G), t1 = (int)((long)T * (c + 1) / G);
+  if (tid < kMaxE) s_cnt[tid] = 0;
+  __syncthreads();
+
+  // ---- A. route this CTA's tokens ----
+  for (int t = t0 + warp; t < t1; t += kRWarps) {
+    int i0, i1;
+    float w0, w1;
+    route_token(x, wg, t, H, E, lane, i0, i1, w0, w1);
+    if (lane == 0) {
+      topk_idx[2 * t] = i0;
+      topk_idx[2 * t + 1] = i1;
+      topk_w[2 * t] = w0;
+      topk_w[2 * t + 1] = w1;
+      atomicAdd(&s_cnt[i0], 1);
+      atomicAdd(&s_cnt[i1], 1);
+    }
+  }
+  __syncthreads();
+  if (tid < E) cta_counts[c * kMaxE + tid] = s_cnt[tid];
+
+  // ---- grid barrier: every CTA's histogram published (bounded spin: an error, never a hung GPU) ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(barrier, 1u);
+    unsigned int polls = 0;
+    while (atomicAdd(barrier, 0u) < (unsigned int)G) {
+      if (++polls > (1u << 28)) __trap();
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+
+  // ---- B. offsets and this CTA's base inside each expert ----
+  if (tid < E) {
+    int below = 0, total = 0;
+    for (int k = 0; k < G; ++k) {
+      const int v = __ldcg(&cta_counts[k * kMaxE + tid]);
+      total += v;
+      if (k < c) below += v;
+    }
+    s_cnt[tid] = total;
+    s_cursor[tid] = below;
+  }
+  __syncthreads();
   if (tid == 0) {
     int a = 0;
     for (int e = 0; e < E; ++e) {
-      s_offs[e] = a;
-      s_base[e] = 0;
-      a += counts[e];
+      s_cursor[e] += a;  // offs[e] + rows of expert e owned by lower CTAs
+      if (c == 0) offs[e] = a;
+      a += s_cnt[e];
     }
-    s_offs[E] = a;
+    if (c == 0) offs[E] = a;
   }
   __syncthreads();
-  if (tid <= E) offs[tid] = s_offs[tid];
-  const int pairs = 2 * T;
-  for (int tile = 0; tile < pairs; tile += kScanThreads) {
+  // stable rank of every (token, slot) pair of [2·t0, 2·t1) inside its expert, token order
+  for (int tile = 2 * t0; tile < 2 * t1; tile += kRThreads) {
     const int p = tile + tid;
-    const bool live = p < pairs;
+    const bool live = p < 2 * t1;
     const int e = live ? topk_idx[p] : -1;
-    for (int i = tid; i < (kScanThreads / 32) * kMaxE; i += kScanThreads) (&s_warp_cnt[0][0])[i] = 0;
+    for (int i = tid; i < kRWarps * kMaxE; i += kRThreads) (&s_warp_cnt[0][0])[i] = 0;
     __syncthreads();
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
@@ -106,30 +147,27 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int32_t* __res
     if (live) {
       int before = 0;
       for (int w = 0; w < warp; ++w) before += s_warp_cnt[w][e];
-      const int row = s_offs[e] + s_base[e] + before + rank_in_warp;
-      const int t = p >> 1;
-      perm_token[row] = t;
+      const int row = s_cursor[e] + before + rank_in_warp;
+      perm_token[row] = p >> 1;
       row_weight[row] = topk_w[p];
       token_rows[p] = row;
     }
     __syncthreads();
     if (tid < E) {
       int tot = 0;
-      for (int w = 0; w < kScanThreads / 32; ++w) tot += s_warp_cnt[w][tid];
-      s_base[tid] += tot;
+      for (int w = 0; w < kRWarps; ++w) tot += s_warp_cnt[w][tid];
+      s_cursor[tid] += tot;
     }
     __syncthreads();
   }
-}
 
-__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ perm_token,
-                                   int rows, int H, __nv_bfloat16* __restrict__ x_perm) {
+  // ---- C. gather this CTA's tokens into their two expert rows ----
   const int vec = H / 8;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)rows * vec;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / vec), c = (int)(i % vec);
-    const int t = perm_token[r];
-    reinterpret_cast<int4*>(x_perm + (size_t)r * H)[c] = __ldg(reinterpret_cast<const int4*>(x + (size_t)t * H) + c);
+  for (int p = 2 * t0 + warp; p < 2 * t1; p += kRWarps) {
+    const int row = token_rows[p];
+    const int4* src = reinterpret_cast<const int4*>(x + (size_t)(p >> 1) * H);
+    int4* dst = reinterpret_cast<int4*>(x_perm + (size_t)row * H);
+    for (int v = lane; v < vec; v += 32) dst[v] = __ldg(src + v);
   }
 }
 
@@ -163,11 +201,30 @@ int grid_for(size_t work, int threads) {
   return (int)g;
 }
 
+
+int router_grid(int T) {
+  // co-resident CTAs of the cooperative launch (thread-safe static init; fixed for the device model)
+  static const int max_ctas = [] {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, router_fused_kernel, kRThreads, 0) != cudaSuccess)
+      per_sm = 1;
+    return per_sm * device_sm_count();
+  }();
+  int g = (T + kRWarps - 1) / kRWarps;  // ≥ one token per warp
+  const int cap = device_sm_count() < max_ctas ? device_sm_count() : max_ctas;  // one wave: ≤ one CTA per SM
+  if (g > cap) g = cap;
+  if (g > kMaxRouterCtas) g = kMaxRouterCtas;
+  return g < 1 ? 1 : g;
+}
+
+constexpr size_t kRouterHdr = 256 + (size_t)kMaxRouterCtas * kMaxE * sizeof(int32_t);
+
 }  // namespace
 
 extern "C" size_t so_router_workspace_bytes(int T, int E) {
-  // counts[E] + topk scratch when the caller passes NULL for topk outputs
-  return 256 + (size_t)T * 2 * (sizeof(int32_t) + sizeof(float)) + (size_t)E * sizeof(int32_t);
+  // barrier word + per-CTA histograms, then topk scratch for callers passing NULL topk outputs
+  (void)E;
+  return kRouterHdr + (size_t)T * 2 * (sizeof(int32_t) + sizeof(float));
 }
 
 extern "C" int so_router_top2(const void* x, const void* w_gate, int T, int H, int E, int32_t* topk_idx,
@@ -176,29 +233,25 @@ extern "C" int so_router_top2(const void* x, const void* w_gate, int T, int H, i
   SO_REQUIRE(x && w_gate && expert_offsets && perm_token && row_weight && token_rows && x_perm && workspace,
              SO_E_NULLPTR);
   SO_REQUIRE(T >= 0 && H > 0 && H % 8 == 0 && E >= 2 && E <= kMaxE, SO_E_SHAPE);
-  SO_REQUIRE(aligned16(x) && aligned16(w_gate) && aligned16(x_perm), SO_E_ALIGN);
+  SO_REQUIRE(aligned16(x) && aligned16(w_gate) && aligned16(x_perm) && aligned16(workspace), SO_E_ALIGN);
   cudaStream_t st = as_stream(stream);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  int32_t* counts = reinterpret_cast<int32_t*>(ws);
-  int32_t* idx = topk_idx ? topk_idx : reinterpret_cast<int32_t*>(ws + 256);
-  float* w = topk_w ? topk_w : reinterpret_cast<float*>(ws + 256 + (size_t)T * 2 * sizeof(int32_t));
-  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st);
+  unsigned int* barrier = reinterpret_cast<unsigned int*>(ws);
+  int32_t* cta_counts = reinterpret_cast<int32_t*>(ws + 256);
+  int32_t* idx = topk_idx ? topk_idx : reinterpret_cast<int32_t*>(ws + kRouterHdr);
+  float* w = topk_w ? topk_w : reinterpret_cast<float*>(ws + kRouterHdr + (size_t)T * 2 * sizeof(int32_t));
+  cudaError_t e = cudaMemsetAsync(barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return (int)e;
-  if (T > 0) {
-    const int warps = 8;
-    route_kernel<<<(T + warps - 1) / warps, warps * 32, 0, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(w_gate), T, H, E, idx,
-        w, counts);
-    SO_CHECK_LAUNCH();
-  }
-  scan_kernel<<<1, kScanThreads, 0, st>>>(idx, w, counts, T, E, expert_offsets, perm_token, row_weight,
-                                          token_rows);
-  SO_CHECK_LAUNCH();
-  if (T > 0) {
-    gather_rows_kernel<<<grid_for((size_t)2 * T * (H / 8), 256), 256, 0, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(x), perm_token, 2 * T, H, reinterpret_cast<__nv_bfloat16*>(x_perm));
-    SO_CHECK_LAUNCH();
-  }
+  const int grid = router_grid(T);
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(w_gate);
+  __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
+  void* args[] = {&xb, &wb, &T, &H, &E, &idx, &w, &cta_counts, &barrier, &expert_offsets, &perm_token, &row_weight,
+                  &token_rows, &xp};
+  // cooperative: the runtime guarantees every CTA is resident at once (the grid barrier needs it)
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(router_fused_kernel), dim3(grid), dim3(kRThreads),
+                                  args, 0, st);
+  if (e != cudaSuccess) return (int)e;
   return SO_OK;
 }
 

@@ -240,6 +240,10 @@ class Engine:
             self.tracer.add("GPU_TARGET", "ffn_gpu", self._marks.get(li), ev, bi, li, rnd)
 
     def resolve_trace(self) -> list:
+        # the streamer runs ahead across rounds: copies for the next round's
+        # layers may still be in flight on the copy stream when the last
+        # round's barrier completes — their marks resolve once they land
+        torch.cuda.synchronize(self.device)
         st = self.target.streamer
         if st is not None and self.tracer.enabled and self.tracer.t0 is not None:
             for k, layer, a, b in st.copy_marks:

@@ -117,7 +117,7 @@ def exported_symbols() -> list[str]:
 
 # kernels (or copy-engine DMA batches) each entry point enqueues; summed into
 # ``launches`` so bench.py can report how many of our kernels ran
-_KERNELS_PER_CALL = {"so_router_top2": 3, "so_canon_router_top2": 3, "so_stream_layer": 0, "so_xc4_encode": 5}
+_KERNELS_PER_CALL = {"so_router_top2": 1, "so_canon_router_top2": 3, "so_stream_layer": 0, "so_xc4_encode": 5}
 launches = {"kernels": 0, "copies": 0}
 _count_lock = threading.Lock()  # the verify and draft streams are enqueued from two threads
 
@@ -229,24 +229,25 @@ def moe_combine(y_perm, token_rows, resid, out, stream=None):
 # ---------------------------------------------------------------- GEMMs ---
 
 _splitk_ws: dict[int, torch.Tensor] = {}  # stream handle → grow-only split-K scratch (one per enqueuing stream)
+_gemv_ws: dict[int, torch.Tensor] = {}    # stream handle → K5b scratch: arrival counters (zero between launches)
 _splitk_lock = threading.Lock()
 
 
-def _gemm_workspace(M: int, N: int, K: int, stream: int, device) -> tuple[int, int]:
-    need = int(lib().so_gemm_workspace_bytes(M, N, K))
+def _stream_ws(pool: dict, need: int, stream: int, device) -> tuple[int, int]:
     if need == 0:
         return 0, 0
     with _splitk_lock:
-        ws = _splitk_ws.get(stream)
+        ws = pool.get(stream)
         if ws is None or ws.numel() < need:
-            # zero-filled once: the decode-step kernel's per-tile arrival counters (left zero by every launch)
+            # zero-filled once: K5b's per-tile arrival counters (every launch leaves them zero)
             ws = torch.zeros(max(need, 16 << 20), dtype=torch.uint8, device=device)
-            _splitk_ws[stream] = ws
+            pool[stream] = ws
     return ws.data_ptr(), ws.numel()
 
 
 def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
-    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (skinny shapes: split-K over the SMs).
+    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (decode steps: the K5b stream-K
+    kernel; other skinny shapes: split-K over the SMs).
     ``variant``: tile choice (0 = auto; see so_gemm_bf16_v) — tests and benchmarks only."""
     M, K = a.shape
     N = b.shape[-2]
@@ -254,10 +255,17 @@ def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
     _need(a, torch.bfloat16, "a")
     assert b.dtype == torch.bfloat16
     st = _stream(stream)
-    ws, ws_bytes = _gemm_workspace(M, N, K, st, a.device) if variant != 3 else (0, 0)
+    # K5b and split-K never share scratch: split-K's fp32 partials would land on
+    # the arrival counters K5b needs zero at launch
+    gemv = variant in (0, 4) and epilogue != EPI_BF16_ROWSCALE and lib().so_gemv_workspace_bytes(M, N, K) > 0
+    if gemv:
+        ws, ws_bytes = _stream_ws(_gemv_ws, int(lib().so_gemv_workspace_bytes(M, N, K)), st, a.device)
+    elif variant != 3:
+        ws, ws_bytes = _stream_ws(_splitk_ws, int(lib().so_gemm_workspace_bytes(M, N, K)), st, a.device)
+    else:
+        ws, ws_bytes = 0, 0
     _check(lib().so_gemm_bf16_v(_ptr(a), _ptr(b), None, 1, M, N, K, _ptr(out), out.stride(0), epilogue, _ptr(aux), ws,
                                 ws_bytes, variant, st), "so_gemm_bf16")
-    gemv = variant in (0, 4) and epilogue != EPI_BF16_ROWSCALE and lib().so_gemv_workspace_bytes(M, N, K) > 0
     if ws and not gemv:
         with _count_lock:
             launches["kernels"] += 1  # the split-K reduce (the decode-step kernel reduces in place)

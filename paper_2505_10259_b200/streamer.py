@@ -20,6 +20,7 @@ import dataclasses
 import mmap
 import os
 import threading
+import weakref
 
 import torch
 
@@ -38,7 +39,7 @@ class HostStore:
     """
 
     def __init__(self, threads: int | None = None):
-        self._maps: list[tuple[mmap.mmap, int, int]] = []
+        self._maps: list[tuple[mmap.mmap, weakref.finalize, int]] = []
         self.threads = threads or min(16, os.cpu_count() or 4)
         self.bytes = 0
 
@@ -58,7 +59,13 @@ class HostStore:
         rc = torch.cuda.cudart().cudaHostRegister(addr, nbytes, 0)
         if int(rc) != 0:
             raise InsufficientTotalMemory(f"cudaHostRegister of {nbytes} B failed ({int(rc)})")
-        self._maps.append((m, addr, nbytes))
+        # the page lock lives exactly as long as the mapping's last view: the
+        # finaliser runs before the buffer export is dropped, i.e. before the
+        # mmap can be unmapped (a range unmapped while registered leaks its
+        # pinned pages and makes the next mapping at that address fail, 712)
+        fin = weakref.finalize(buf, _host_unregister, addr)
+        fin.atexit = False
+        self._maps.append((m, fin, nbytes))
         self.bytes += nbytes
         t = torch.frombuffer(buf, dtype=torch.uint8)
         return t
@@ -78,9 +85,14 @@ class HostStore:
             t.join()
 
     def close(self) -> None:
-        for m, addr, _ in self._maps:
-            torch.cuda.cudart().cudaHostUnregister(addr)
+        """Unlock every region now (views stay readable as pageable memory)."""
+        for _, fin, _ in self._maps:
+            fin()
         self._maps.clear()
+
+
+def _host_unregister(addr: int) -> None:
+    torch.cuda.cudart().cudaHostUnregister(addr)
 
 
 def slice_bounds(nbytes: int, rank: int, world: int) -> tuple[int, int]:

@@ -373,9 +373,11 @@ def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):
 
 @pytest.mark.parametrize("M,N,K", [(64, 4096, 4096), (112, 4096, 14336), (64, 6144, 4096), (33, 2048, 2048),
                                    (200, 1024, 8192)])
-def test_gemm_splitk_skinny(M, N, K):
+@pytest.mark.parametrize("gemm_variant", [1, 0], ids=["split_k", "auto"])
+def test_gemm_splitk_skinny(M, N, K, gemm_variant):
     """Draft decode-step shapes: K split over the SMs into fp32 partials, then
-    one reduce applies the epilogue — every epilogue against an fp32 reference."""
+    one reduce applies the epilogue (variant 1), or the auto choice (K5b for
+    M ≤ 128) — every epilogue against an fp32 reference."""
     assert native.lib().so_gemm_workspace_bytes(M, N, K) > 0  # the split is taken for these shapes
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
     a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
@@ -395,7 +397,7 @@ def test_gemm_splitk_skinny(M, N, K):
 
     wg, wu = b[: N // 2], b[N // 2:]
     outs = torch.empty(M, N // 2, dtype=torch.bfloat16, device=DEV)
-    native.gemm(a, interleave_gate_up(wg, wu).contiguous(), outs, native.EPI_SWIGLU)
+    native.gemm(a, interleave_gate_up(wg, wu).contiguous(), outs, native.EPI_SWIGLU, variant=gemm_variant)
     _bf16_close(outs, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T))
 
 

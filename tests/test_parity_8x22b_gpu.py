@@ -159,7 +159,8 @@ def _oracle_arch(a):
 
 def _layer_parity(arch, model_of, stream_layers, codec, n_seq=32, n_cand=8, ctx=503, seed=7):
     """Verify pass of n_seq sequences × (n_cand + 1) tokens over ctx positions of
-    shared random KV, engine vs oracle.  Returns (got, want, router_gap)."""
+    shared random KV, engine vs oracle.  Returns (got, want, router_gap, want_fp32):
+    ``want`` mirrors the kernels' bf16 rounding points, ``want_fp32`` keeps fp32."""
     W = _logical(arch, seed)
     rng = np.random.default_rng(seed)
     tokens = rng.integers(0, arch.vocab, (n_seq, n_cand + 1)).astype(np.int32)
@@ -210,12 +211,15 @@ def _layer_parity(arch, model_of, stream_layers, codec, n_seq=32, n_cand=8, ctx=
     finally:
         model_ref.rmsnorm = orig
     want = np.stack(want)
+    # the same oracle without bf16 rounding points: exact arithmetic, for the calibration bar
+    want32 = np.stack(model_ref.forward(_oracle_arch(arch), Wn, kv_np, list(range(n_seq)), list(tokens),
+                                        [ctx] * n_seq, False, "all"))
     gap = None
     if arch.is_moe:  # min(top1 − top2, top2 − top3) router-logit gap per token
         lr = cap["hn"].astype(np.float64) @ Wn["layers"][0]["router"].T.astype(np.float64)
         srt = -np.sort(-lr, axis=1)
         gap = np.minimum(srt[:, 0] - srt[:, 1], srt[:, 1] - srt[:, 2]).reshape(tokens.shape)
-    return got, want, gap
+    return got, want, gap, want32
 
 
 def _dense_verify(model, state, tokens):
@@ -229,31 +233,45 @@ MISTRAL_7B_V3_1L = dataclasses.replace(MISTRAL_7B_V3, n_layer=1)
 MIXTRAL_1L_TINYFFN = dataclasses.replace(MIXTRAL_8X22B, n_layer=1, inter=128)
 
 
-def _check_logits(got, want, exclude=None):
-    """0.05 + 2 % of |ref| on every compared row; argmax equal off near-ties."""
+def _check_logits(got, want, exclude=None, want32=None):
+    """Logits tolerance.  Every intermediate hidden state is stored in bf16 (the
+    kernels' and the mirroring oracle's rounding points), and a 1-ulp rounding
+    disagreement anywhere in the 6144- (4096-) wide state moves every logit by
+    ≈ ulp·|w_lm|, so the bar is stated relative to the logit scale:
+      * rms(Δ) ≤ 1 % of rms(want) and max |Δ| ≤ 0.15·rms(want);
+      * argmax equal wherever the oracle's top-1/top-2 gap exceeds 0.25·rms(want);
+      * calibration: the GPU is no further from exact fp32 arithmetic than the
+        bf16-mirroring oracle itself, within 2× (rms(got − fp32) ≤ 2·rms(want − fp32)).
+    Tokens whose top-2 routing is a near-tie in the oracle (``exclude``) are
+    skipped: a rounding difference may legitimately pick the other expert."""
     n_seq, T, V = want.shape
     mask = np.ones((n_seq, T), bool) if exclude is None else ~exclude
     assert mask.mean() > 0.9, f"too many near-tie routed tokens excluded ({(~mask).sum()})"
-    d = np.abs(got - want)
-    tol = 0.05 + 0.02 * np.abs(want)
-    bad = (d > tol) & mask[..., None]
-    assert not bad.any(), f"{bad.sum()} logits off; max |Δ| {d[mask].max():.4f}"
+    d = np.abs(got - want)[mask]
+    scale = float(np.sqrt((want[mask] ** 2).mean()))
+    rms = float(np.sqrt((d ** 2).mean()))
+    assert rms <= 0.01 * scale, f"rms |Δ| {rms:.4f} > 1% of rms logit {scale:.3f}"
+    assert d.max() <= 0.15 * scale, f"max |Δ| {d.max():.4f} > 0.15·rms logit {scale:.3f}"
     top2 = -np.sort(-want, axis=-1)[..., :2]
-    decisive = (top2[..., 0] - top2[..., 1] > 0.1) & mask
+    decisive = (top2[..., 0] - top2[..., 1] > 0.25 * scale) & mask
     assert (got.argmax(-1) == want.argmax(-1))[decisive].all()
-    return float(d[mask].max()), float(decisive.mean())
+    if want32 is not None:
+        e_gpu = float(np.sqrt(((got - want32)[mask] ** 2).mean()))
+        e_orc = float(np.sqrt(((want - want32)[mask] ** 2).mean()))
+        assert e_gpu <= 2.0 * e_orc + 1e-4 * scale, f"GPU {e_gpu:.4f} vs oracle {e_orc:.4f} from exact fp32"
+    return float(d.max()), float(decisive.mean())
 
 
 def test_mixtral_8x22b_layer_and_lm_head_vs_oracle():
     a = dataclasses.replace(MIXTRAL_8X22B, n_layer=1)
-    got, want, gap = _layer_parity(a, lambda e: e.target, {0}, "xc4")
+    got, want, gap, want32 = _layer_parity(a, lambda e: e.target, {0}, "xc4")
     near = gap < 1e-3
-    maxd, dec = _check_logits(got, want, exclude=near)
+    maxd, dec = _check_logits(got, want, exclude=near, want32=want32)
     print(f"8x22B layer: max |Δlogit| {maxd:.4f}, decisive rows {dec:.2f}, near-tie routed tokens {near.sum()}")
 
 
 def test_mistral_7b_draft_layer_and_lm_head_vs_oracle():
     a = MISTRAL_7B_V3_1L
-    got, want, _ = _layer_parity(a, lambda e: e.draft, set(), "none", n_seq=32, n_cand=4)
-    maxd, dec = _check_logits(got, want)
+    got, want, _, want32 = _layer_parity(a, lambda e: e.draft, set(), "none", n_seq=32, n_cand=4)
+    maxd, dec = _check_logits(got, want, want32=want32)
     print(f"Mistral-7B layer: max |Δlogit| {maxd:.4f}, decisive rows {dec:.2f}")
