@@ -90,6 +90,15 @@ METRIC = "decode tokens/s (offloaded Mixtral target + draft) vs host-link roofli
 NVLINK_PEER_BPS = 770e9  # B200_PROFILING.md: measured NVLink 5 peer copy per direction
 
 
+def _weights_checksum(eng) -> str:
+    """SO_DEBUG_CHECKSUM=1: checksums of the resident weights (a debugging aid for
+    stray device writes; off by default)."""
+    t, d = eng.target.w, eng.draft.w
+    parts = [("t.lm_head", t.lm_head), ("t.embed", t.embed), ("t.final_norm", t.final_norm),
+             ("t.router0", t.layers[0].router), ("d.lm_head", d.lm_head), ("d.embed", d.embed)]
+    return " ".join(f"{n}={x.double().sum().item():.6e}" for n, x in parts if x is not None)
+
+
 def log(msg: str) -> None:
     """Progress line on stderr (rank-tagged): locates a stall in multi-rank runs."""
     print(f"[rank {os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
@@ -382,12 +391,22 @@ def main():
                         bs_draft=plan.bs_draft, draft_kv=plan.draft_kv, draft_cached=plan.draft_cached,
                         kv_host=plan.kv_host)
     eng.synthetic_context(s, args.ctx, max_new, seed=rank)
+    dbg_sum = os.environ.get("SO_DEBUG_CHECKSUM") == "1"
+    if dbg_sum:
+        torch.cuda.synchronize(device)
+        log(f"checksum after build+context: {_weights_checksum(eng)}")
     eng.first_draft(s)
+    if dbg_sum:
+        torch.cuda.synchronize(device)
+        log(f"checksum after first draft: {_weights_checksum(eng)}")
     setup_s = time.perf_counter() - t_setup
     log(f"setup {setup_s:.1f} s")
     for i in range(warm):
         eng.round(s)
         log(f"warm-up round {i}")
+        if dbg_sum:
+            torch.cuda.synchronize(device)
+            log(f"checksum after warm-up round {i}: {_weights_checksum(eng)}")
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()

@@ -158,8 +158,9 @@ int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, 
  * stream-K split of the (tile, k-block) space, deterministic in-kernel
  * reduction of split tiles).  N % 128 == 0, K % 64 == 0; epilogues
  * SO_EPI_BF16 / F32 / BF16_RESID / SWIGLU.  The workspace
- * (so_gemv_workspace_bytes, 0 = shape not eligible) holds per-tile arrival
- * counters followed by fp32 partials; it must be zero-filled before its first
+ * (so_gemv_workspace_bytes, 0 = shape not eligible) holds a fixed 64 KiB
+ * region of per-tile arrival counters followed by fp32 partials, so one
+ * workspace serves every eligible shape in turn; it must be zero-filled before its first
  * use — every launch leaves the counters zero again — and must not double as
  * a split-K workspace (split-K partials would overwrite the counters).  so_gemm_bf16_ex and
  * so_gemm_bf16_v (variant 0 or 4) route eligible shapes here. */

@@ -32,6 +32,7 @@ constexpr int kGMaxStages = 12;
 constexpr int kWRows = 128;                   // weight rows per tile (MMA M)
 constexpr int kWBytes = kWRows * kTmaBoxK * 2;  // 16 KB per k-block
 constexpr size_t kGSmemBudget = 200 * 1024;
+constexpr size_t kArrivalBytes = 64 * 1024;   // per-tile arrival counters: ≤ 16384 weight tiles (N ≤ 2 Mi)
 
 // contiguous range [lo, hi) of the flattened (tile, k-block) space owned by CTA g of G
 __device__ __forceinline__ void cta_range(long total, int g, int G, long& lo, long& hi) {
@@ -275,7 +276,10 @@ GemvPlan plan_gemv(int M, int N, int K) {
   // contributors of one tile: ≤ ceil(num_kb / per_cta) + 1
   const long per = total / G;
   p.max_contrib = (int)((K / kTmaBoxK + per - 1) / (per > 0 ? per : 1)) + 2;
-  p.arrivals_bytes = ((size_t)p.n_tiles * 4 + 255) / 256 * 256;
+  // a FIXED counter region for every shape: a workspace serves many shapes in
+  // turn, and a shape with fewer tiles must not lay its partials over counters
+  // a wider shape relies on being zero
+  p.arrivals_bytes = kArrivalBytes;
   p.partial_bytes = (size_t)p.n_tiles * p.max_contrib * p.NT * kWRows * 4;
   return p;
 }
@@ -301,6 +305,7 @@ int launch_gemv(const GemvPlan& p, const CUtensorMap& mw, const CUtensorMap& mx,
 
 extern "C" size_t so_gemv_workspace_bytes(int M, int N, int K) {
   if (M <= 0 || M > 128 || N <= 0 || K <= 0 || N % kWRows || K % kTmaBoxK) return 0;
+  if ((size_t)(N / kWRows) * sizeof(int) > kArrivalBytes) return 0;
   const GemvPlan p = plan_gemv(M, N, K);
   return p.arrivals_bytes + p.partial_bytes;
 }
@@ -309,6 +314,7 @@ extern "C" int so_gemv_bf16(const void* X, const void* W, int M, int N, int K, v
                             const void* aux, void* workspace, size_t ws_bytes, void* stream) {
   SO_REQUIRE(X && W && C && workspace, SO_E_NULLPTR);
   SO_REQUIRE(M >= 0 && M <= 128 && N > 0 && K > 0 && N % kWRows == 0 && K % kTmaBoxK == 0, SO_E_SHAPE);
+  SO_REQUIRE((size_t)(N / kWRows) * sizeof(int) <= kArrivalBytes, SO_E_SHAPE);
   SO_REQUIRE(aligned16(X) && aligned16(W) && aligned16(workspace), SO_E_ALIGN);
   if (epilogue == SO_EPI_SWIGLU) SO_REQUIRE(ldc >= N / 2, SO_E_SHAPE);
   else SO_REQUIRE(ldc >= N, SO_E_SHAPE);

@@ -238,6 +238,7 @@ class Engine:
             self._marks[li] = ev
         else:
             self.tracer.add("GPU_TARGET", "ffn_gpu", self._marks.get(li), ev, bi, li, rnd)
+            self._last_ffn_end = ev
 
     def resolve_trace(self) -> list:
         # the streamer runs ahead across rounds: copies for the next round's
@@ -246,10 +247,13 @@ class Engine:
         torch.cuda.synchronize(self.device)
         st = self.target.streamer
         if st is not None and self.tracer.enabled and self.tracer.t0 is not None:
-            for k, layer, a, b in st.copy_marks:
+            tags = {}
+            for k, layer, a, b, resource, label in st.copy_marks:
                 if a is not None and b is not None:
-                    rnd, bi = st.use_tags.pop(k, (None, None))
-                    self.tracer.add("IO_C2G", "ffn_load", a, b, bi, layer, rnd)
+                    if k not in tags:
+                        tags[k] = st.use_tags.pop(k, (None, None))
+                    rnd, bi = tags[k]
+                    self.tracer.add(resource, label, a, b, bi, layer, rnd)
             st.copy_marks.clear()
         return self.tracer.resolve()
 
@@ -645,7 +649,13 @@ class Engine:
             native.sample_tokens(logits[T:T + nn], first, uniforms=u, temperature=s.temperature, stream=st)
             native.copy_sm(s.res_first[bi].data_ptr(), first.data_ptr(), nn * 4, st)
         ev2 = tr.mark(st)
-        tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
+        if self.target.hooks is not None and getattr(self, "_last_ffn_end", None) is not None:
+            # per-layer events cover the pass (one event at a time per resource, _checks.py:7-18):
+            # only the final norm + LM head remain
+            tr.add("GPU_TARGET", "lm_head", self._last_ffn_end, ev1, batch=bi, rnd=rnd)
+            self._last_ffn_end = None
+        else:
+            tr.add("GPU_TARGET", "verify", ev0, ev1, batch=bi, rnd=rnd)
         tr.add("GPU_TARGET", "accept", ev1, ev2, batch=bi, rnd=rnd)
 
     def _commit(self, s: DecodeSession, bi: int) -> int:

@@ -416,7 +416,8 @@ class LayerStreamer:
         self.raw_bytes_issued = 0  # layer bytes this rank's copies / shards delivered
         self.nvlink_bytes_issued = 0  # bytes this rank receives in the all-gathers
         self.trace = trace
-        self.copy_marks: list[tuple[int, int, torch.cuda.Event, torch.cuda.Event]] = []
+        # (use, layer, start event, end event, resource, label)
+        self.copy_marks: list[tuple] = []
         # (round, batch) of the pass that consumed each use: the engine sets
         # pass_tag before a verify pass, so a load's trace event carries the
         # round of its ffn_gpu (the reference's causality check keys on it)
@@ -442,7 +443,8 @@ class LayerStreamer:
             self.nvlink_bytes_issued += (self.world - 1) * (self.hi - self.lo)
             self.raw_bytes_issued += self.hi - self.lo
             if self.trace:
-                self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.comm_stream)))
+                self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.comm_stream),
+                                        "IO_C2G", "ffn_load"))
             return
         if k >= self.n_slots and not self.coded:  # coded: the decoder waits instead, the link runs ahead
             self.free[slot].wait(self.copy_stream)
@@ -472,8 +474,13 @@ class LayerStreamer:
             self.bytes_issued += unit.frame_bytes(f0, f1)
             self.raw_bytes_issued += self.hi - self.lo
             if self.trace:
+                # two resources (T7: one timeline per stream): the copy engine moving
+                # the frames, then the decoder (and, N > 1, the all-gather) finishing the slot
+                copied = native.Event(timing=True).record(self.copy_stream)
+                self.copy_marks.append((k, layer, start, copied, "IO_C2G", "ffn_load"))
                 end_stream = self.decode_stream if self.world == 1 else self.comm_stream
-                self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream)))
+                self.copy_marks.append((k, layer, copied, native.Event(timing=True).record(end_stream),
+                                        "GPU_DECODE", "ffn_decode"))
             return
         if self.world == 1:
             native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
@@ -491,7 +498,8 @@ class LayerStreamer:
             self.loaded[slot].record(self.comm_stream)
         if self.trace:
             end_stream = self.copy_stream if self.world == 1 else self.comm_stream
-            self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream)))
+            self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream), "IO_C2G",
+                                    "ffn_load"))
         self.bytes_issued += self.hi - self.lo
         self.raw_bytes_issued += self.hi - self.lo
 

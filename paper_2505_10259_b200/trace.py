@@ -16,9 +16,9 @@ import io
 import json
 
 
-RESOURCES = ("GPU_TARGET", "GPU_DRAFT", "CPU", "IO_C2G", "IO_G2C", "IO_DISK")
+RESOURCES = ("GPU_TARGET", "GPU_DRAFT", "CPU", "IO_C2G", "IO_G2C", "IO_DISK", "GPU_DECODE")
 LABELS = ("attn_gpu", "ffn_load", "ffn_gpu", "draft_prefill", "draft_decode", "accept", "kv_offload",
-          "disk_prefetch", "barrier", "prefill")
+          "disk_prefetch", "barrier", "prefill", "ffn_decode", "lm_head", "verify")
 
 
 @dataclasses.dataclass(frozen=True)

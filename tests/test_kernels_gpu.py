@@ -447,6 +447,28 @@ def test_gemv_decode_step(M, N, K, epi):
         _bf16_close(outs[0], ref)
 
 
+def test_gemv_shared_workspace_across_shapes():
+    """One K5b workspace serves every shape in turn (the verify pass: QKV, O,
+    then the 256-tile LM head): a narrow shape's fp32 partials must never land
+    on the arrival counters a wider shape needs zero (regression: the LM head of
+    an 18-row verify read stale counters after the O projection)."""
+    g = torch.Generator(device=DEV).manual_seed(5)
+    ws = torch.zeros(max(native.lib().so_gemv_workspace_bytes(18, N, 6144) for N in (6144, 8192, 32768)),
+                     dtype=torch.uint8, device=DEV)
+    for N, epi in [(8192, native.EPI_BF16), (6144, native.EPI_F32), (32768, native.EPI_F32), (6144, native.EPI_F32),
+                   (32768, native.EPI_F32)]:
+        a = torch.randn(18, 6144, device=DEV, generator=g).to(torch.bfloat16)
+        b = (torch.randn(N, 6144, device=DEV, generator=g) / math.sqrt(6144)).to(torch.bfloat16)
+        out = torch.empty(18, N, dtype=torch.float32 if epi == native.EPI_F32 else torch.bfloat16, device=DEV)
+        native._check(native.lib().so_gemv_bf16(a.data_ptr(), b.data_ptr(), 18, N, 6144, out.data_ptr(), N, epi,
+                                                None, ws.data_ptr(), ws.numel(), native._stream(None)), "gemv")
+        ref = a.float() @ b.float().T
+        if epi == native.EPI_F32:
+            torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+        else:
+            _bf16_close(out, ref)
+
+
 def test_gemv_is_the_auto_choice_for_decode_steps():
     """Auto (variant 0) routes M ≤ 128 dense GEMMs to the decode-step kernel and
     larger M to the tiled kernels: same results either way within bf16."""

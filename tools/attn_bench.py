@@ -57,8 +57,13 @@ def run(bs=248, n=8, ctx=520, hq=48, hkv=8, dh=128, ps=16, reps=20, variant=0):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # one variant at the verify shape of the bench plan (profiling)
+        v = int(sys.argv[1])
+        print(json.dumps(run(bs=488, n=8, ctx=520, variant=v, reps=5)))
+        sys.exit(0)
     for variant, label in ((1, "cp_async"), (0, "tma"), (2, "tcgen05")):
         for r in [run(variant=variant), run(bs=128, n=4, variant=variant), run(bs=248, n=8, ctx=2000, variant=variant),
-                  run(bs=472, n=8, ctx=520, variant=variant), run(bs=64, n=519, ctx=1, hq=32, hkv=8, variant=variant)]:
+                  run(bs=488, n=8, ctx=520, variant=variant), run(bs=64, n=519, ctx=1, hq=32, hkv=8, variant=variant),
+                  run(bs=64, n=0, ctx=520, hq=32, hkv=8, variant=variant)]:
             r["staging"] = label
             print(json.dumps(r))

@@ -216,10 +216,22 @@ def verify_teacher_forced(eng, state: SeqState, draft_tokens: torch.Tensor, stre
             per_layer.append(rec)
         xf = _rms(xs[nL].float(), w.final_norm, a.eps)
         want = (xf @ w.lm_head.float().T).view(bs, T, -1)
+        # the same final norm + LM head re-run through the native ops on the snapshot
+        from paper_2505_10259_b200 import native
+        xf_n = torch.empty((R, H), dtype=torch.bfloat16, device=dev)
+        native.rmsnorm(xs[nL], w.final_norm, xf_n, a.eps, stream)
+        lg_n = torch.empty((R, a.vocab), dtype=torch.float32, device=dev)
+        native.gemm(xf_n, w.lm_head, lg_n, native.EPI_F32, None, stream)
+        xf_prod = tm.ws.get("xf", (R, H), torch.bfloat16).clone()
     stream.synchronize()
     got = got.float()
     d = (got - want).abs()
     row_max = d.amax(-1).reshape(-1)
+    diag = {"native_rerun_vs_fp32_max": (lg_n.view_as(want) - want).abs().max().item(),
+            "native_rerun_vs_product_max": (lg_n.view_as(got) - got).abs().max().item(),
+            "xf_product_vs_rerun_max": (xf_prod.float() - xf_n.float()).abs().max().item(),
+            "lm_head_ptr_aligned": w.lm_head.data_ptr() % 16 == 0, "lm_head_shape": list(w.lm_head.shape),
+            "lm_head_contig": w.lm_head.is_contiguous()}
     scale = want.abs().max().item()
     top2 = torch.topk(want, 2, dim=-1).values
     decisive = (top2[..., 0] - top2[..., 1]) > 0.02 * scale
@@ -232,7 +244,7 @@ def verify_teacher_forced(eng, state: SeqState, draft_tokens: torch.Tensor, stre
            "argmax_agree_decisive": agree[decisive].float().mean().item() if decisive.any() else None,
            "decisive_rows": int(decisive.sum().item()), "per_layer": per_layer,
            "lm_head_row_max_abs": [round(v, 4) for v in row_max.tolist()],
-           "got_zero_rows": int((got.reshape(-1, got.shape[-1]).abs().amax(-1) == 0).sum().item())}
+           "got_zero_rows": int((got.reshape(-1, got.shape[-1]).abs().amax(-1) == 0).sum().item()), "diag": diag}
     if E:
         res["route_agree_min"] = min(r["route_agree"] for r in per_layer)
     return res
