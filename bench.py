@@ -50,6 +50,11 @@ def parse():
     ap.add_argument("--n-cand", type=int, default=8, help="draft length (8 = the paper's best 8x22B policy)")
     ap.add_argument("--p", type=float, default=0.8)
     ap.add_argument("--ctx", type=int, default=503)
+    ap.add_argument("--max-new", type=int, default=16,
+                    help="tokens per request (the reference Workload's max_new_tokens; paper tables: 16): a finished "
+                         "sequence restarts as a new request for its cached prompt, commits clamped to what is "
+                         "left — the steady state, independent of --steps; 0 = legacy (contexts grow for the "
+                         "whole run, nothing clamped)")
     ap.add_argument("--bs", type=int, default=0, help="per-batch size (0 = planner)")
     ap.add_argument("--host-gb", type=float, default=193.0,
                     help="pinned host budget for streamed units, GB (default 193: 55 XC4 8x22B units on the "
@@ -295,7 +300,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2505_10259_b200 import Policy, native
-    from paper_2505_10259_b200.acceptance import AcceptanceModel, expected_accepted
+    from paper_2505_10259_b200.acceptance import AcceptanceModel, committed_per_verify, expected_accepted
     from paper_2505_10259_b200.api import build_engine
     from paper_2505_10259_b200.planner_b200 import draft_flops, plan_offload, roofline_tokens_per_s, verify_flops
     from paper_2505_10259_b200.streamer import HostStore
@@ -338,8 +343,11 @@ def main():
     steps, warm = args.steps, args.warmup
     # rounds alternate batches: batch 0 is verified ceil(R/2) times in R rounds, each committing
     # ≤ n_cand+1 tokens, so no sequence can be clamped by `remaining` inside the run
-    verifies_per_batch = -(-(warm + steps) // 2)
-    max_new = verifies_per_batch * (args.n_cand + 1)
+    if args.max_new > 0:  # steady state of max_new-token requests (recycled on their cached prompt)
+        max_new = args.max_new
+    else:  # legacy: batch 0 is verified ceil(R/2) times in R rounds, each committing ≤ n_cand+1 tokens
+        verifies_per_batch = -(-(warm + steps) // 2)
+        max_new = verifies_per_batch * (args.n_cand + 1)
     from paper_2505_10259_b200.planner_b200 import B200Rates
 
     rates = B200Rates(h2d_bytes_per_s=link, hbm_bytes_per_s=peaks["hbm_gbs"] * 1e9)
@@ -362,7 +370,8 @@ def main():
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
                         draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
                         world=world, allow_shards=not args.no_shards, disk_budget=int(args.disk_gb * 1e9),
-                        kv_host_modes=(False, True) if world == 1 else (False,))
+                        kv_host_modes=(False, True) if world == 1 else (False,),
+                        tokens_per_verify=committed_per_verify(AcceptanceModel(args.p, args.n_cand), args.max_new))
     log(f"plan: bs {plan.bs_decoding} draft {plan.draft_kv}/{plan.draft_cached} pinned {len(plan.pinned_layers)} "
         f"streamed {len(plan.stream_layers)} (disk {len(plan.disk_layers)}) sharded {len(plan.shard_layers)} "
         f"link {link / 1e9:.1f} GB/s")
@@ -390,7 +399,7 @@ def main():
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
                         bs_draft=plan.bs_draft, draft_kv=plan.draft_kv, draft_cached=plan.draft_cached,
                         kv_host=plan.kv_host)
-    eng.synthetic_context(s, args.ctx, max_new, seed=rank)
+    eng.synthetic_context(s, args.ctx, max_new, seed=rank, recycle=args.max_new > 0)
     dbg_sum = os.environ.get("SO_DEBUG_CHECKSUM") == "1"
     if dbg_sum:
         torch.cuda.synchronize(device)
@@ -464,7 +473,8 @@ def main():
     # ---- dominant kernel: the copy engine (host link) ----
     layer_bytes = ffn_offsets(tgt)[2]
     achieved_link = streamed / dev_s if dev_s > 0 else 0.0
-    e_tok = expected_accepted(AcceptanceModel(args.p, args.n_cand))
+    # expected commits per verification: E[k], clamped by what each request has left (steady state)
+    e_tok = committed_per_verify(AcceptanceModel(args.p, args.n_cand), args.max_new)
     # compute term: the verify pass plus the concurrent draft work of the round
     F_verify = verify_flops(tgt, bs, args.n_cand, args.ctx)
     F_draft = draft_flops(drf, bs, args.n_cand, args.ctx, plan.draft_kv, plan.draft_cached)
@@ -650,6 +660,11 @@ def main():
                    "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
                    "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,
+                   "max_new_tokens": args.max_new if args.max_new > 0 else None,
+                   "requests": ("steady state: a sequence that generated max_new tokens restarts as a new request "
+                                "for its cached 503-token prompt (commits clamped, simulator.py:213-214); "
+                                f"expected commits per verify {e_tok:.4f}") if args.max_new > 0 else
+                               "legacy: contexts grow for the whole run",
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "hbm_sharded_layers": len(plan.shard_layers), "disk_layers": len(plan.disk_layers),
                    "target_kv": "host DRAM (one batch staged per layer)" if plan.kv_host else "HBM",

@@ -152,18 +152,17 @@ int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, 
 /* Grouped (MoE) GEMM: rows [offs[e], offs[e+1]) of A use expert e's weight
  * B + e·N·K.  max_rows bounds offs[E] (no host sync: the tile schedule is
  * derived on device from offs). */
-/* K5b — decode-step GEMM, M ≤ 128 activation rows (the draft's n_cand decode
+/* K5c — decode-step GEMM, M ≤ 128 activation rows (the draft's n_cand decode
  * steps, costmodel.py:53-57 t_draft_decode_gpu): the weights W [N,K] stream
- * once from HBM over every SM (swap-AB tcgen05 tiles of 128 weight rows,
- * stream-K split of the (tile, k-block) space, deterministic in-kernel
- * reduction of split tiles).  N % 128 == 0, K % 64 == 0; epilogues
- * SO_EPI_BF16 / F32 / BF16_RESID / SWIGLU.  The workspace
- * (so_gemv_workspace_bytes, 0 = shape not eligible) holds a fixed 64 KiB
- * region of per-tile arrival counters followed by fp32 partials, so one
- * workspace serves every eligible shape in turn; it must be zero-filled before its first
- * use — every launch leaves the counters zero again — and must not double as
- * a split-K workspace (split-K partials would overwrite the counters).  so_gemm_bf16_ex and
- * so_gemm_bf16_v (variant 0 or 4) route eligible shapes here. */
+ * once from HBM over (nearly) every SM — swap-AB tcgen05 tiles of 128 weight
+ * rows; each tile's K range split over the C ≤ 8 CTAs of a thread-block
+ * cluster; the fp32 partials reduced through distributed shared memory in
+ * fixed CTA order (deterministic) with the epilogue fused.  N % 128 == 0,
+ * K % 128 == 0; epilogues SO_EPI_BF16 / F32 / BF16_RESID / SWIGLU.
+ * so_gemv_workspace_bytes returns 256 for shapes K5c serves (fewer weight
+ * tiles than SMs) and 0 otherwise; the kernel itself needs no scratch (the
+ * workspace arguments are accepted and ignored).  so_gemm_bf16_v (variant 0
+ * or 4) routes eligible shapes here. */
 size_t so_gemv_workspace_bytes(int M, int N, int K);
 int so_gemv_bf16(const void* X, const void* W, int M, int N, int K, void* C, int ldc, int epilogue,
                  const void* aux, void* workspace, size_t ws_bytes, void* stream);
@@ -176,9 +175,9 @@ int so_gemm_grouped_bf16(const void* A, const void* B, const int32_t* expert_off
  * double-buffered TMEM accumulators: CTA-pair 256×256 cta_group::2 tiles for
  * dense M ≥ 1024 with N % 256 == 0, else 1-CTA 128×{128,256}), 1 = persistent
  * 1-CTA only, 2 = persistent CTA-pair wherever legal, 3 = the auto choice with
- * one tile per CTA (non-persistent, no split-K), 4 = the K5b decode-step
- * kernel (so_gemv_bf16) where eligible, else auto.  Auto (0) takes K5b for
- * dense M ≤ 128 when the workspace allows.  No process-wide state. */
+ * one tile per CTA (non-persistent, no split-K), 4 = the K5c decode-step
+ * kernel (so_gemv_bf16) where eligible, else auto.  Auto (0) takes K5c for
+ * dense M ≤ 128 with fewer weight tiles than SMs.  No process-wide state. */
 int so_gemm_bf16_v(const void* A, const void* B, const int32_t* expert_offsets, int E, int M, int N, int K,
                    void* C, int ldc, int epilogue, const void* aux, void* workspace, size_t ws_bytes,
                    int variant, void* stream);

@@ -45,6 +45,21 @@ def expected_accepted(model: AcceptanceModel) -> float:
     return float((1.0 - model.p ** (model.n_cand + 1)) / (1.0 - model.p))
 
 
+def committed_per_verify(model: AcceptanceModel, max_new: int) -> float:
+    """Expected tokens committed per verification when every sequence generates
+    exactly ``max_new`` tokens and the last verification is clamped to what is
+    left (simulator.py:213-214): max_new / E[verifications to finish], with
+    V(r) = 1 + Σ_k P[k] · V(r − k) for r > 0 (V ≤ 0 = 0) — the steady-state
+    rate of a pool whose finished sequences are immediately replaced."""
+    if max_new <= 0:
+        return expected_accepted(model)
+    probs = pmf(model)
+    V = np.zeros(max_new + 1)
+    for r in range(1, max_new + 1):
+        V[r] = 1.0 + sum(probs[k - 1] * V[max(r - k, 0)] for k in range(1, model.n_cand + 2))
+    return float(max_new / V[max_new])
+
+
 def sample_accepted(model: AcceptanceModel, rng: np.random.Generator, size: int | None = None):
     cdf = np.cumsum(pmf(model))
     cdf[-1] = 1.0

@@ -901,12 +901,10 @@ extern "C" int so_gemm_bf16_v(const void* A, const void* B, const int32_t* exper
                               int variant, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (expert_offsets != nullptr) return gemm_dispatch(A, B, expert_offsets, E, M, N, K, C, ldc, epilogue, aux, variant, st);
-  // decode steps (M ≤ 128 rows): the weight-streaming stream-K kernel, unless a tile variant is forced
-  if ((variant == 0 || variant == 4) && epilogue != SO_EPI_BF16_ROWSCALE && workspace != nullptr) {
-    const size_t need = so_gemv_workspace_bytes(M, N, K);
-    if (need && ws_bytes >= need)
-      return so_gemv_bf16(A, B, M, N, K, C, ldc, epilogue, aux, workspace, ws_bytes, stream);
-  }
+  // decode steps (M ≤ 128 rows, fewer weight tiles than SMs): the K5c cluster split-K kernel
+  // (no scratch), unless a tile variant is forced
+  if ((variant == 0 || variant == 4) && epilogue != SO_EPI_BF16_ROWSCALE && so_gemv_workspace_bytes(M, N, K) > 0)
+    return so_gemv_bf16(A, B, M, N, K, C, ldc, epilogue, aux, nullptr, 0, stream);
   if (variant == 4) variant = 0;  // not eligible: the automatic choice
   const int ks = (M > 0 && N > 0 && K >= BK && K % BK == 0 && N % 128 == 0) ? splitk_factor(M, N, K, variant) : 0;
   if (ks == 0 || workspace == nullptr || ws_bytes < (size_t)ks * M * N * sizeof(float))

@@ -17,17 +17,21 @@
 //               the permutation is the same as one global stable sort;
 //   C. gather:  x_perm[row] = x[token] for its own tokens, 16-B vectors (the x
 //               rows were read in A a few µs earlier: L2 hits).
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int kMaxE = 16;  // Mixtral uses 8; accumulators stay in registers
 
-constexpr int kRThreads = 256;
+constexpr int kRThreads = 512;
+constexpr size_t kRouterSmemMax = 160 * 1024;  // the gate weights E·H bf16 staged in shared memory up to this
 constexpr int kRWarps = kRThreads / 32;
 constexpr int kMaxRouterCtas = 1024;
 
-__device__ __forceinline__ void route_token(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+__device__ __forceinline__ void route_token(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* wg,
                                             int t, int H, int E, int lane, int& i0, int& i1, float& w0, float& w1) {
   float acc[kMaxE];
 #pragma unroll
@@ -40,7 +44,7 @@ __device__ __forceinline__ void route_token(const __nv_bfloat16* __restrict__ x,
     for (int e = 0; e < kMaxE; ++e) {
       if (e >= E) break;
       float wf[8];
-      unpack8(__ldg(reinterpret_cast<const int4*>(wg + (size_t)e * H) + c), wf);
+      unpack8(reinterpret_cast<const int4*>(wg + (size_t)e * H)[c], wf);
       float s = 0.0f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) s = fmaf(xf[j], wf[j], s);
@@ -70,7 +74,8 @@ __global__ void __launch_bounds__(kRThreads) router_fused_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T, int H, int E,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ cta_counts,
     unsigned int* __restrict__ barrier, int32_t* __restrict__ offs, int32_t* __restrict__ perm_token,
-    float* __restrict__ row_weight, int32_t* __restrict__ token_rows, __nv_bfloat16* __restrict__ x_perm) {
+    float* __restrict__ row_weight, int32_t* __restrict__ token_rows, __nv_bfloat16* __restrict__ x_perm,
+    int stage_w) {
   __shared__ int s_cnt[kMaxE];
   __shared__ int s_cursor[kMaxE];
   __shared__ int s_warp_cnt[kRWarps][kMaxE];
@@ -78,13 +83,22 @@ __global__ void __launch_bounds__(kRThreads) router_fused_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = (int)((long)T * c / G), t1 = (int)((long)T * (c + 1) / G);
   if (tid < kMaxE) s_cnt[tid] = 0;
+  // the gate weights (Mixtral-8x22B: 8 × 6144 bf16 = 96 KB) read once per CTA into shared memory:
+  // every token's E dot products then read them at shared-memory speed instead of through L1/L2
+  extern __shared__ int4 s_wg[];
+  const __nv_bfloat16* wsrc = wg;
+  if (stage_w) {
+    const int n16 = E * H / 8;
+    for (int i = tid; i < n16; i += kRThreads) s_wg[i] = __ldg(reinterpret_cast<const int4*>(wg) + i);
+    wsrc = reinterpret_cast<const __nv_bfloat16*>(s_wg);
+  }
   __syncthreads();
 
   // ---- A. route this CTA's tokens ----
   for (int t = t0 + warp; t < t1; t += kRWarps) {
     int i0, i1;
     float w0, w1;
-    route_token(x, wg, t, H, E, lane, i0, i1, w0, w1);
+    route_token(x, wsrc, t, H, E, lane, i0, i1, w0, w1);
     if (lane == 0) {
       topk_idx[2 * t] = i0;
       topk_idx[2 * t + 1] = i1;
@@ -202,14 +216,22 @@ int grid_for(size_t work, int threads) {
 }
 
 
-int router_grid(int T) {
-  // co-resident CTAs of the cooperative launch (thread-safe static init; fixed for the device model)
-  static const int max_ctas = [] {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, router_fused_kernel, kRThreads, 0) != cudaSuccess)
-      per_sm = 1;
-    return per_sm * device_sm_count();
-  }();
+int router_grid(int T, size_t smem) {
+  // co-resident CTAs of the cooperative launch at this shared-memory size (per process; fixed for a device model)
+  static std::mutex mu;
+  static std::map<size_t, int> per_size;
+  int max_ctas;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = per_size.find(smem);
+    if (it == per_size.end()) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, router_fused_kernel, kRThreads, smem) != cudaSuccess)
+        per_sm = 1;
+      it = per_size.emplace(smem, per_sm * device_sm_count()).first;
+    }
+    max_ctas = it->second;
+  }
   int g = (T + kRWarps - 1) / kRWarps;  // ≥ one token per warp
   const int cap = device_sm_count() < max_ctas ? device_sm_count() : max_ctas;  // one wave: ≤ one CTA per SM
   if (g > cap) g = cap;
@@ -242,15 +264,21 @@ extern "C" int so_router_top2(const void* x, const void* w_gate, int T, int H, i
   float* w = topk_w ? topk_w : reinterpret_cast<float*>(ws + kRouterHdr + (size_t)T * 2 * sizeof(int32_t));
   cudaError_t e = cudaMemsetAsync(barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return (int)e;
-  const int grid = router_grid(T);
+  const size_t wbytes = (size_t)E * H * sizeof(__nv_bfloat16);
+  int stage_w = wbytes <= kRouterSmemMax ? 1 : 0;
+  const size_t smem = stage_w ? wbytes : 0;
+  if (stage_w) {
+    if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(router_fused_kernel), smem)) return rc;
+  }
+  const int grid = router_grid(T, smem);
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(w_gate);
   __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
   void* args[] = {&xb, &wb, &T, &H, &E, &idx, &w, &cta_counts, &barrier, &expert_offsets, &perm_token, &row_weight,
-                  &token_rows, &xp};
+                  &token_rows, &xp, &stage_w};
   // cooperative: the runtime guarantees every CTA is resident at once (the grid barrier needs it)
   e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(router_fused_kernel), dim3(grid), dim3(kRThreads),
-                                  args, 0, st);
+                                  args, smem, st);
   if (e != cudaSuccess) return (int)e;
   return SO_OK;
 }

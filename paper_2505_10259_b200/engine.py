@@ -189,6 +189,8 @@ class DecodeSession:
         self.res_first = [torch.empty(max(b.n, 1), dtype=torch.int32, pin_memory=True) for b in self.batches]
         self.rounds = 0
         self.committed_decode = 0
+        self.recycle = None   # (ctx0, t_last0, max_new): finished sequences restart (synthetic_context)
+        self.recycled = 0
 
 
 class Engine:
@@ -388,10 +390,19 @@ class Engine:
         self.drf_stream.synchronize()
         self._release_staging()
 
-    def synthetic_context(self, s: DecodeSession, ctx_len: int, max_new: int, seed: int = 0) -> None:
+    def synthetic_context(self, s: DecodeSession, ctx_len: int, max_new: int, seed: int = 0,
+                          recycle: bool = False) -> None:
         """Decode-only benchmark input: caches hold ``ctx_len`` random KV rows per
         sequence (as if prefilled), t_last random.  The prompt KV is an input
-        of the decode metric, resident in HBM before timing starts."""
+        of the decode metric, resident in HBM before timing starts.
+
+        ``recycle``: the steady state of a pool serving ``max_new``-token
+        requests (the reference's Workload, commits clamped to what is left,
+        simulator.py:213-214): a sequence that has generated ``max_new``
+        tokens restarts as a new request for the same ``ctx_len``-token prompt,
+        whose KV is still cached (a prefix-cache hit: its context rows are
+        kept, everything past them is overwritten).  Prefill is not decode
+        work; ``generate()`` times it end to end."""
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
         for kv in (s.tkv, s.dkv):
@@ -405,6 +416,8 @@ class Engine:
         s.ctx[:] = ctx_len
         s.remaining[:] = max_new
         s.active[:] = True
+        if recycle:
+            s.recycle = (s.ctx.copy(), s.t_last.copy(), int(max_new))
         if s.hist is not None:
             s.hist.random_(0, self.target.arch.vocab, generator=g)
             self._hist_write(s, np.arange(s.n_seq), s.ctx, s.t_last, self.drf_stream)
@@ -679,6 +692,10 @@ class Engine:
             if s.refill and s.remaining[i] <= 0:  # done: free the slot for the next prompt
                 s.active[i] = False
                 s.slot_prompt[i] = -1
+            elif s.recycle is not None and s.remaining[i] <= 0:  # done: the same prompt again (cached prefix)
+                ctx0, t0, new_tokens = s.recycle
+                s.ctx[i], s.t_last[i], s.remaining[i] = ctx0[i], t0[i], new_tokens
+                s.recycled += 1
         if new.size:
             first = s.res_first[bi][:new.size].numpy()
             for k, i in enumerate(new):

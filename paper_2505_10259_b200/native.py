@@ -229,7 +229,6 @@ def moe_combine(y_perm, token_rows, resid, out, stream=None):
 # ---------------------------------------------------------------- GEMMs ---
 
 _splitk_ws: dict[int, torch.Tensor] = {}  # stream handle → grow-only split-K scratch (one per enqueuing stream)
-_gemv_ws: dict[int, torch.Tensor] = {}    # stream handle → K5b scratch: arrival counters (zero between launches)
 _splitk_lock = threading.Lock()
 
 
@@ -239,15 +238,14 @@ def _stream_ws(pool: dict, need: int, stream: int, device) -> tuple[int, int]:
     with _splitk_lock:
         ws = pool.get(stream)
         if ws is None or ws.numel() < need:
-            # zero-filled once: K5b's per-tile arrival counters (every launch leaves them zero)
             ws = torch.zeros(max(need, 16 << 20), dtype=torch.uint8, device=device)
             pool[stream] = ws
     return ws.data_ptr(), ws.numel()
 
 
 def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
-    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (decode steps: the K5b stream-K
-    kernel; other skinny shapes: split-K over the SMs).
+    """out = epilogue(a[M,K] · b[N,K]ᵀ) on tcgen05 (decode steps: the K5c cluster
+    split-K kernel; other skinny shapes: split-K over the SMs).
     ``variant``: tile choice (0 = auto; see so_gemm_bf16_v) — tests and benchmarks only."""
     M, K = a.shape
     N = b.shape[-2]
@@ -255,11 +253,10 @@ def gemm(a, b, out, epilogue=EPI_BF16, aux=None, stream=None, variant: int = 0):
     _need(a, torch.bfloat16, "a")
     assert b.dtype == torch.bfloat16
     st = _stream(stream)
-    # K5b and split-K never share scratch: split-K's fp32 partials would land on
-    # the arrival counters K5b needs zero at launch
+    # decode steps go to K5c, which reduces in distributed shared memory (no scratch)
     gemv = variant in (0, 4) and epilogue != EPI_BF16_ROWSCALE and lib().so_gemv_workspace_bytes(M, N, K) > 0
     if gemv:
-        ws, ws_bytes = _stream_ws(_gemv_ws, int(lib().so_gemv_workspace_bytes(M, N, K)), st, a.device)
+        ws, ws_bytes = 0, 0
     elif variant != 3:
         ws, ws_bytes = _stream_ws(_splitk_ws, int(lib().so_gemm_workspace_bytes(M, N, K)), st, a.device)
     else:

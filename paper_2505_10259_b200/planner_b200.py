@@ -131,7 +131,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,
                  world: int = 1, allow_shards: bool = True, disk_budget: int = 0,
-                 kv_host_modes=(False,)) -> OffloadPlan:
+                 kv_host_modes=(False,), tokens_per_verify: float | None = None) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
@@ -156,7 +156,9 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     window of one batch's per-layer KV, host DRAM the pool, and every pass also
     moves the verified batch's KV host → GPU (the write-back uses the other
     link direction)."""
-    e_tok = expected_accepted(AcceptanceModel(acceptance_p, n_cand))
+    # commits per verification: E[k], or the caller's steady-state figure (clamped requests,
+    # acceptance.committed_per_verify) — a constant factor of every candidate's rate
+    e_tok = tokens_per_verify or expected_accepted(AcceptanceModel(acceptance_p, n_cand))
     max_len = ctx_len + max_new + n_cand + 2
     draft_w = resident_bytes(draft, True)
     best = None

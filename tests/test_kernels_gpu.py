@@ -322,12 +322,24 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
     (64, 4, 2, [33, 1], [3, 200], 64),                       # mixed
     (128, 32, 8, [9, 1, 40], [300, 31, 0], 8),               # small pages: 4 TMA boxes per tile
     (64, 4, 2, [5, 3], [20, 7], 5),                          # odd pages: cp.async staging only
+    (128, 8, 8, [9, 3], [200, 70], 16),                      # G = 1
+    (128, 64, 8, [9, 16, 2], [129, 0, 64], 16),              # G = 8: 16 positions per 128-row unit
+    (128, 32, 8, [300, 45], [0, 500], 16),                   # long prefill rows: many row tiles per head
+    (128, 48, 8, [9] * 160, list(range(0, 800, 5)), 16),     # 1280 units > 148 SMs: persistent O/Q buffers
 ])
 @pytest.mark.parametrize("attn_variant", [0, 1, 2], ids=["tma", "cp_async", "tcgen05"])
 def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
     if attn_variant == 2 and (dh != 128 or not (ps >= 8 and (64 % ps == 0 if ps <= 64 else ps % 64 == 0))):
-        pytest.skip("K6b covers dh 128 with pages dividing 64 (or multiples of 64)")
+        pytest.skip("K6c covers dh 128 with pages dividing 64 (or multiples of 64)")
     _check_attn(dh, hq, hkv, qlens, kvbs, ps, attn_variant)
+
+
+@pytest.mark.parametrize("attn_variant", [0, 2], ids=["tma", "tcgen05"])
+@pytest.mark.parametrize("hq,qlens,kvbs", [(48, [9] * 6, [503, 40, 700, 1, 64, 300]), (32, [200, 7], [0, 900])])
+def test_attn_paged_growing_scores(hq, qlens, kvbs, attn_variant):
+    """Scores that grow with the key index move every row's running max tile
+    after tile, past K6c's 2^8 lazy-rescale threshold: O is rescaled in TMEM."""
+    _check_attn(128, hq, 8, qlens, kvbs, 16, attn_variant, key_growth=3.0)
 
 
 @pytest.mark.parametrize("qlens,kvbs,hq", [
@@ -341,7 +353,7 @@ def test_attn_tcgen05_larger(qlens, kvbs, hq):
     _check_attn(128, hq, 8, qlens, kvbs, 16, 2)
 
 
-def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):
+def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0, key_growth=0.0):
     bs = len(qlens)
     max_len = max(q + k for q, k in zip(qlens, kvbs))
     pps = (max_len + ps - 1) // ps + 1
@@ -349,11 +361,15 @@ def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):
     g = torch.Generator(device=DEV).manual_seed(dh + bs)
     kc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
     vc = torch.randn(npages, hkv, ps, dh, device=DEV, generator=g).to(torch.bfloat16)
-    # unwritten cache slots may hold anything: poison every slot past each
-    # sequence's keys with NaN — the kernel must never let them reach P·V
-    bt_host = None
     perm = torch.randperm(npages, device=DEV, generator=g).to(torch.int32)  # scattered pages
     bt = perm.view(bs, pps)
+    if key_growth:  # later keys score ever higher: the running row max keeps moving (K6c's lazy rescale)
+        pos = torch.arange(pps * ps, device=DEV, dtype=torch.float32)
+        f = (1.0 + key_growth * pos / 64.0).view(pps, 1, ps, 1)
+        for s_ in range(bs):
+            kc[bt[s_].long()] = (kc[bt[s_].long()].float() * f).to(torch.bfloat16)
+    # unwritten cache slots may hold anything: poison every slot past each
+    # sequence's keys with NaN — the kernel must never let them reach P·V
     bt_host = bt.long().cpu().numpy()
     for s in range(bs):
         nk = qlens[s] + kvbs[s]
@@ -376,7 +392,7 @@ def _check_attn(dh, hq, hkv, qlens, kvbs, ps, variant=0):
 @pytest.mark.parametrize("gemm_variant", [1, 0], ids=["split_k", "auto"])
 def test_gemm_splitk_skinny(M, N, K, gemm_variant):
     """Draft decode-step shapes: K split over the SMs into fp32 partials, then
-    one reduce applies the epilogue (variant 1), or the auto choice (K5b for
+    one reduce applies the epilogue (variant 1), or the auto choice (K5c for
     M ≤ 128) — every epilogue against an fp32 reference."""
     assert native.lib().so_gemm_workspace_bytes(M, N, K) > 0  # the split is taken for these shapes
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
@@ -401,7 +417,7 @@ def test_gemm_splitk_skinny(M, N, K, gemm_variant):
     _bf16_close(outs, torch.nn.functional.silu(a.float() @ wg.float().T) * (a.float() @ wu.float().T))
 
 
-# ------------------------------------------------------------- K5b decode steps ---
+# ------------------------------------------------------------- K5c decode steps ---
 
 @pytest.mark.parametrize("M,N,K,epi", [
     (64, 6144, 4096, 0),          # Mistral-7B QKV decode step
@@ -410,15 +426,17 @@ def test_gemm_splitk_skinny(M, N, K, gemm_variant):
     (64, 4096, 14336, 2),         # down + residual (tiles split over many CTAs)
     (112, 4096, 14336, 2),
     (128, 32768, 4096, 1),        # LM head (fp32 logits)
-    (1, 128, 64, 0),              # one row, one tile, one k-block
-    (17, 384, 192, 3),            # ragged rows, 3 tiles of 3 k-blocks
-    (33, 1024, 640, 1),
+    (1, 128, 128, 0),             # one row, one tile, two k-blocks (cluster of 1)
+    (17, 384, 256, 3),            # ragged rows, 3 tiles: clusters of 2
+    (33, 1024, 640, 1),           # 8 tiles, clusters of 5 over 10 k-blocks
+    (16, 8192, 6144, 0),          # 8x22B QKV at a tiny verify batch
+    (128, 6144, 6144, 2),
     (100, 256, 8192, 0),          # two tiles, long K: every CTA a slice of one tile
 ])
 def test_gemv_decode_step(M, N, K, epi):
-    """The stream-K decode-step kernel (so_gemv_bf16, variant 4) against fp32
-    torch; run twice: bitwise deterministic, and the per-tile arrival counters
-    are left zero by the first launch (the second is just as correct)."""
+    """The decode-step kernel (so_gemv_bf16, variant 4: cluster split-K, DSMEM
+    reduction) against fp32 torch; run twice: bitwise deterministic (fixed
+    peer order in the reduction)."""
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N + K)
     a = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
     b = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
@@ -447,21 +465,19 @@ def test_gemv_decode_step(M, N, K, epi):
         _bf16_close(outs[0], ref)
 
 
-def test_gemv_shared_workspace_across_shapes():
-    """One K5b workspace serves every shape in turn (the verify pass: QKV, O,
-    then the 256-tile LM head): a narrow shape's fp32 partials must never land
-    on the arrival counters a wider shape needs zero (regression: the LM head of
-    an 18-row verify read stale counters after the O projection)."""
+def test_gemv_back_to_back_shapes():
+    """The verify pass's sequence of decode-step shapes (QKV, O, the 256-tile LM
+    head, …) back to back on one stream, every output against fp32 torch
+    (regression: the 18-row verify LM head once read state a narrower shape
+    had left behind)."""
     g = torch.Generator(device=DEV).manual_seed(5)
-    ws = torch.zeros(max(native.lib().so_gemv_workspace_bytes(18, N, 6144) for N in (6144, 8192, 32768)),
-                     dtype=torch.uint8, device=DEV)
     for N, epi in [(8192, native.EPI_BF16), (6144, native.EPI_F32), (32768, native.EPI_F32), (6144, native.EPI_F32),
                    (32768, native.EPI_F32)]:
         a = torch.randn(18, 6144, device=DEV, generator=g).to(torch.bfloat16)
         b = (torch.randn(N, 6144, device=DEV, generator=g) / math.sqrt(6144)).to(torch.bfloat16)
         out = torch.empty(18, N, dtype=torch.float32 if epi == native.EPI_F32 else torch.bfloat16, device=DEV)
         native._check(native.lib().so_gemv_bf16(a.data_ptr(), b.data_ptr(), 18, N, 6144, out.data_ptr(), N, epi,
-                                                None, ws.data_ptr(), ws.numel(), native._stream(None)), "gemv")
+                                                None, None, 0, native._stream(None)), "gemv")
         ref = a.float() @ b.float().T
         if epi == native.EPI_F32:
             torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())

@@ -3,7 +3,7 @@
 
     python tools/gemm_bench.py > gpurun_out/gemm_bench.json
 
-CUDA-event timing, 3 warm-up + 20 timed launches, best of 3 interleaved trials per variant; TFLOP/s against
+CUDA-event timing of 20 launches captured in one CUDA graph (device time, no per-call host overhead), 3 warm-up launches, best of 3 interleaved trials per variant; TFLOP/s against
 the measured cuBLAS bf16 burst peak (MEASURED_PEAKS.json).  Weights are
 re-used across launches (L2-resident up to 126 MB; the MoE shapes exceed it).
 """
@@ -25,12 +25,25 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
 
 
 def timed(fn, reps=10):
-    for _ in range(3):
-        fn()
+    """Seconds per call of ``fn``: ``reps`` calls captured in one CUDA graph and
+    replayed, so the figure is device time — a per-call Python/ctypes enqueue
+    (≈ 10 µs) would otherwise bound any kernel shorter than that."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(reps):
-        fn()
+    g.replay()
     b.record()
     b.synchronize()
     return a.elapsed_time(b) / reps * 1e-3
@@ -58,6 +71,9 @@ def main():
         ("draft decode step gate_up (64 seqs)", 64, 28672, 4096, native.EPI_SWIGLU, 0),
         ("draft decode step down (64 seqs)", 64, 4096, 14336, native.EPI_BF16_RESID, 0),
         ("draft decode step down (112 seqs)", 112, 4096, 14336, native.EPI_BF16_RESID, 0),
+        ("draft decode step QKV (128 seqs)", 128, 6144, 4096, native.EPI_BF16, 0),
+        ("draft decode step O (128 seqs)", 128, 4096, 4096, native.EPI_BF16_RESID, 0),
+        ("draft decode step LM head (64 seqs)", 64, 32768, 4096, native.EPI_F32, 0),
     ]
     for name, M, N, K, epi, E in shapes:
         if only and only not in name:
@@ -93,7 +109,7 @@ def main():
         res = {"shape": name, "M": M, "N": N, "K": K, "weight_copies_cycled": copies}
         variants = ((3, "tile_per_cta_auto"), (0, "persistent_auto"), (1, "cta1"), (2, "cta_pair"))
         if M <= 128 and not E:
-            variants = ((3, "tile_per_cta_auto"), (1, "splitk_cta1"), (4, "gemv_streamk"))
+            variants = ((3, "tile_per_cta_auto"), (1, "splitk_cta1"), (4, "k5c_cluster_splitk"))
         best = {}
         for _ in range(3):  # interleaved trials, best of 3 (clocks drift under the power cap)
             for variant, label in variants:
