@@ -55,6 +55,21 @@ constexpr uint32_t kTmemCols = 512;          // S: 2 × 64 columns at 0; O: 2 ×
 constexpr uint32_t kOCol = 128;
 constexpr float kRescaleLog2 = 8.0f;         // lazy max: rescale only past a 2^8 growth
 
+#ifdef SO_ATTN_TRACE
+// debug build only (make EXTRA=-DSO_ATTN_TRACE): per CTA, cycles each role spent in each wait
+// (slot = wait site) plus the role's total cycles; read with so_attn_trace_copy
+__device__ unsigned long long g_attn_trace[1024][16];
+#define AW(slot, call)                                                         \
+  do {                                                                         \
+    const long long t0_ = clock64();                                           \
+    call;                                                                      \
+    if (blockIdx.x < 1024 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64)) \
+      g_attn_trace[blockIdx.x][slot] += clock64() - t0_;                      \
+  } while (0)
+#else
+#define AW(slot, call) call
+#endif
+
 struct Unit {
   int seq, kvh, p0, np, kvb, qs, n_keys, n_kt;
   bool live;
@@ -178,6 +193,9 @@ __global__ void __launch_bounds__(kAThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
+#ifdef SO_ATTN_TRACE
+  const long long t_start = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const Unit x = unit_info(u, hkv, row_tiles, P, q_start, kv_before);
         if (!x.live) continue;
         const uint32_t qb = uq & 1;
-        mbar_wait_guard(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
+        AW(0, mbar_wait_guard(&q_empty[qb], ((uq >> 1) & 1) ^ 1));
         mbar_expect_tx(&q_full[qb], (uint32_t)(x.np * G * 256));
         uint8_t* q_dst = sQ + qb * kQBytes;
         for (int j = 0; j < x.np; ++j) {
@@ -214,14 +232,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
           if (kt < x.n_kt) {
             const uint32_t t = it + kt;
             const int s = t % kKStages;
-            mbar_wait_guard(&k_empty[s], ((t / kKStages) & 1) ^ 1);
+            AW(1, mbar_wait_guard(&k_empty[s], ((t / kKStages) & 1) ^ 1));
             mbar_expect_tx(&k_full[s], kKBytes);
             load_tile(&tmK, sK + s * kKBytes, &k_full[s], kt);
           }
           if (kt > 0) {
             const uint32_t t = it + kt - 1;
             const int s = t % kVStages;
-            mbar_wait_guard(&v_empty[s], ((t / kVStages) & 1) ^ 1);
+            AW(2, mbar_wait_guard(&v_empty[s], ((t / kVStages) & 1) ^ 1));
             mbar_expect_tx(&v_full[s], kKBytes);
             load_tile(&tmV, sV + s * kKBytes, &v_full[s], kt - 1);
           }
@@ -239,8 +257,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
       uint32_t it = 0, uq = 0;  // global tile counter (ring stage, S/P buffer), unit counter (Q/O buffer)
       auto issue_s = [&](uint32_t t, uint32_t q0) {
         const int s = t % kKStages;
-        mbar_wait_guard(&k_full[s], (t / kKStages) & 1);
-        mbar_wait_guard(&s_empty[t & 1], ((t >> 1) & 1) ^ 1);
+        AW(3, mbar_wait_guard(&k_full[s], (t / kKStages) & 1));
+        AW(4, mbar_wait_guard(&s_empty[t & 1], ((t >> 1) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t k0 = smem_u32(sK + s * kKBytes);
 #pragma unroll
@@ -256,14 +274,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const uint32_t qb = uq & 1, ob = uq & 1;
         const uint32_t q0 = smem_u32(sQ + qb * kQBytes);
         const uint32_t o_tm = tmem_base + kOCol + ob * kDH;
-        mbar_wait_guard(&q_full[qb], (uq >> 1) & 1);
+        AW(5, mbar_wait_guard(&q_full[qb], (uq >> 1) & 1));
         issue_s(it, q0);
-        mbar_wait_guard(&o_empty[ob], ((uq >> 1) & 1) ^ 1);  // unit uq−2's epilogue has read this O buffer
+        AW(6, mbar_wait_guard(&o_empty[ob], ((uq >> 1) & 1) ^ 1));  // unit uq−2's epilogue has read this O buffer
         for (int kt = 0; kt < x.n_kt; ++kt, ++it) {
           if (kt + 1 < x.n_kt) issue_s(it + 1, q0);
           else umma_commit(&q_empty[qb]);  // the unit's last S MMA: Q may be replaced once it completes
-          mbar_wait_guard(&v_full[it % kVStages], (it / kVStages) & 1);
-          mbar_wait_guard(&p_full[it & 1], (it >> 1) & 1);
+          AW(7, mbar_wait_guard(&v_full[it % kVStages], (it / kVStages) & 1));
+          AW(8, mbar_wait_guard(&p_full[it & 1], (it >> 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t v0 = smem_u32(sV + (it % kVStages) * kKBytes);
           const uint32_t p0 = smem_u32(sP + (it & 1) * kPBytes);
@@ -297,7 +315,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       float m_ref = -INFINITY, l = 0.f;
       for (int kt = 0; kt < x.n_kt; ++kt, ++it) {
         // ---- this thread's 32 S values of the tile ----
-        mbar_wait_guard(&s_full[it & 1], (it >> 1) & 1);
+        AW(9, mbar_wait_guard(&s_full[it & 1], (it >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float sv[32];
         {
@@ -329,7 +347,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
           // rescale the warp's rows of O (its 64-column half) in TMEM once the previous tile's P·V has
           // landed — warp-wide (tcgen05.ld/st are .sync.aligned); rows that keep their max scale by 1
           const uint32_t pt = it - 1;
-          mbar_wait_guard(&p_empty[pt & 1], (pt >> 1) & 1);
+          AW(10, mbar_wait_guard(&p_empty[pt & 1], (pt >> 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int c = 0; c < 64; c += 32) {
@@ -360,14 +378,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
           const int vr = row & (kTKeys - 1);
           if (keep < kTKeys && vr >= keep) {
             // V(t) lands after S(t) is read (the producer runs K ahead): wait for it
-            mbar_wait_guard(&v_full[it % kVStages], (it / kVStages) & 1);
+            AW(11, mbar_wait_guard(&v_full[it % kVStages], (it / kVStages) & 1));
             uint8_t* v_row = sV + (it % kVStages) * kKBytes + (row >> 6) * kHalf + vr * 128;
 #pragma unroll
             for (int c = 0; c < 4; ++c) reinterpret_cast<int4*>(v_row)[half * 4 + c] = make_int4(0, 0, 0, 0);
           }
         }
         // ---- P (bf16) → shared memory once the buffer's previous P·V is done (K-major SWIZZLE_128B) ----
-        mbar_wait_guard(&p_empty[it & 1], ((it >> 1) & 1) ^ 1);
+        AW(12, mbar_wait_guard(&p_empty[it & 1], ((it >> 1) & 1) ^ 1));
         uint8_t* pb = sP + (it & 1) * kPBytes + row * 128;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -383,7 +401,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       xsum[half * kQRows + row] = l;
       softmax_sync();
       l += xsum[(half ^ 1) * kQRows + row];
-      mbar_wait_guard(&o_full[ob], (uq >> 1) & 1);
+      AW(13, mbar_wait_guard(&o_full[ob], (uq >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float o[64];
 #pragma unroll
@@ -413,6 +431,10 @@ __global__ void __launch_bounds__(kAThreads, 1)
       ++uq;
     }
   }
+#ifdef SO_ATTN_TRACE
+  if (threadIdx.x == 64 && blockIdx.x < 1024) g_attn_trace[blockIdx.x][14] += clock64() - t_start;
+  if (threadIdx.x == 32 && blockIdx.x < 1024) g_attn_trace[blockIdx.x][15] += clock64() - t_start;
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -473,3 +495,15 @@ extern "C" int so_attn_paged_tc(const void* q, const void* k_cache, const void* 
   SO_CHECK_LAUNCH();
   return SO_OK;
 }
+
+#ifdef SO_ATTN_TRACE
+extern "C" int so_attn_trace_copy(void* host, size_t bytes, int reset) {
+  if (bytes > sizeof(g_attn_trace)) bytes = sizeof(g_attn_trace);
+  int rc = (int)cudaMemcpyFromSymbol(host, g_attn_trace, bytes);
+  if (reset) {
+    static unsigned long long zero[1024][16];
+    cudaMemcpyToSymbol(g_attn_trace, zero, sizeof(zero));
+  }
+  return rc;
+}
+#endif

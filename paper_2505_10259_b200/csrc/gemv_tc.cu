@@ -52,11 +52,16 @@ __device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
   return r;
 }
 
-__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+// 16-B asynchronous store into (possibly another CTA's) shared memory; completion is counted in bytes on
+// the destination CTA's mbarrier (complete_tx), so the receiver needs no round trip to the sender
+__device__ __forceinline__ void st_async4(uint32_t cluster_addr, const uint32_t* v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cluster_addr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(cluster_bar)
+               : "memory");
 }
 
-// wait with cluster-scope acquire: the peers' shared-memory writes before their release-arrive are visible
+// wait with cluster-scope acquire: the data the peers' asynchronous stores delivered is visible
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0, spins = 0;
   const uint32_t a = smem_u32(bar);
@@ -70,12 +75,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "memory");
     if (++spins > (1u << 26)) __trap();
   } while (!done);
-}
-
-__device__ __forceinline__ float ld_dsmem(uint32_t cluster_addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
-  return v;
 }
 
 #ifdef SO_GEMV_TRACE
@@ -123,18 +122,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
   // two accumulators, each a power of two ≥ 32 columns (tcgen05.ld reads 32 at a time)
   const uint32_t acc_cols = NT <= 32 ? 64 : (NT <= 64 ? 128 : 256);
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
   uint8_t* sW = smem;
   uint8_t* sX = smem + (size_t)stages * kWBytes;
-  float* red = reinterpret_cast<float*>(smem + (size_t)stages * stage_bytes);  // partial tile [NT][128] fp32
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + (size_t)NT * kWRows);
+  // receive buffer of the rows this CTA reduces: [CS senders][its rows][NT + 4] fp32 (a row's tokens
+  // contiguous for 16-B loads; the 4-float pad spreads the rows over the banks)
+  const int ldr = NT + 4;
+  float* red = reinterpret_cast<float*>(smem + (size_t)stages * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + (size_t)(kWRows + kMaxCluster) * ldr);
   uint64_t* empty = full + kGMaxStages;
   uint64_t* tmem_full = empty + kGMaxStages;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* ready = tmem_empty + 2;     // every CTA's partial of the tile is in its shared memory
-  uint64_t* consumed = ready + 1;       // every CTA has read this CTA's partial
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(consumed + 1);
+  uint64_t* ready = tmem_empty + 2;     // every sender's slice of the rows I reduce has landed (tx bytes)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ready + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -147,8 +148,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 4);
     }
-    mbar_init(ready, 4 * CS);
-    mbar_init(consumed, 4 * CS);
+    mbar_init(ready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -210,85 +210,78 @@ __global__ void __launch_bounds__(kGThreads, 1)
       gtrace(3);
     }
   } else {
-    // ===== epilogue warps: TMEM partial → shared memory → cluster reduction of 1/CS of the rows =====
+    // ===== epilogue warps: TMEM partial → pushed to the row's owner CTA → owner reduces its rows =====
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int tid = threadIdx.x - 64;  // 0..127
-    const uint32_t red_s = smem_u32(red);
-    uint32_t red_peer[kMaxCluster];  // every peer's partial tile (own rank included), cluster addresses
-#pragma unroll
-    for (int p = 0; p < kMaxCluster; ++p) red_peer[p] = CS > 1 && p < (int)CS ? map_peer(red_s, p) : red_s;
     const bool swiglu = EPI == SO_EPI_SWIGLU;
-    // this CTA's share of the reduction: rows [r_lo, r_hi) of the tile (SwiGLU: gate rows of the lower
+    // row ownership: CTA r reduces rows [r_lo, r_hi) of the tile (SwiGLU: gate rows of the lower
     // half, each with its up row + 64)
     const int R = swiglu ? kWRows / 2 : kWRows;
     const int r_lo = (int)((long)R * rank / CS), r_hi = (int)((long)R * (rank + 1) / CS);
     const int nr = r_hi - r_lo;
+    // where MY row goes: owner CTA, its local row index in each sender's block, the block's row count
+    const int key = swiglu ? (row & 63) : row;
+    int owner = (int)(((long)key * CS) / R);
+    while (owner > 0 && (int)((long)R * owner / CS) > key) --owner;
+    while (owner + 1 < (int)CS && (int)((long)R * (owner + 1) / CS) <= key) ++owner;
+    const int o_lo = (int)((long)R * owner / CS), o_nr = (int)((long)R * (owner + 1) / CS) - o_lo;
+    const int blk_rows = swiglu ? 2 * o_nr : o_nr;
+    const int li = key - o_lo + ((swiglu && row >= 64) ? o_nr : 0);
+    // receive buffer [CS senders][blk_rows][ldr] on the owner; my slice starts at sender block `rank`
+    const uint32_t dst = (CS > 1 ? map_peer(smem_u32(red), owner) : smem_u32(red)) +
+                         (uint32_t)(((int)rank * blk_rows + li) * ldr * 4);
+    const uint32_t dst_bar = CS > 1 ? map_peer(smem_u32(ready), owner) : smem_u32(ready);
+    const int my_blk = swiglu ? 2 * nr : nr;                  // rows per sender block that I receive
+    const int quads = (M + 3) / 4;                            // 16-B token quads per row
+    const uint32_t tx = (uint32_t)(CS * my_blk * quads * 16);  // bytes all senders push to me, per tile
     uint32_t acc_i = 0;
     for (int tile = cluster; tile < n_tiles; tile += n_clusters, ++acc_i) {
       const uint32_t buf = acc_i & 1, aph = (acc_i >> 1) & 1;
-      if (acc_i > 0) mbar_wait_cluster(consumed, (acc_i - 1) & 1);  // peers are done with my previous partial
+      if (acc_i > 0) asm volatile("bar.sync 2, 128;" ::: "memory");  // CS == 1: my previous tile's reads done
+      if (tid == 0) mbar_expect_tx(ready, tx);                       // arm before or after the pushes land
       mbar_wait_guard(&tmem_full[buf], aph);
       if (tid == 0) gtrace(4);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tbase = tmem_base + buf * (acc_cols / 2) + ((uint32_t)(quarter * 32) << 16);
-      for (int c = 0; c < NT; c += 32) {
+      for (int c = 0; c < M; c += 32) {
         uint32_t r[32];
         tmem_ld32(tbase + c, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c + j < NT) red[(size_t)(c + j) * kWRows + row] = __uint_as_float(r[j]);  // token-major: conflict-free
+        for (int j = 0; j < 8; ++j)
+          if ((c >> 2) + j < quads)  // 16-B asynchronous stores into the owner's shared memory, counted on its barrier
+            st_async4(dst + (uint32_t)((c + 4 * j) * 4), r + 4 * j, dst_bar);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[buf])) : "memory");
-        for (uint32_t p = 0; p < CS; ++p)  // release: my partial is readable by every peer
-          arrive_remote(CS > 1 ? map_peer(smem_u32(ready), p) : smem_u32(ready));
-      }
-      mbar_wait_cluster(ready, acc_i & 1);
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[buf])) : "memory");
+      mbar_wait_cluster(ready, acc_i & 1);  // every sender's slice of my rows has landed
       if (tid == 0) gtrace(5);
       const int n0 = tile * kWRows;
-      // fixed peer order 0..CS-1: the sum does not depend on arrival order; 4 outputs per
-      // thread per step, every peer's DSMEM load of them issued before the adds
-      const int total = nr * M;
-      for (int base = tid; base < total; base += 4 * 128) {
-        float v[4][kMaxCluster], u[4][kMaxCluster];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int idx = base + q * 128;
-          if (idx < total) {
-            const uint32_t off = (uint32_t)(((idx / nr) * kWRows + r_lo + idx % nr) * 4);
-#pragma unroll
-            for (int p = 0; p < kMaxCluster; ++p)
-              if (p < (int)CS) {
-                v[q][p] = ld_dsmem(red_peer[p] + off);
-                if (swiglu) u[q][p] = ld_dsmem(red_peer[p] + off + 64 * 4);
-              }
+      // fixed sender order 0..CS-1 (deterministic); thread → (row, 4 tokens), consecutive threads on
+      // consecutive rows (coalesced output stores); local 16-B loads
+      for (int w = tid; w < nr * quads; w += 128) {
+        const int rl = w % nr, q = w / nr;
+        float4 sv = make_float4(0.f, 0.f, 0.f, 0.f), su = sv;
+        for (int p = 0; p < (int)CS; ++p) {
+          const float* src = red + (size_t)(p * my_blk + rl) * ldr + 4 * q;
+          const float4 v = *reinterpret_cast<const float4*>(src);
+          sv.x += v.x; sv.y += v.y; sv.z += v.z; sv.w += v.w;
+          if (swiglu) {
+            const float4 u = *reinterpret_cast<const float4*>(src + (size_t)nr * ldr);
+            su.x += u.x; su.y += u.y; su.z += u.z; su.w += u.w;
           }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int idx = base + q * 128;
-          if (idx < total) {
-            float sv = 0.f, su = 0.f;
-#pragma unroll
-            for (int p = 0; p < kMaxCluster; ++p)
-              if (p < (int)CS) {
-                sv += v[q][p];
-                if (swiglu) su += u[q][p];
-              }
-            const int rl = r_lo + idx % nr;
-            // SwiGLU: gate row rl ↔ output column n0/2 + rl (64-row interleave of the packed FFN)
-            store_out<EPI>(idx / nr, swiglu ? n0 / 2 + rl : n0 + rl, sv, su, C, ldc, aux);
-          }
-        }
+        // SwiGLU: gate row ↔ output column n0/2 + row (64-row interleave of the packed FFN)
+        const int n = swiglu ? n0 / 2 + r_lo + rl : n0 + r_lo + rl;
+        const int m = 4 * q;
+        store_out<EPI>(m, n, sv.x, su.x, C, ldc, aux);
+        if (m + 1 < M) store_out<EPI>(m + 1, n, sv.y, su.y, C, ldc, aux);
+        if (m + 2 < M) store_out<EPI>(m + 2, n, sv.z, su.z, C, ldc, aux);
+        if (m + 3 < M) store_out<EPI>(m + 3, n, sv.w, su.w, C, ldc, aux);
       }
-      __syncwarp();
       if (tid == 0) gtrace(6);
-      if (lane == 0)  // I am done reading every peer's partial
-        for (uint32_t p = 0; p < CS; ++p) arrive_remote(CS > 1 ? map_peer(smem_u32(consumed), p) : smem_u32(consumed));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -306,7 +299,7 @@ struct GemvPlan {
 };
 
 size_t smem_bytes(int NT, int stages) {
-  return 1024 + (size_t)stages * (kWBytes + NT * kTmaBoxK * 2) + (size_t)NT * kWRows * 4 + 512;
+  return 1024 + (size_t)stages * (kWBytes + NT * kTmaBoxK * 2) + (size_t)(NT + 4) * (kWRows + kMaxCluster) * 4 + 512;
 }
 
 // how many clusters of `cs` CTAs (this kernel, this shared-memory size) the GPU holds at once: clusters
@@ -348,7 +341,7 @@ GemvPlan plan_gemv(int M, int N, int K) {
   p.NT = ((M + 15) / 16) * 16;
   if (p.NT < 16) p.NT = 16;
   const int stage = kWBytes + p.NT * kTmaBoxK * 2;
-  p.stages = (int)((kGSmemBudget - (size_t)p.NT * kWRows * 4 - 2048) / stage);
+  p.stages = (int)((kGSmemBudget - (size_t)(p.NT + 4) * (kWRows + kMaxCluster) * 4 - 2048) / stage);
   if (p.stages > kGMaxStages) p.stages = kGMaxStages;
   p.n_tiles = N / kWRows;
   const int num_kb = K / kTmaBoxK;
