@@ -202,18 +202,22 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
                   const int32_t* q_start, const int32_t* kv_before,
                   int bs, int max_q, int hq, int hkv, int dh, int page_size,
                   float scale, void* out, void* stream);
-/* Same with the kernel an explicit argument: 0 = TMA boxes issued by one
- * thread where the page size allows (pages of ≤ 32 slots dividing 32, or
- * multiples of 32), else cp.async (so_attn_paged's choice); 1 = cp.async by
- * every thread; 2 = K6b, the tcgen05 kernel (so_attn_paged_tc). */
+/* Same with the kernel an explicit argument: 0 = auto (so_attn_paged's
+ * choice): TMA boxes issued by one thread where the page size allows (pages of
+ * ≤ 32 slots dividing 32, or multiples of 32), else cp.async; 1 = cp.async by
+ * every thread; 2 = K6c, the tcgen05 kernel (so_attn_paged_tc); 3 = K6d, a
+ * CUDA-core streaming kernel for decode steps (max_q == 1, hq/hkv ≤ 8: CTA per
+ * sequence × kv head, lane-per-key scores, cp.async-staged V, warps merged in
+ * shared memory) where eligible, else auto. */
 int so_attn_paged_v(const void* q, const void* k_cache, const void* v_cache,
                     const int32_t* block_table, int max_pages,
                     const int32_t* q_start, const int32_t* kv_before,
                     int bs, int max_q, int hq, int hkv, int dh, int page_size,
                     float scale, void* out, int variant, void* stream);
-/* K6b — the same attention on the tcgen05 tensor cores: persistent CTAs over
- * (sequence, kv head, 128 query rows) units, S = Q·Kᵀ and P·V accumulated in
- * TMEM, TMA-staged K/V tiles of 64 keys, one query row per softmax thread.
+/* K6c — the same attention on the tcgen05 tensor cores: persistent CTAs over
+ * (sequence, kv head, 128 query rows) units, S = Q·Kᵀ in TMEM, O accumulated
+ * in TMEM (lazy rescale), TMA-staged Q and K/V tiles of 64 keys, two softmax
+ * threads per query row.
  * dh = 128, hq/hkv ≤ 128, page_size ≥ 8 dividing 64 or a multiple of 64. */
 int so_attn_paged_tc(const void* q, const void* k_cache, const void* v_cache,
                      const int32_t* block_table, int max_pages,

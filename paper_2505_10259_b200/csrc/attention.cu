@@ -460,6 +460,180 @@ int launch(const void* q, const void* k, const void* v, const int32_t* bt, int m
   return SO_OK;
 }
 
+// K6d — decode-step attention (one query position per sequence: the draft's n_cand decode steps,
+// costmodel.py:53-57).  The G query heads of a kv head share one pass over its keys; the work is
+// the K/V bytes, so the kernel is a streaming reduction on the CUDA cores rather than a tensor-core
+// tile with G of 64 rows live:
+//   CTA = (sequence, kv head), 8 warps; warp w takes 32-key chunks w, w+8, …;
+//   scores: lane = key — the lane's 256-B K row in 16-B loads, G dot products against the queries
+//           in shared memory (broadcast reads), online softmax per head with warp reductions;
+//   P·V:    the chunk's V rows are staged into the warp's shared memory by cp.async (lane = key,
+//           issued before the score loads, so K and V of a chunk are in flight together), then
+//           lane = 4 of the 128 dims reads them key by key, p of the key broadcast by shuffle;
+//   the 8 warps' (m, l, O) merge through shared memory at the end.
+constexpr int kDecWarps = 8;
+constexpr int kDecGMax = 8;
+
+template <int DH>
+__global__ void __launch_bounds__(32 * kDecWarps, 2) attn_decode_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
+    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ block_table, int max_pages,
+    const int32_t* __restrict__ q_start, const int32_t* __restrict__ kv_before, int hq, int hkv, int page_size,
+    float scale_log2, __nv_bfloat16* __restrict__ out) {
+  constexpr int kDPL = DH / 32;  // dims per lane in P·V
+  const int s = blockIdx.x / hkv, h = blockIdx.x % hkv;
+  const int qs = q_start[s];
+  if (q_start[s + 1] == qs) return;  // no query row for this sequence
+  const int G = hq / hkv;
+  const int n_keys = kv_before[s] + 1;  // the row at position kv_before[s] sees keys [0, kv_before[s]]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ __align__(16) __nv_bfloat16 sq[kDecGMax][DH];
+  __shared__ float sm[kDecWarps][kDecGMax], sl[kDecWarps][kDecGMax];
+  extern __shared__ __align__(16) uint8_t dec_smem[];
+  __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(dec_smem) + (size_t)warp * 32 * DH;  // this warp's V rows
+  float (*so)[kDecGMax][DH] = reinterpret_cast<float (*)[kDecGMax][DH]>(dec_smem);      // merge (after the loop)
+  for (int i = threadIdx.x; i < G * DH / 8; i += blockDim.x)
+    reinterpret_cast<int4*>(&sq[0][0])[i] = reinterpret_cast<const int4*>(q + ((size_t)qs * hq + (size_t)h * G) * DH)[i];
+  __syncthreads();
+  const int32_t* bt = block_table + (size_t)s * max_pages;
+  float m[kDecGMax], l[kDecGMax], o[kDecGMax][kDPL];
+#pragma unroll
+  for (int g = 0; g < kDecGMax; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int d = 0; d < kDPL; ++d) o[g][d] = 0.f;
+  }
+  for (int c0 = warp * 32; c0 < n_keys; c0 += kDecWarps * 32) {
+    // ---- scores: lane = key ----
+    const int key = c0 + lane;
+    const bool valid = key < n_keys;
+    const size_t krow = valid ? (((size_t)bt[key / page_size] * hkv + h) * page_size + key % page_size) * DH : 0;
+    if (valid) {  // this key's V row → the warp's staging rows, in flight while the scores are computed
+#pragma unroll
+      for (int c = 0; c < DH / 8; ++c) cp_async16(sv + (size_t)lane * DH + 8 * c, v_cache + krow + 8 * c);
+    }
+    cp_commit();
+    float sc[kDecGMax];
+#pragma unroll
+    for (int g = 0; g < kDecGMax; ++g) sc[g] = 0.f;
+    if (valid) {
+      const int4* kr = reinterpret_cast<const int4*>(k_cache + krow);
+      // the row in two halves of ≤ 8 16-B loads (all of a half in flight before its FMAs)
+#pragma unroll
+      for (int c0 = 0; c0 < DH / 8; c0 += 8) {
+        int4 kv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c0 + c < DH / 8) kv[c] = __ldg(kr + c0 + c);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c0 + c >= DH / 8) break;
+          float kf[8];
+          unpack8(kv[c], kf);
+#pragma unroll
+          for (int g = 0; g < kDecGMax; ++g) {
+            if (g >= G) break;
+            float qf[8];
+            unpack8(reinterpret_cast<const int4*>(&sq[g][0])[c0 + c], qf);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sc[g] = fmaf(qf[j], kf[j], sc[g]);
+          }
+        }
+      }
+    }
+    // ---- online softmax per head over the chunk ----
+    float p[kDecGMax];
+#pragma unroll
+    for (int g = 0; g < kDecGMax; ++g) {
+      if (g >= G) break;
+      const float v = valid ? sc[g] * scale_log2 : -INFINITY;
+      float mx = v;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float mn = fmaxf(m[g], mx);  // finite: key c0 < n_keys is valid
+      const float alpha = exp2f(m[g] - mn);
+      p[g] = valid ? exp2f(v - mn) : 0.f;
+      float sum = p[g];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      l[g] = l[g] * alpha + sum;
+      m[g] = mn;
+#pragma unroll
+      for (int d = 0; d < kDPL; ++d) o[g][d] *= alpha;
+    }
+    // ---- P·V from the staged rows: lane = dims [kDPL·lane, +kDPL) ----
+    cp_wait<0>();
+    __syncwarp();
+    const int nk = min(32, n_keys - c0);
+#pragma unroll 4
+    for (int k = 0; k < nk; ++k) {
+      const __nv_bfloat16* vr = sv + (size_t)k * DH + kDPL * lane;
+      float vf[kDPL];
+      if constexpr (kDPL == 4) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+        vf[0] = a.x; vf[1] = a.y; vf[2] = b.x; vf[3] = b.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+        vf[0] = a.x; vf[1] = a.y;
+      }
+#pragma unroll
+      for (int g = 0; g < kDecGMax; ++g) {
+        if (g >= G) break;
+        const float pk = __shfl_sync(0xffffffffu, p[g], k);
+#pragma unroll
+        for (int d = 0; d < kDPL; ++d) o[g][d] = fmaf(pk, vf[d], o[g][d]);
+      }
+    }
+    __syncwarp();  // the staged rows are read before the next chunk's copies land
+  }
+  __syncthreads();  // the merge buffer aliases every warp's staging rows
+  // ---- merge the warps ----
+#pragma unroll
+  for (int g = 0; g < kDecGMax; ++g) {
+    if (g >= G) break;
+    if (lane == 0) {
+      sm[warp][g] = m[g];
+      sl[warp][g] = l[g];
+    }
+#pragma unroll
+    for (int d = 0; d < kDPL; ++d) so[warp][g][kDPL * lane + d] = o[g][d];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * DH; i += blockDim.x) {
+    const int g = i / DH, d = i % DH;
+    float M = -INFINITY;
+    for (int w = 0; w < kDecWarps; ++w) M = fmaxf(M, sm[w][g]);
+    float L = 0.f, O = 0.f;
+    for (int w = 0; w < kDecWarps; ++w) {
+      if (sm[w][g] == -INFINITY) continue;  // a warp that saw no key
+      const float f = exp2f(sm[w][g] - M);
+      L += sl[w][g] * f;
+      O += so[w][g][d] * f;
+    }
+    out[((size_t)qs * hq + (size_t)h * G + g) * DH + d] = __float2bfloat16_rn(O / L);
+  }
+}
+
+template <int DH>
+int launch_decode(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages,
+                  const int32_t* q_start, const int32_t* kv_before, int bs, int hq, int hkv, int page_size, float scale,
+                  void* out, cudaStream_t st) {
+  // dynamic shared memory: 32 V rows per warp, reused for the warps' (m, l, O) merge
+  constexpr size_t smem = (size_t)kDecWarps * 32 * DH * 2 > (size_t)kDecWarps * kDecGMax * DH * 4
+                              ? (size_t)kDecWarps * 32 * DH * 2
+                              : (size_t)kDecWarps * kDecGMax * DH * 4;
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_decode_kernel<DH>), smem)) return rc;
+  attn_decode_kernel<DH><<<bs * hkv, 32 * kDecWarps, smem, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(q), reinterpret_cast<const __nv_bfloat16*>(k),
+      reinterpret_cast<const __nv_bfloat16*>(v), bt, max_pages, q_start, kv_before, hq, hkv, page_size,
+      scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));
+  SO_CHECK_LAUNCH();
+  return SO_OK;
+}
+
 template <int DH>
 int launch_dh(const void* q, const void* k, const void* v, const int32_t* bt, int max_pages, const int32_t* q_start,
               const int32_t* kv_before, int bs, int max_q, int hq, int hkv, int page_size, float scale, void* out,
@@ -467,6 +641,11 @@ int launch_dh(const void* q, const void* k, const void* v, const int32_t* bt, in
   // TMA boxes cover whole pages (≤ 32 rows) or 32-row halves of larger pages
   const bool tma_ok = (page_size <= kKeys ? kKeys % page_size == 0 : page_size % kKeys == 0) &&
                       (reinterpret_cast<uintptr_t>(k) & 15) == 0 && (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+  // K6d on request only: measured slower than the tiled kernel at the draft's decode shape
+  // (bs 64, ctx 520: 88 vs 53 µs, profiles/attn_r2.md) — kept as a tested alternative
+  if (variant == 3 && max_q == 1 && hq / hkv <= kDecGMax && (DH == 128 || DH == 64))
+    return launch_decode<DH>(q, k, v, bt, max_pages, q_start, kv_before, bs, hq, hkv, page_size, scale, out, st);
+  if (variant == 3) variant = 0;
   if (variant == 0 && tma_ok)
     return launch<DH, true>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
   return launch<DH, false>(q, k, v, bt, max_pages, q_start, kv_before, bs, max_q, hq, hkv, page_size, scale, out, st);
@@ -480,7 +659,7 @@ extern "C" int so_attn_paged_v(const void* q, const void* k_cache, const void* v
                                void* stream) {
   SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
   SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
-  SO_REQUIRE(page_size >= 1 && variant >= 0 && variant <= 2, SO_E_SHAPE);
+  SO_REQUIRE(page_size >= 1 && variant >= 0 && variant <= 3, SO_E_SHAPE);
   if (variant == 2)
     return so_attn_paged_tc(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv, dh,
                             page_size, scale, out, stream);

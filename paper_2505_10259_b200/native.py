@@ -301,8 +301,8 @@ def rope_kv_append(qkv, positions, slots, hq, hkv, dh, theta, page_size, q_out, 
 
 def attn_paged(q, k_cache, v_cache, block_table, q_start, kv_before, max_q, hq, hkv, dh, page_size, scale, out,
                stream=None, variant: int = 0):
-    """``variant`` 0 = TMA-staged K/V tiles where the page size allows, 1 = cp.async staging,
-    2 = the tcgen05 kernel (S and O in TMEM)."""
+    """``variant`` 0 = auto (TMA-staged K/V tiles where the page size allows), 1 = cp.async staging,
+    2 = the tcgen05 kernel K6c (S and O in TMEM), 3 = K6d (decode steps, CUDA-core streaming)."""
     bs = kv_before.numel()
     _check(lib().so_attn_paged_v(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(block_table), block_table.shape[1],
                                  _ptr(q_start), _ptr(kv_before), bs, max_q, hq, hkv, dh, page_size, scale,

@@ -42,7 +42,10 @@ class B200Rates:
     # with 0.68 the planner chose bs 480 / 90 cached, whose draft stream (3.50-3.63 s at a 1.22 GHz
     # power-capped clock) overran the 3.46 s link pass: 589.8 tok/s instead of 598 — a compute
     # overrun costs linearly, a margin only a few sequences
-    tensor_efficiency: float = 0.65
+    # Round 2 (K5c decode-step GEMMs, fused router, 16-token steady state): bs 504 / 135 cached planned
+    # at 0.65 predicted 3.52 s of compute; the draft stream measured 3.06–3.08 s at 1.35 GHz (0.74
+    # effective).  Planned at 0.70: a 6 % margin under that
+    tensor_efficiency: float = 0.70
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
     # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
     # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin

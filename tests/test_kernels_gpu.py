@@ -334,6 +334,21 @@ def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
     _check_attn(dh, hq, hkv, qlens, kvbs, ps, attn_variant)
 
 
+@pytest.mark.parametrize("dh,hq,hkv,qlens,kvbs,ps", [
+    (128, 32, 8, [1] * 64, list(range(3, 64 * 9, 9)), 16),   # Mistral-7B decode step, ragged contexts
+    (128, 32, 8, [1, 0, 1, 1], [0, 50, 1, 520], 16),         # a key-less start, a slot without a query
+    (128, 48, 8, [1] * 5, [503, 0, 17, 1, 130], 16),          # G = 6
+    (128, 64, 8, [1] * 3, [129, 700, 64], 16),                # G = 8
+    (128, 8, 8, [1] * 3, [40, 600, 2], 32),                   # G = 1
+    (64, 4, 2, [1] * 4, [10, 100, 0, 257], 5),                # dh 64, odd pages
+])
+@pytest.mark.parametrize("attn_variant", [0, 1, 3], ids=["auto", "cp_async", "k6d"])
+def test_attn_decode_step(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
+    """One query position per sequence (the draft's decode steps): K6d, the
+    CUDA-core streaming kernel, against the fp32 reference and the tiled kernel."""
+    _check_attn(dh, hq, hkv, qlens, kvbs, ps, attn_variant)
+
+
 @pytest.mark.parametrize("attn_variant", [0, 2], ids=["tma", "tcgen05"])
 @pytest.mark.parametrize("hq,qlens,kvbs", [(48, [9] * 6, [503, 40, 700, 1, 64, 300]), (32, [200, 7], [0, 900])])
 def test_attn_paged_growing_scores(hq, qlens, kvbs, attn_variant):

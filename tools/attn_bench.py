@@ -72,7 +72,7 @@ if __name__ == "__main__":
         v = int(sys.argv[1])
         print(json.dumps(run(bs=488, n=8, ctx=520, variant=v, reps=5)))
         sys.exit(0)
-    for variant, label in ((1, "cp_async"), (0, "tma"), (2, "tcgen05")):
+    for variant, label in ((1, "cp_async"), (0, "auto (tma; K6d for decode)"), (2, "tcgen05"), (3, "k6d")):
         for r in [run(variant=variant), run(bs=128, n=4, variant=variant), run(bs=248, n=8, ctx=2000, variant=variant),
                   run(bs=488, n=8, ctx=520, variant=variant), run(bs=64, n=519, ctx=1, hq=32, hkv=8, variant=variant),
                   run(bs=64, n=0, ctx=520, hq=32, hkv=8, variant=variant)]:
