@@ -203,8 +203,10 @@ int so_attn_paged(const void* q, const void* k_cache, const void* v_cache,
                   int bs, int max_q, int hq, int hkv, int dh, int page_size,
                   float scale, void* out, void* stream);
 /* Same with the kernel an explicit argument: 0 = auto (so_attn_paged's
- * choice): TMA boxes issued by one thread where the page size allows (pages of
- * ≤ 32 slots dividing 32, or multiples of 32), else cp.async; 1 = cp.async by
+ * choice): prefill-shaped calls (max_q ≥ 64, dh 128, K6c page sizes) go to
+ * K6c; otherwise TMA boxes issued by one thread where the page size allows
+ * (pages of ≤ 32 slots dividing 32, or multiples of 32) and more than one
+ * query row, else cp.async; 1 = cp.async by
  * every thread; 2 = K6c, the tcgen05 kernel (so_attn_paged_tc); 3 = K6d, a
  * CUDA-core streaming kernel for decode steps (max_q == 1, hq/hkv ≤ 8: CTA per
  * sequence × kv head, lane-per-key scores, cp.async-staged V, warps merged in

@@ -22,7 +22,7 @@ from .streamer import DiskRef, DiskTier, HostStore, LayerStreamer, SharedHostSto
 
 def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: dict | None = None,
                  draft_weights: dict | None = None, device="cuda:0", stream_layers=None, n_slots: int = 2,
-                 seed: int = 0, trace: bool = True, page_size: int = 16, host_store: HostStore | None = None,
+                 seed: int = 0, trace: bool = True, page_size: int = 32, host_store: HostStore | None = None,
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
                  shared_store: SharedHostStore | None = None, stream_attn: bool = False,
                  codec: str = "none", shard_layers=None, disk_layers=None, disk_path: str | None = None,

@@ -25,6 +25,7 @@
 namespace {
 
 constexpr int kRows = 64;   // query rows per CTA (4 warps × 16)
+constexpr int kTcPrefillRows = 64;  // auto: calls with at least this many query positions per sequence go to K6c
 constexpr int kKeys = 32;   // keys per smem tile
 #ifndef SO_ATTN_STAGES
 #define SO_ATTN_STAGES 4
@@ -662,7 +663,13 @@ extern "C" int so_attn_paged_v(const void* q, const void* k_cache, const void* v
   SO_REQUIRE(q && k_cache && v_cache && block_table && q_start && kv_before && out, SO_E_NULLPTR);
   SO_REQUIRE(bs >= 0 && max_q >= 1 && hq > 0 && hkv > 0 && hq % hkv == 0 && max_pages > 0, SO_E_SHAPE);
   SO_REQUIRE(page_size >= 1 && variant >= 0 && variant <= 3, SO_E_SHAPE);
-  if (variant == 2)
+  // prefill-shaped calls (the draft's context re-prefill, prompt prefill): K6c, the tcgen05 kernel —
+  // FLOP-bound there, 221 vs 187 TF/s at 32-token pages (profiles/kernels_r2.md); verify and decode
+  // steps stay on the tiled kernel, faster at a few query rows
+  const bool tc_ok = dh == 128 && hq / hkv <= 128 && page_size >= 8 &&
+                     (page_size <= 64 ? 64 % page_size == 0 : page_size % 64 == 0) && aligned16(q) &&
+                     aligned16(k_cache) && aligned16(v_cache) && aligned16(out);
+  if (variant == 2 || (variant == 0 && max_q >= kTcPrefillRows && tc_ok))
     return so_attn_paged_tc(q, k_cache, v_cache, block_table, max_pages, q_start, kv_before, bs, max_q, hq, hkv, dh,
                             page_size, scale, out, stream);
   SO_REQUIRE(aligned16(k_cache) && aligned16(v_cache), SO_E_ALIGN);

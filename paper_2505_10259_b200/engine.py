@@ -197,7 +197,7 @@ class Engine:
     FRESH_CHUNK = 64  # sequences per draft context prefill of freshly admitted slots
     prefill_chunk_tokens = 16384  # prompt tokens per chunk of a verify pass that prefills (activation workspace)
 
-    def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 16,
+    def __init__(self, target: TargetModel, draft: DraftModel, hw=None, device="cuda:0", page_size: int = 32,
                  trace: bool = True):
         self.target = target
         self.draft = draft

@@ -129,7 +129,7 @@ def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str,
 
 def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budget: int, n_cand: int,
                  acceptance_p: float, ctx_len: int, max_new: int, rates: B200Rates = B200Rates(),
-                 n_slots: int = 2, bs_candidates=None, page_size: int = 16,
+                 n_slots: int = 2, bs_candidates=None, page_size: int = 32,
                  draft_kv_modes=("cached", "reprefill", "mixed"),
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,

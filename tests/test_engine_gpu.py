@@ -407,15 +407,25 @@ def test_host_resident_kv_matches(pair, draft_kv, refill):
 def test_host_kv_refill_at_scale_does_not_stall():
     """Host-resident KV + slot refill at the capped configs[1] shapes (8 layers of
     the 8x7B target, 576 prompts through 192 slots) finishes; an intermittent
-    stall at round 11 was seen once (DESIGN.md robustness notes)."""
+    stall (round 1: twice in ~10 runs; round 2: once in ~6, inside a full test
+    session, not in 4 standalone repeats) is unexplained (DESIGN.md robustness
+    notes).  The workload runs under tools/stall_probe.py, so a stall leaves its
+    diagnosis — every thread's stack, every stream and pipeline event's status,
+    the first pending native call per stream, the resident kernels (cuda-gdb) —
+    in gpurun_out/stall_probe_gpu_test.txt."""
+    import gc
     import os
     import subprocess
     import sys
 
+    gc.collect()
+    torch.cuda.empty_cache()  # the session's cached device memory is not the child's to compete with
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = os.path.join(root, "gpurun_out", "stall_probe_gpu_test.txt")
     env = dict(os.environ)
     env.pop("CUDA_DEVICE_MAX_CONNECTIONS", None)  # the tool reserves its work queues explicitly
-    r = subprocess.run([sys.executable, os.path.join(root, "tools", "repro_hostkv.py"), "576"], cwd=root, env=env,
-                       capture_output=True, text=True, timeout=400)
-    assert r.returncode == 0, r.stderr[-2000:]
-    assert "done 576" in r.stdout
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "stall_probe.py"), "--prompts", "576",
+                        "--repeats", "1", "--stall-s", "60", "--linger-s", "30", "--gdb", "--out", out], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, f"stalled (diagnosis in {out}): " + r.stdout[-1000:] + r.stderr[-1000:]
+    assert "no stall" in r.stdout
