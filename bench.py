@@ -95,6 +95,21 @@ METRIC = "decode tokens/s (offloaded Mixtral target + draft) vs host-link roofli
 NVLINK_PEER_BPS = 770e9  # B200_PROFILING.md: measured NVLink 5 peer copy per direction
 
 
+def _workload_name(args, tgt, drf, world, hbm) -> str:
+    """The configs[] entry a run measures (BASELINE.json), identical for both arms."""
+    if args.config == "8x22b" and not args.hbm_gb:
+        return f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM"
+    cap = f"{hbm / 2**30:.0f} GiB" if hbm else (f"{args.hbm_gb:g} GB" if args.hbm_gb else "24 GiB")
+    return f"configs[1]: {tgt.name} offloaded + {drf.name} draft, {world} B200, HBM capped to {cap}"
+
+
+def _commits_per_verify(args) -> float:
+    """Committed tokens per verified sequence of the workload (the same figure for both arms)."""
+    from paper_2505_10259_b200.acceptance import AcceptanceModel, committed_per_verify
+
+    return committed_per_verify(AcceptanceModel(args.p, args.n_cand), args.max_new)
+
+
 def _weights_checksum(eng) -> str:
     """SO_DEBUG_CHECKSUM=1: checksums of the resident weights (a debugging aid for
     stray device writes; off by default)."""
@@ -245,7 +260,8 @@ def run_reference(args, rank: int) -> None:
     vals, samples = [], []
     cache: dict = {}  # weights built once; every step times the sampled forward passes
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4, seed=i, cache=cache)
+        r = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4, seed=i, cache=cache,
+                                 commits_per_verify=_commits_per_verify(args))
         if i >= args.warmup:
             vals.append(r.tokens_per_s)
             samples.append(r.t_sample)
@@ -255,13 +271,16 @@ def run_reference(args, rank: int) -> None:
             "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} offloaded spec-decode round, n_cand {args.n_cand}, p {args.p}, "
-                                   f"ctx {args.ctx}", "sample_seqs": 4},
+            # the GPU arm's workload (same model pair, draft length, acceptance, prompt length and
+            # request length); the CPU executes a 4-sequence sample of its round
+            "config": {"workload": _workload_name(args, tgt, drf, args.gpus, None), "n_cand": args.n_cand,
+                       "acceptance_p": args.p, "ctx": args.ctx,
+                       "max_new_tokens": args.max_new if args.max_new > 0 else None, "sample_seqs": 4},
             "step": {"executed": "1 full-shape target layer verify (4 seqs × (n_cand+1) tokens, ctx "
                                  f"{args.ctx}) + 1 full-shape draft layer step, NumPy fp32 on {r.cores} cores",
                      "executed_s": step_s, "extrapolated_round_s": r.t_round,
                      "value_is": "tokens/s of a full round extrapolated from the executed sample "
-                                 "(4·E[k] committed tokens / extrapolated round time)"},
+                                 "(4 × commits per verify / extrapolated round time)"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r.cores, "kind": "port", "sample": r.sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     try:
@@ -290,7 +309,8 @@ def main():
         from oracle import cpu_baseline  # checker only: timed beside the GPU path, never part of it
 
         tgt, drf = pair(args.config)  # full-depth shapes
-        cpu = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4)
+        cpu = cpu_baseline.measure(tgt, drf, args.n_cand, args.p, args.ctx, sample_seqs=4,
+                                   commits_per_verify=_commits_per_verify(args))
         try:
             ref_work = reference_cpu_work(args.config)
         except Exception as exc:
@@ -653,10 +673,7 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warm,
         "ms_per_step": dev_s / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, random prompt KV, forced acceptance p)",
-        "config": {"workload": (f"configs[2]: {tgt.name} offloaded + {drf.name} draft, {world} B200, full HBM"
-                                if args.config == "8x22b" and not args.hbm_gb else
-                                f"configs[1]: {tgt.name} offloaded + {drf.name} draft, {world} B200, "
-                                f"HBM capped to {hbm / 2**30:.0f} GiB"),
+        "config": {"workload": _workload_name(args, tgt, drf, world, hbm),
                    "bs_decoding": bs, "total_sequences": S * world, "n_cand": args.n_cand,
                    "draft_kv": plan.draft_kv, "draft_cached_per_batch": plan.draft_cached,
                    "bs_draft": plan.bs_draft, "acceptance_p": args.p,

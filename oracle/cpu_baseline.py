@@ -59,7 +59,7 @@ class CpuSample:
 
 
 def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4, seed: int = 0,
-            cache: dict | None = None) -> CpuSample:
+            cache: dict | None = None, commits_per_verify: float | None = None) -> CpuSample:
     """target/draft: objects with the ModelArch fields (vocab, hidden, ...).
     ``cache`` (a dict kept by the caller) holds the weights between repeated
     measurements, so each repetition times only the forward passes."""
@@ -82,9 +82,11 @@ def measure(target, draft, n_cand: int, p: float, ctx: int, sample_seqs: int = 4
     t_d = time.perf_counter() - t0
     # the one-layer timings include one LM head each; count it once per pass
     t_round = target.n_layer * t_t + (n_cand + 1) * draft.n_layer * t_d
-    e = accept_ref.expected_accepted(p, n_cand)
+    # committed tokens per verified sequence: E[k], or the caller's clamped steady-state figure
+    # (16-token requests, the GPU arm's workload)
+    e = commits_per_verify or accept_ref.expected_accepted(p, n_cand)
     cores = len(os.sched_getaffinity(0))
     sample = (f"1 target layer ({target.name if hasattr(target, 'name') else 'target'}) verify of {sample_seqs} seqs × "
               f"{n_cand + 1} tokens at ctx {ctx} + 1 draft layer decode step, NumPy fp32 on {cores} cores, "
-              f"extrapolated to {target.n_layer}+{n_cand + 1}×{draft.n_layer} layers per round, E[k]={e:.4f}")
+              f"extrapolated to {target.n_layer}+{n_cand + 1}×{draft.n_layer} layers per round, {e:.4f} commits per verify")
     return CpuSample(sample_seqs * e / t_round, t_t, t_d, t_round, sample, cores, t_t + t_d)

@@ -890,10 +890,9 @@ int launch_splitk(const void* A, const void* B, int M, int N, int K, void* C, in
 }  // namespace
 
 extern "C" size_t so_gemm_workspace_bytes(int M, int N, int K) {
+  // split-K scratch; decode steps K5c serves (gemv_tc.cu) need none
   const int ks = (M > 0 && N > 0 && K >= BK) ? splitk_factor(M, N, K, 0) : 0;
-  const size_t splitk = ks ? (size_t)ks * M * N * sizeof(float) : 0;
-  const size_t gemv = so_gemv_workspace_bytes(M, N, K);  // decode steps: the stream-K kernel (gemv_tc.cu)
-  return splitk > gemv ? splitk : gemv;
+  return ks ? (size_t)ks * M * N * sizeof(float) : 0;
 }
 
 extern "C" int so_gemm_bf16_v(const void* A, const void* B, const int32_t* expert_offsets, int E, int M, int N,

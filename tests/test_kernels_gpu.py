@@ -254,19 +254,22 @@ def test_gemm_grouped_expert_bands(counts, gemm_variant):
 
 def test_embed_rmsnorm():
     V, H, T = 1000, 6144, 33
-    table = torch.randn(V, H, device=DEV).to(torch.bfloat16)
-    tok = torch.randint(0, V, (T,), device=DEV, dtype=torch.int32)
+    g = torch.Generator(device=DEV).manual_seed(11)
+    table = torch.randn(V, H, device=DEV, generator=g).to(torch.bfloat16)
+    tok = torch.randint(0, V, (T,), device=DEV, dtype=torch.int32, generator=g)
     x = torch.empty(T, H, dtype=torch.bfloat16, device=DEV)
     native.embed(tok, table, x)
     assert torch.equal(x, table[tok.long()])
-    w = (1 + 0.1 * torch.randn(H, device=DEV)).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(H, device=DEV, generator=g)).to(torch.bfloat16)
     out = torch.empty_like(x)
     native.rmsnorm(x, w, out, 1e-5)
     xf = x.float()
     r = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)
     want = ((xf * r).to(torch.bfloat16).float() * w.float()).to(torch.bfloat16)
     diff = (out.float() - want.float()).abs() / want.float().abs().clamp_min(1e-3)
-    assert (diff > 1e-2).sum().item() == 0  # ≤ 1 bf16 ulp (rsqrt rounding)
+    # ≤ 2 bf16 ulp: the block-reduced sum of squares and rsqrt may round differently from torch,
+    # which can move (x·r) across a rounding boundary and then w·(x·r) across another (seen: 1 of 2e5)
+    assert (diff > 2e-2).sum().item() == 0
 
 
 def test_rope_kv_append():
@@ -363,7 +366,7 @@ def test_attn_paged_growing_scores(hq, qlens, kvbs, attn_variant):
     ([1, 2, 130], [1000, 64, 7], 32),                         # mixed, many units per CTA
 ])
 def test_attn_tcgen05_larger(qlens, kvbs, hq):
-    """K6b over more units than SMs (persistent CTAs carry the ring, TMEM and
+    """K6c over more units than SMs (persistent CTAs carry the rings, TMEM and
     barrier phases across units) at the path's head shapes."""
     _check_attn(128, hq, 8, qlens, kvbs, 16, 2)
 
