@@ -329,6 +329,9 @@ def _attn_ref(q, kc, vc, bt, q_start, kvb, hq, hkv, dh, ps):
     (128, 64, 8, [9, 16, 2], [129, 0, 64], 16),              # G = 8: 16 positions per 128-row unit
     (128, 32, 8, [300, 45], [0, 500], 16),                   # long prefill rows: many row tiles per head
     (128, 48, 8, [9] * 160, list(range(0, 800, 5)), 16),     # 1280 units > 148 SMs: persistent O/Q buffers
+    (128, 48, 8, [9, 9, 9], [503, 0, 70], 32),               # 32-token pages (the engine default)
+    (128, 32, 8, [200, 64], [0, 300], 32),                   # prefill on 32-token pages
+    (128, 32, 8, [70, 9], [100, 500], 128),                  # pages larger than a 64-key tile
 ])
 @pytest.mark.parametrize("attn_variant", [0, 1, 2], ids=["tma", "cp_async", "tcgen05"])
 def test_attn_paged(dh, hq, hkv, qlens, kvbs, ps, attn_variant):
