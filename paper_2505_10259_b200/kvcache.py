@@ -16,7 +16,7 @@ import torch
 from .config import ModelArch
 
 
-DEFAULT_PAGE = 16  # tokens per page: small pages waste ≤ 15 slots per sequence
+DEFAULT_PAGE = 32  # tokens per page: ≤ 31 slots wasted per sequence; half the TMA page boxes of 16 (profiles/kernels_r2.md)
 
 
 class PagedKVCache:

@@ -429,3 +429,29 @@ def test_host_kv_refill_at_scale_does_not_stall():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, f"stalled (diagnosis in {out}): " + r.stdout[-1000:] + r.stderr[-1000:]
     assert "no stall" in r.stdout
+
+
+@pytest.mark.parametrize("draft_kv", ["cached", "reprefill"])
+def test_steady_state_requests_recycle_on_cached_prompt(pair, draft_kv):
+    """bench.py's default workload: max_new-token requests whose commits are
+    clamped to what is left; a finished sequence restarts on its cached prompt
+    (ctx back to the prompt length, t_last back to the prompt's last token), so
+    every slot stays active and contexts stay within [ctx0, ctx0 + max_new)."""
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 3})
+    n, ctx0, max_new, p = 4, 40, 6, 0.8
+    s = eng.new_session(16, 8, ctx0 + max_new + n + 2, n, forced_p=p, bs_draft=4, draft_kv=draft_kv)
+    eng.synthetic_context(s, ctx0, max_new, seed=3, recycle=True)
+    eng.first_draft(s)
+    t0 = s.t_last.copy()
+    committed = 0
+    for _ in range(16):
+        committed += eng.round(s)
+        assert s.active.all()
+        assert ((s.ctx >= ctx0) & (s.ctx < ctx0 + max_new)).all()
+        assert (s.remaining >= 1).all() and (s.remaining <= max_new).all()
+    assert s.recycled > 0
+    # each batch was verified 8 times: every request commits ≤ max_new tokens before it restarts
+    assert committed == sum(len(o) for o in s.out)
+    restarted = s.ctx == ctx0
+    assert (s.t_last[restarted] == t0[restarted]).all()

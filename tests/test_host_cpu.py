@@ -137,3 +137,30 @@ def test_import_changes_no_process_state_and_work_queues_are_explicit():
             "assert not p.reserve_work_queues(16); assert os.environ['CUDA_DEVICE_MAX_CONNECTIONS'] == '32'")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_committed_per_verify_matches_monte_carlo():
+    """acceptance.committed_per_verify (the bench's steady state of max_new-token
+    requests, commits clamped to what is left, simulator.py:213-214) against a
+    direct simulation with the reference-identical sampler."""
+    import numpy as np
+
+    from paper_2505_10259_b200.acceptance import (AcceptanceModel, committed_per_verify, expected_accepted,
+                                                  sample_accepted)
+
+    rng = np.random.default_rng(5)
+    for p, n, max_new in [(0.8, 8, 16), (0.6, 4, 16), (0.9, 8, 128), (0.5, 2, 7)]:
+        m = AcceptanceModel(p, n)
+        verifies = tokens = 0
+        for _ in range(4000):
+            left = max_new
+            while left > 0:
+                c = min(int(sample_accepted(m, rng)), left)
+                left -= c
+                tokens += c
+                verifies += 1
+        mc = tokens / verifies
+        exact = committed_per_verify(m, max_new)
+        assert abs(mc - exact) < 0.02 * exact, (p, n, max_new, mc, exact)
+        assert exact <= expected_accepted(m) + 1e-12
+    assert committed_per_verify(AcceptanceModel(0.8, 8), 0) == expected_accepted(AcceptanceModel(0.8, 8))
