@@ -524,7 +524,8 @@ class Engine:
         dpos = ctx[None, :] + np.arange(1, steps + 1)[:, None]
         dslots = s.dkv.slots(np.broadcast_to(rows, dpos.shape), dpos)
         parts = [pos.astype(np.int32), slots, qs, np.zeros(cm, np.int32), (qs[1:] - 1).astype(np.int32),
-                 dpos.astype(np.int32).ravel(), dslots.ravel(), np.arange(cm + 1, dtype=np.int32)]
+                 dpos.astype(np.int32).ravel(), dslots.ravel(), np.arange(cm + 1, dtype=np.int32),
+                 ctx.astype(np.int32)]
         if u_all is not None:
             parts.append(u_all[p0:p0 + cm].T.ravel().view(np.int32))
         meta = self._up(np.concatenate(parts), st)
@@ -539,13 +540,16 @@ class Engine:
         dpos_d = meta[o:o + D]; o += D
         dslot_d = meta[o:o + D]; o += D
         dqs_d = meta[o:o + cm + 1]; o += cm + 1
+        ctx_d = meta[o:o + cm]; o += cm                   # position of each sequence's last context row
         u_d = meta[o:].view(torch.float32) if u_all is not None else None
         toks = self.draft.ws.get("rp_tokens", (T,), torch.int32)
         native.gather_i32(s.hist, idx, toks, st)
         bt = self._bt(s.dkv, rows, st)
         for j in range(steps + 1):
             if j == 0:
-                fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_d)
+                # the last layer runs attention onward for the last rows only (one per sequence)
+                fb = ForwardBatch(toks, pos_d, slot_d, qs_d, zero_d, bt, cm, int(lens.max()), last_d,
+                                  last_pos=ctx_d, last_qs=dqs_d)
             else:
                 sl = slice((j - 1) * cm, j * cm)
                 fb = ForwardBatch(s.drafts[bi][j - 1, p0:p0 + cm], dpos_d[sl], dslot_d[sl], dqs_d, dpos_d[sl], bt,

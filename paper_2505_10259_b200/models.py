@@ -68,7 +68,7 @@ class ForwardBatch:
     """
 
     def __init__(self, tokens, positions, slots, q_start, kv_before, block_table, n_seq, max_q,
-                 last_rows=None, row0: int = 0):
+                 last_rows=None, row0: int = 0, last_pos=None, last_qs=None):
         self.tokens = tokens          # int32 [T]
         self.positions = positions    # int32 [T]
         self.slots = slots            # int32 [T]
@@ -79,6 +79,10 @@ class ForwardBatch:
         self.max_q = max_q
         self.last_rows = last_rows    # int32 [k] absolute rows whose logits are wanted (None = all)
         self.row0 = row0
+        # with last_rows: the positions of those rows (int32 [k]) and arange(k + 1) (int32) — given,
+        # the last layer runs attention onward for those rows only (the rest only feeds the KV cache)
+        self.last_pos = last_pos
+        self.last_qs = last_qs
 
     @property
     def T(self) -> int:
@@ -141,6 +145,13 @@ class CausalLM:
             native.embed(c.tokens, self.w.embed, xa[c.row0:c.row0 + c.T], stream)
         hook = self.hooks
         q_dim = hq * dh
+        c0 = chunks[0]
+        # last-layer pruning (a context re-prefill wants one row of logits per sequence): the last
+        # layer's K/V need every row, its attention, O, FFN and the LM head only the wanted rows
+        prune = (len(chunks) == 1 and c0.row0 == 0 and c0.last_rows is not None and c0.last_pos is not None
+                 and c0.last_qs is not None and self.arith == "tensor")
+        n_layers = len(self.w.layers)
+        x_last = None
         for li, L in enumerate(self.w.layers):
             if hook:
                 hook(li, "attn_start", stream)
@@ -159,8 +170,18 @@ class CausalLM:
                 self._rmsnorm(x, L.attn_norm, xn[:T], a.eps, stream)
                 self._gemm(xn[:T], wqkv, qkv[:T], native.EPI_BF16, None, stream)
                 self._rope(kv, qkv[:T], c.positions, c.slots, q[:T], kc, vc, stream)
-                self._attn(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
-                           kv.page_size, scale, att[:T], stream)
+                if prune and li == n_layers - 1:  # the wanted rows only from here on
+                    k = c.last_rows.numel()
+                    q_l = ws.get("q_last", (k, q_dim), torch.bfloat16)
+                    x_last = ws.get("x_last", (k, H), torch.bfloat16)
+                    native.embed(c.last_rows, q[:T], q_l, stream)
+                    native.embed(c.last_rows, xa, x_last, stream)
+                    self._attn(q_l, kc, vc, c.block_table, c.last_qs, c.last_pos, 1, hq, hkv, dh, kv.page_size,
+                               scale, att[:k], stream)
+                    T, x, out = k, x_last, x_last
+                else:
+                    self._attn(q[:T], kc, vc, c.block_table, c.q_start, c.kv_before, c.max_q, hq, hkv, dh,
+                               kv.page_size, scale, att[:T], stream)
                 self._gemm(att[:T], wo, h[:T], native.EPI_BF16_RESID, x, stream)
                 self._rmsnorm(h[:T], L.ffn_norm, xn[:T], a.eps, stream)
                 if ci == 0:
@@ -180,7 +201,9 @@ class CausalLM:
             return None
         rows_idx = [c.last_rows for c in chunks if c.last_rows is not None]
         x = xa
-        if rows_idx:
+        if x_last is not None:  # pruned last layer: the wanted rows are already compact
+            x = x_last
+        elif rows_idx:
             assert len(rows_idx) == 1, "last_rows are given once, on the first chunk"
             sel = rows_idx[0]
             rows = ws.get("lastx", (sel.numel(), H), torch.bfloat16)

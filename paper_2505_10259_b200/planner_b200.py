@@ -123,7 +123,15 @@ def draft_flops(draft: ModelArch, bs: int, n_cand: int, ctx: int, draft_kv: str,
     ``draft_cached`` sequences are cached)."""
     kc = bs if draft_kv == "cached" else (0 if draft_kv == "reprefill" else min(draft_cached, bs))
     cached = kc * (n_cand + 1) * draft.verify_flops_per_token(ctx)
-    rp = (bs - kc) * (ctx * draft.verify_flops_per_token(ctx // 2) + (n_cand - 1) * draft.verify_flops_per_token(ctx))
+    # a context re-prefill: every position through every layer, except that the LM head runs for
+    # the last row only, and so do the last layer's attention, O projection and FFN (models.py
+    # last-layer pruning: the other rows only feed that layer's K/V)
+    H, q_dim = draft.hidden, draft.n_head * draft.head_dim
+    lm = 2 * H * draft.vocab
+    ffn = 2 * draft.top_k * 3 * H * draft.inter if draft.is_moe else 2 * 3 * H * draft.inter
+    last_layer_rest = 2 * q_dim * H + ffn + 4 * q_dim * (ctx // 2)
+    prefill = ctx * (draft.verify_flops_per_token(ctx // 2) - lm) + lm - (ctx - 1) * last_layer_rest
+    rp = (bs - kc) * (prefill + (n_cand - 1) * draft.verify_flops_per_token(ctx))
     return cached + rp
 
 
