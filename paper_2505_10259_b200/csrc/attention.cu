@@ -160,13 +160,17 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
   const int g = lane >> 2, c = lane & 3;
 
   // ---- Q fragments (A operand, row-major [16 rows × DH]) ----
-  const int rA = r0 + warp * 16 + g, rB = rA + 8;
+  // decode steps (≤ 16 query rows per CTA, cp.async staging): only warp 0 would hold live rows, so
+  // every warp takes those rows and a different share of the KEY tiles ("warp split"), and the
+  // warps' (m, l, O) merge through shared memory at the end
+  const bool wsplit = !TMA && rows_total - r0 <= 16;
+  const int rA = r0 + (wsplit ? 0 : warp * 16) + g, rB = rA + 8;
   const bool vA = rA < rows_total, vB = rB < rows_total;
   const int jA = vA ? rA / G : 0, jB = vB ? rB / G : 0;
   const int hA = g_kv * G + (vA ? rA % G : 0), hB = g_kv * G + (vB ? rB % G : 0);
   const __nv_bfloat16* qA = q + ((size_t)(qs + jA) * hq + hA) * DH;
   const __nv_bfloat16* qB = q + ((size_t)(qs + jB) * hq + hB) * DH;
-  const bool warp_live = (r0 + warp * 16) < rows_total;
+  const bool warp_live = wsplit || (r0 + warp * 16) < rows_total;
   uint32_t qf[DH / 16][4];
 #pragma unroll
   for (int ks = 0; ks < DH / 16; ++ks) {
@@ -244,48 +248,9 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
     }
   };
 
-  // kStages-deep ring: kStages−1 tiles stream from HBM while one is consumed
-  // (cp.async: one commit group per tile, empty groups past the end keep the
-  // wait_group arithmetic uniform; TMA: one mbarrier phase per tile and stage)
-  if constexpr (TMA) {
-    if (threadIdx.x == 0)
-      for (int p = 0; p < kStages - 1 && p < n_tiles; ++p) issue_tile(p, p);
-  } else {
-#pragma unroll
-    for (int p = 0; p < kStages - 1; ++p) {
-      if (p < n_tiles) load_tile(p, p);
-      cp_commit();
-    }
-  }
-  for (int kt = 0; kt < n_tiles; ++kt) {
-    const int nxt = kt + kStages - 1;
-    if constexpr (TMA) {
-      // the stage of tile nxt held tile kt−1: refill it once every warp is done
-      // with that tile — warps otherwise run up to kStages−1 tiles apart, no
-      // CTA-wide barrier per tile
-      if (threadIdx.x == 0 && nxt < n_tiles) {
-        if (kt >= 1) mbar_wait(&empty[(kt - 1) % kStages], ((kt - 1) / kStages) & 1);
-        issue_tile(nxt, nxt % kStages);
-      }
-      mbar_wait(&full[kt % kStages], (kt / kStages) & 1);
-      const int valid = n_keys - kt * kKeys;
-      if (valid < kKeys) {  // last tile: V rows past the keys hold stale data (0·NaN must not reach O)
-        uint8_t* sv = smem + (kt % kStages) * 2 * TL::kBytes + TL::kBytes;
-        for (int i = threadIdx.x; i < (kKeys - valid) * (DH / 64) * 8; i += kThreads) {
-          const int row = valid + i / ((DH / 64) * 8), rest = i % ((DH / 64) * 8);
-          *reinterpret_cast<int4*>(sv + (rest >> 3) * (kKeys * 128) + row * 128 + ((rest & 7) << 4)) =
-              make_int4(0, 0, 0, 0);
-        }
-        __syncthreads();
-      }
-    } else {
-      if (nxt < n_tiles) load_tile(nxt, nxt % kStages);
-      cp_commit();
-      cp_wait<kStages - 1>();
-      __syncthreads();
-    }
-    if (warp_live) {
-      const uint32_t sk = smem_u32(smem + (kt % kStages) * 2 * TL::kBytes);
+  // one key tile from ring stage `stage`: S = Q·Kᵀ, masked online softmax, O += P·V (this warp's rows)
+  auto compute_tile = [&](int kt, int stage) {
+      const uint32_t sk = smem_u32(smem + stage * 2 * TL::kBytes);
       const uint32_t sv = sk + TL::kBytes;
       // ---- S = Q Kᵀ  (16 rows × kKeys keys per warp) ----
       float sfr[kKeys / 8][4];
@@ -367,7 +332,101 @@ __global__ void __launch_bounds__(kThreads, SO_ATTN_MINB) attn_paged_kernel(
           mma_bf16(o[dn + 1], pf[kk], b2, b3);
         }
       }
+      };
+  if (wsplit) {
+    // rounds of kStages tiles, one per warp (kStages == warps): all loads of a round in flight together
+    static_assert(kStages == kThreads / 32, "warp split: one ring stage per warp");
+    for (int kt0 = 0; kt0 < n_tiles; kt0 += kStages) {
+#pragma unroll
+      for (int w = 0; w < kStages; ++w)
+        if (kt0 + w < n_tiles) load_tile(kt0 + w, w);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+      if (kt0 + warp < n_tiles) compute_tile(kt0 + warp, warp);
+      __syncthreads();
     }
+    // merge: every warp's rows g, g+8 (row sums reduced over the quad first) through shared memory
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+    lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+    float* sm = reinterpret_cast<float*>(smem);                // [warp][16] row maxima
+    float* sl = sm + kStages * 16;                             // [warp][16] row sums
+    float* so = sl + kStages * 16;                             // [warp][16][DH] unnormalised O
+    if (c == 0) {
+      sm[warp * 16 + g] = mA;
+      sm[warp * 16 + g + 8] = mB;
+      sl[warp * 16 + g] = lA;
+      sl[warp * 16 + g + 8] = lB;
+    }
+#pragma unroll
+    for (int dn = 0; dn < DH / 8; ++dn) {
+      const int d = dn * 8 + 2 * c;
+      so[(warp * 16 + g) * DH + d] = o[dn][0];
+      so[(warp * 16 + g) * DH + d + 1] = o[dn][1];
+      so[(warp * 16 + g + 8) * DH + d] = o[dn][2];
+      so[(warp * 16 + g + 8) * DH + d + 1] = o[dn][3];
+    }
+    __syncthreads();
+    const int rows = rows_total - r0;
+    for (int i = threadIdx.x; i < rows * DH; i += kThreads) {
+      const int r = i / DH, d = i % DH;
+      float M = -INFINITY;
+      for (int w = 0; w < kStages; ++w) M = fmaxf(M, sm[w * 16 + r]);
+      float L = 0.f, O = 0.f;
+      for (int w = 0; w < kStages; ++w) {
+        if (sm[w * 16 + r] == -INFINITY) continue;  // a warp that saw no key of this row
+        const float f = exp2f(sm[w * 16 + r] - M);
+        L += sl[w * 16 + r] * f;
+        O += so[(w * 16 + r) * DH + d] * f;
+      }
+      const int row = r0 + r, j = row / G, hh = g_kv * G + row % G;
+      out[((size_t)(qs + j) * hq + hh) * DH + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    }
+    return;
+  }
+  // kStages-deep ring: kStages−1 tiles stream from HBM while one is consumed
+  // (cp.async: one commit group per tile, empty groups past the end keep the
+  // wait_group arithmetic uniform; TMA: one mbarrier phase per tile and stage)
+  if constexpr (TMA) {
+    if (threadIdx.x == 0)
+      for (int p = 0; p < kStages - 1 && p < n_tiles; ++p) issue_tile(p, p);
+  } else {
+#pragma unroll
+    for (int p = 0; p < kStages - 1; ++p) {
+      if (p < n_tiles) load_tile(p, p);
+      cp_commit();
+    }
+  }
+  for (int kt = 0; kt < n_tiles; ++kt) {
+    const int nxt = kt + kStages - 1;
+    if constexpr (TMA) {
+      // the stage of tile nxt held tile kt−1: refill it once every warp is done
+      // with that tile — warps otherwise run up to kStages−1 tiles apart, no
+      // CTA-wide barrier per tile
+      if (threadIdx.x == 0 && nxt < n_tiles) {
+        if (kt >= 1) mbar_wait(&empty[(kt - 1) % kStages], ((kt - 1) / kStages) & 1);
+        issue_tile(nxt, nxt % kStages);
+      }
+      mbar_wait(&full[kt % kStages], (kt / kStages) & 1);
+      const int valid = n_keys - kt * kKeys;
+      if (valid < kKeys) {  // last tile: V rows past the keys hold stale data (0·NaN must not reach O)
+        uint8_t* sv = smem + (kt % kStages) * 2 * TL::kBytes + TL::kBytes;
+        for (int i = threadIdx.x; i < (kKeys - valid) * (DH / 64) * 8; i += kThreads) {
+          const int row = valid + i / ((DH / 64) * 8), rest = i % ((DH / 64) * 8);
+          *reinterpret_cast<int4*>(sv + (rest >> 3) * (kKeys * 128) + row * 128 + ((rest & 7) << 4)) =
+              make_int4(0, 0, 0, 0);
+        }
+        __syncthreads();
+      }
+    } else {
+      if (nxt < n_tiles) load_tile(nxt, nxt % kStages);
+      cp_commit();
+      cp_wait<kStages - 1>();
+      __syncthreads();
+    }
+    if (warp_live) compute_tile(kt, kt % kStages);
     if constexpr (TMA) {
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[kt % kStages])) : "memory");
