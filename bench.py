@@ -61,6 +61,9 @@ def parse():
                          "pool's 196 GiB boxes; lowered to MemAvailable − 12 GB only if the box has less)")
     ap.add_argument("--hbm-gb", type=float, default=0.0, help="HBM budget (0 = device; 8x7b config: 24 GiB cap)")
     ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--window", choices=("split", "whole"), default="whole",
+                    help="split: streamed FFN units move as [gate_up | down] segments, one window slot each "
+                         "(one unit of HBM instead of --slots units; single GPU)")
     ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill", "mixed"), default="auto",
                     help="draft KV policy (auto = planner)")
     ap.add_argument("--layers", type=int, default=0,
@@ -385,13 +388,15 @@ def main():
         enc.release()
         del probe
         torch.cuda.empty_cache()
+    split = args.window == "split" and world == 1
     plan = plan_offload(tgt, drf, hbm, host, args.n_cand, args.p, args.ctx, max_new, rates, n_slots=args.slots,
                         bs_candidates=[args.bs] if args.bs else None, draft_kv_modes=modes, stream_ratio=ratio,
                         ring_bytes=ring, max_pinned=None if args.max_pinned < 0 else args.max_pinned,
                         draft_cached_candidates=None if args.draft_cached < 0 else [args.draft_cached],
                         world=world, allow_shards=not args.no_shards, disk_budget=int(args.disk_gb * 1e9),
                         kv_host_modes=(False, True) if world == 1 else (False,),
-                        tokens_per_verify=committed_per_verify(AcceptanceModel(args.p, args.n_cand), args.max_new))
+                        tokens_per_verify=committed_per_verify(AcceptanceModel(args.p, args.n_cand), args.max_new),
+                        split_window=split)
     log(f"plan: bs {plan.bs_decoding} draft {plan.draft_kv}/{plan.draft_cached} pinned {len(plan.pinned_layers)} "
         f"streamed {len(plan.stream_layers)} (disk {len(plan.disk_layers)}) sharded {len(plan.shard_layers)} "
         f"link {link / 1e9:.1f} GB/s")
@@ -413,7 +418,8 @@ def main():
         store = HostStore()
         eng = build_engine(tgt, drf, device=device, stream_layers=set(plan.stream_layers), n_slots=args.slots,
                            seed=1, trace=bool(args.trace_out), host_store=store, stream_attn=plan.stream_attn,
-                           codec=args.codec, disk_layers=set(plan.disk_layers), disk_path=args.disk_path or None)
+                           codec=args.codec, disk_layers=set(plan.disk_layers), disk_path=args.disk_path or None,
+                           split_window=plan.split_window)
     bs = plan.bs_decoding
     S = 2 * bs
     s = eng.new_session(S, bs, args.ctx + max_new + args.n_cand + 2, args.n_cand, forced_p=args.p, seed=rank,
@@ -685,7 +691,7 @@ def main():
                    "ctx": args.ctx, "streamed_layers": len(plan.stream_layers),
                    "hbm_sharded_layers": len(plan.shard_layers), "disk_layers": len(plan.disk_layers),
                    "target_kv": "host DRAM (one batch staged per layer)" if plan.kv_host else "HBM",
-                   "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots,
+                   "pinned_layers": len(plan.pinned_layers), "window_slots": args.slots, "window": "split" if plan.split_window else "whole",
                    "codec": args.codec, "stream_ratio": streamed / streamed_raw if streamed_raw else None,
                    "streamed_bytes_per_round": int(streamed / steps * world),
                    "kv_h2d_bytes_per_round": int(kv_link / steps * world),

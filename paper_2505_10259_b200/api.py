@@ -26,7 +26,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
                  chunk_bytes: int = 256 << 20, rank: int = 0, world: int = 1, group=None,
                  shared_store: SharedHostStore | None = None, stream_attn: bool = False,
                  codec: str = "none", shard_layers=None, disk_layers=None, disk_path: str | None = None,
-                 arith: str = "tensor") -> Engine:
+                 arith: str = "tensor", split_window: bool = False) -> Engine:
     """Build an engine.  ``*_weights`` are logical (HF-shaped) arrays; None =
     synthetic random init of the architecture.  ``stream_layers`` = target
     FFN layers kept in pinned host DRAM and streamed each pass (default:
@@ -40,7 +40,10 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     ``disk_layers`` (§8 f4): streamed layers kept in a file at ``disk_path``
     (default: a temporary file) and staged through pinned DRAM each pass.
     ``arith="canonical"`` runs both models through the parity-mode kernels
-    (fixed IEEE order, bit-identical to the CPU oracle; tiny shapes only)."""
+    (fixed IEEE order, bit-identical to the CPU oracle; tiny shapes only).
+    ``split_window``: each streamed unit moves as [gate_up | down] into its
+    own slot, so the HBM window is one unit instead of ``n_slots`` units
+    (single GPU, FFN-only units; the link still runs a unit ahead)."""
     if codec not in ("none", "xc4"):
         raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
@@ -62,7 +65,11 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
             with tempfile.NamedTemporaryFile(prefix="specoffload_disk_", suffix=".bin", delete=False) as f:
                 disk_path = f.name
         disk = DiskTier(disk_path)
-    enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
+    segments = W.unit_segments(target_arch, stream_attn, split_window)
+    if split_window and (world > 1 or shard_layers or disk_layers):
+        raise ValueError("split_window is single-GPU and host-DRAM only")
+    enc = (C.Encoder(dev, align_elems=segments[0][1] // 2 if split_window else 0)
+           if codec == "xc4" and stream_layers else None)
     if target_weights is not None:
         store = host_store or HostStore()
         tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc,
@@ -88,7 +95,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     host = {li: t if isinstance(t, (C.XC4Unit, DiskRef)) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
                              chunk_bytes=chunk_bytes, rank=rank, world=world, group=group,
-                             shards=tw.shard_ffn, disk=disk) if (host or tw.shard_ffn) else None
+                             shards=tw.shard_ffn, disk=disk, segments=segments) if (host or tw.shard_ffn) else None
     if disk is not None:
         weakref.finalize(streamer, disk.close)
     target = TargetModel(tw, dev, streamer, arith=arith)

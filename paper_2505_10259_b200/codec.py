@@ -26,13 +26,24 @@ MIN_FRAME_ELEMS = 4096
 SLICE_WORLD = 8             # frames split evenly over 1, 2, 4 or 8 ranks when the unit allows it
 
 
-def frame_elems_for(n_elems: int, world: int = SLICE_WORLD) -> int:
+def frame_elems_for(n_elems: int, world: int = SLICE_WORLD, align_elems: int = 0) -> int:
     """Largest frame (a multiple of 4096 weights, ≤ 32 Mi) that tiles the unit
     into a multiple of ``world`` whole frames — any divisor works, so awkward
     unit sizes (e.g. attention + FFN units, 2^22·597 weights) still get frames
     of tens of MB rather than a power of two small enough to divide them.
     Units that cannot split evenly fall back to world = 1, then to a partial
-    last frame (single rank only)."""
+    last frame (single rank only).  ``align_elems`` > 0: frames must also tile
+    [0, align_elems) exactly — a split window's segment boundary (streamer.py)."""
+    if align_elems:
+        for w in (world, 1):
+            if n_elems % w:
+                continue
+            share = n_elems // w
+            for k in range(max(1, -(-share // MAX_FRAME_ELEMS)), share // MIN_FRAME_ELEMS + 1):
+                fe = share // k
+                if share % k == 0 and fe % MIN_FRAME_ELEMS == 0 and align_elems % fe == 0:
+                    return fe
+        raise ValueError(f"no XC4 frame size tiles both {n_elems} and {align_elems} weights")
     for w in (world, 1):
         if n_elems % w:
             continue
@@ -98,9 +109,10 @@ class XC4Unit:
 class Encoder:
     """Device-side XC4 encoder with grow-only scratch (setup time only)."""
 
-    def __init__(self, device, world: int = SLICE_WORLD, code_bits: int = 0):
+    def __init__(self, device, world: int = SLICE_WORLD, code_bits: int = 0, align_elems: int = 0):
         self.device = torch.device(device)
         self.world = world
+        self.align_elems = align_elems  # split window: frames also tile the segment boundary
         self.code_bits = code_bits  # 0 = per unit, the smaller of 3- and 4-bit codes
         self._scratch = None
         self._dst = None
@@ -120,7 +132,7 @@ class Encoder:
         if flat.dtype != torch.bfloat16:
             flat = flat.view(torch.bfloat16)
         n = flat.numel()
-        fe = frame_elems_for(n, self.world)
+        fe = frame_elems_for(n, self.world, self.align_elems)
         scratch = self._grow("_scratch", native.xc4_scratch_bytes(n, fe))
         nbytes, _ = native.xc4_encode(flat, fe, None, scratch, code_bits=self.code_bits)
         dst = self._grow("_dst", nbytes)

@@ -217,6 +217,7 @@ class Engine:
         self.tracer = Tracer(trace)
         self._cur = (None, None)  # (round, batch) being verified, for trace tags
         self._marks: dict = {}
+        self._part: dict = {}  # layers whose FFN ran in two parts (split window)
         self._arenas: dict = {}   # stream handle -> _StagingArena (per-round H2D metadata)
         self.nvtx_range: str | None = None  # mirrored onto the draft-enqueue thread when set
         self._join = native.Event()
@@ -238,8 +239,13 @@ class Engine:
         elif phase == "ffn_start":
             self.tracer.add("GPU_TARGET", "attn_gpu", self._marks.get(li), ev, bi, li, rnd)
             self._marks[li] = ev
-        else:
+        elif phase == "ffn_part":  # split window: the down GEMM's part waits for the second segment
             self.tracer.add("GPU_TARGET", "ffn_gpu", self._marks.get(li), ev, bi, li, rnd)
+            self._marks[li] = ev
+            self._part[li] = True
+        else:
+            label = "ffn_gpu_part" if self._part.pop(li, False) else "ffn_gpu"
+            self.tracer.add("GPU_TARGET", label, self._marks.get(li), ev, bi, li, rnd)
             self._last_ffn_end = ev
 
     def resolve_trace(self) -> list:

@@ -157,6 +157,8 @@ class CausalLM:
                 hook(li, "attn_start", stream)
             kc, vc = kv.layer(li, stream)
             base = None
+            split = self._split(li)  # [gate_up | down] in two window slots (streamer segments)
+            base_dn = None
             wqkv, wo = L.wqkv, L.wo
             if wqkv is None:  # attention weights stream with the layer: wait before QKV
                 unit = self._ffn_acquire(li, L, stream)
@@ -190,11 +192,30 @@ class CausalLM:
                     if hook:
                         hook(li, "ffn_start", stream)
                 if a.is_moe:
-                    self._moe(L, base, xn[:T], h[:T], out, T, stream)
+                    self._moe_up(L, base, xn[:T], T, stream)
                 else:
-                    self._mlp(base, xn[:T], h[:T], out, T, stream)
+                    self._mlp_up(base, xn[:T], T, stream)
+                if base_dn is None:
+                    if split:
+                        # one chunk: gate_up's slot goes back to the link before down waits for its own
+                        if len(chunks) == 1:
+                            self.streamer.release(li, stream, 0)
+                        base_dn = self.streamer.acquire(li, stream, 1)
+                        if hook:
+                            hook(li, "ffn_part", stream)
+                    else:
+                        base_dn = base
+                if a.is_moe:
+                    self._moe_down(base_dn, h[:T], out, T, stream)
+                else:
+                    self._mlp_down(base_dn, h[:T], out, T, stream)
             kv.release(li, stream)  # host-resident KV: write the layer's window back
-            self._ffn_release(li, stream)
+            if split:
+                if len(chunks) > 1:
+                    self.streamer.release(li, stream, 0)
+                self.streamer.release(li, stream, 1)
+            else:
+                self._ffn_release(li, stream)
             if hook:
                 hook(li, "ffn_end", stream)
         if not want_logits:
@@ -239,7 +260,13 @@ class CausalLM:
         if self.streamer is not None:
             self.streamer.release(li, stream)
 
-    def _moe(self, L, base, xn, h, out, T, stream):
+    def _split(self, li) -> bool:
+        st = self.streamer
+        return st is not None and len(st.segments) > 1 and li in st.host
+
+    def _moe_up(self, L, base, xn, T, stream):
+        """top-2 router + permute, grouped gate_up GEMM with the SwiGLU epilogue
+        (reads the unit's gate_up range only)."""
         a, ws = self.arch, self.ws
         E, H, I = a.n_expert, a.hidden, a.inter
         rows = 2 * T
@@ -249,22 +276,38 @@ class CausalLM:
         trows = ws.get("trows", (T, 2), torch.int32)
         xperm = ws.get("xperm", (rows, H), torch.bfloat16)
         act = ws.get("act", (rows, I), torch.bfloat16)
-        y = ws.get("y", (rows, H), torch.bfloat16)
         rws = ws.get("router_ws", (native.router_workspace_bytes(T, E),), torch.uint8)
         self._router(xn, L.router, offs, perm, roww, trows, xperm, rws, stream=stream)
-        gu_elems, _, _ = ffn_offsets(a)
         self._gemm_grouped(xperm, base, offs, E, 2 * I, act, native.EPI_SWIGLU, None, stream)
+
+    def _moe_down(self, base, h, out, T, stream):
+        """grouped down GEMM with the routing-weight row scale, then the top-2
+        combine + residual (reads the unit's down range only)."""
+        a, ws = self.arch, self.ws
+        E, H, I = a.n_expert, a.hidden, a.inter
+        rows = 2 * T
+        offs = ws.get("offs", (E + 1,), torch.int32)
+        roww = ws.get("roww", (rows,), torch.float32)
+        trows = ws.get("trows", (T, 2), torch.int32)
+        act = ws.get("act", (rows, I), torch.bfloat16)
+        y = ws.get("y", (rows, H), torch.bfloat16)
+        gu_elems, _, _ = ffn_offsets(a)
         self._gemm_grouped(act, base + 2 * gu_elems, offs, E, H, y, native.EPI_BF16_ROWSCALE, roww, stream)
         native.moe_combine(y, trows, h, out, stream)
 
-    def _mlp(self, base, xn, h, out, T, stream):
+    def _mlp_up(self, base, xn, T, stream):
+        a, ws = self.arch, self.ws
+        I, H = a.inter, a.hidden
+        act = ws.get("act", (T, I), torch.bfloat16)
+        gu = _raw_bf16(base, (2 * I, H), self.device)
+        self._gemm(xn, gu, act, native.EPI_SWIGLU, None, stream)
+
+    def _mlp_down(self, base, h, out, T, stream):
         a, ws = self.arch, self.ws
         I, H = a.inter, a.hidden
         act = ws.get("act", (T, I), torch.bfloat16)
         gu_elems, _, _ = ffn_offsets(a)
-        gu = _raw_bf16(base, (2 * I, H), self.device)
         dn = _raw_bf16(base + 2 * gu_elems, (H, I), self.device)
-        self._gemm(xn, gu, act, native.EPI_SWIGLU, None, stream)
         self._gemm(act, dn, out, native.EPI_BF16_RESID, h, stream)
 
 

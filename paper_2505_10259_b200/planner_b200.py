@@ -79,6 +79,7 @@ class OffloadPlan:
     disk_layers: tuple[int, ...] = ()   # f4: streamed layers kept on disk (subset of stream_layers)
     t_disk_s: float = 0.0
     kv_host: bool = False               # target KV in pinned host DRAM, one batch staged per layer
+    split_window: bool = False  # FFN units move as [gate_up | down] segments: n_slots / 2 units of window
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -142,7 +143,8 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                  max_draft_chunk: int = 64, stream_attn_modes=(False, True), stream_ratio: float = 1.0,
                  ring_bytes: int = 0, max_pinned: int | None = None, draft_cached_candidates=None,
                  world: int = 1, allow_shards: bool = True, disk_budget: int = 0,
-                 kv_host_modes=(False,), tokens_per_verify: float | None = None) -> OffloadPlan:
+                 kv_host_modes=(False,), tokens_per_verify: float | None = None,
+                 split_window: bool = False) -> OffloadPlan:
     """Choose bs_decoding, the draft-KV policy and the pinned / streamed split that
     maximise predicted decode tokens/s under both memory budgets.
 
@@ -166,7 +168,13 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     reference's CPU-resident KV, placement.py:120-130): HBM keeps a 2-slot
     window of one batch's per-layer KV, host DRAM the pool, and every pass also
     moves the verified batch's KV host → GPU (the write-back uses the other
-    link direction)."""
+    link direction).
+
+    ``split_window`` (single GPU): FFN-only units stream as [gate_up | down]
+    segments, one slot each, so the window costs n_slots / 2 units of HBM
+    (streamer.py); units that carry the attention projections keep whole slots."""
+    if split_window and (world > 1 or n_slots % 2):
+        raise ValueError("split_window needs world == 1 and an even slot count")
     # commits per verification: E[k], or the caller's steady-state figure (clamped requests,
     # acceptance.committed_per_verify) — a constant factor of every candidate's rate
     e_tok = tokens_per_verify or expected_accepted(AcceptanceModel(acceptance_p, n_cand))
@@ -180,8 +188,10 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
         # unit = bytes of one streamed (or pinned) layer; with stream_attn the
         # attention projections travel with the FFN and leave the resident set
         layer_bytes = unit_layout(target, stream_attn)[1]
+        window_units = n_slots // 2 if (split_window and not stream_attn) else n_slots
         fixed = (resident_bytes(target, False) - (target.n_layer * attn_layer if stream_attn else 0)
-                 + resident_bytes(draft, True) + n_slots * layer_bytes + (ring_bytes if stream_ratio < 1 else 0))
+                 + resident_bytes(draft, True) + window_units * layer_bytes
+                 + (ring_bytes if stream_ratio < 1 else 0))
         host_unit = int(math.ceil(layer_bytes * stream_ratio))
         for bs in cands:
             if mode == "mixed":  # interior split points; the endpoints are the pure modes
@@ -270,7 +280,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                         "shards": int(n_sh * layer_bytes / world)},
                        streamed * host_unit, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
                        kc if mode == "mixed" else 0, shard_l, world, t_nvl, disk_l,
-                       n_disk * host_unit / rates.disk_bytes_per_s, kv_host)
+                       n_disk * host_unit / rates.disk_bytes_per_s, kv_host, split_window and not sa)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

@@ -353,6 +353,15 @@ class LayerStreamer:
         ... expert GEMMs reading ptr ...
         streamer.release(ℓ, stream)
     Resident layers return their HBM buffer and never touch the link.
+
+    ``segments`` (split window): the unit is moved as consecutive byte ranges
+    [lo, hi) — e.g. [gate_up | down] of an FFN — each into its own slot, so the
+    window holds one unit instead of two while the link still runs a whole
+    unit ahead of the compute (a segment's slot frees as soon as its GEMM has
+    read it).  Per layer the compute acquires segment 0, 1, … in order
+    (``acquire(ℓ, stream, seg)``); the pointer returned for segment s is the
+    unit's *virtual* base (slot address − lo), so unit-relative offsets keep
+    working — only addresses inside [lo, hi) of that segment may be read.
     """
 
     RING_SLOTS = 4  # encoded frames in flight between the copy engine and the decoder (XC4 units)
@@ -360,8 +369,18 @@ class LayerStreamer:
     def __init__(self, layer_bytes: int, resident: dict[int, torch.Tensor], host: dict,
                  n_layer: int, device, n_slots: int = 2, chunk_bytes: int = 256 << 20, trace: bool = False,
                  rank: int = 0, world: int = 1, group=None, shards: dict[int, torch.Tensor] | None = None,
-                 disk: "DiskTier | None" = None):
+                 disk: "DiskTier | None" = None, segments: list[tuple[int, int]] | None = None):
         self.layer_bytes = layer_bytes
+        self.segments = list(segments) if segments else [(0, layer_bytes)]
+        S = len(self.segments)
+        if (self.segments[0][0] != 0 or self.segments[-1][1] != layer_bytes
+                or any(a[1] != b[0] for a, b in zip(self.segments, self.segments[1:]))
+                or any(lo % 256 or hi <= lo for lo, hi in self.segments[:-1])):
+            raise ValueError(f"segments must tile [0, {layer_bytes}) in 256-B aligned ranges: {self.segments}")
+        if S > 1 and (world > 1 or shards or disk is not None):
+            raise ValueError("a split window is single-GPU and host-DRAM only")
+        if n_slots % S:
+            raise ValueError(f"{n_slots} slots do not hold {S} segments per unit evenly")
         # f4: host values that are DiskRefs are staged from ``disk`` each use
         self.disk = disk
         self.disk_uses = 0
@@ -383,6 +402,8 @@ class LayerStreamer:
         self.resident = resident
         self.host = host
         self.streamed = [li for li in range(n_layer) if li in host or li in self.shards]
+        # one pass = every streamed layer's segments in order
+        self.uses = [(li, sg) for li in self.streamed for sg in range(S)]
         self.n_slots = n_slots if self.streamed else 0
         self.chunk = chunk_bytes
         self.device = torch.device(device)
@@ -393,7 +414,8 @@ class LayerStreamer:
         self.lo, self.hi = slice_bounds(layer_bytes, rank, world) if world > 1 else (0, layer_bytes)
         self.comm_stream = torch.cuda.Stream(device=self.device) if (self.streamed and world > 1) else None
         self.copied = [native.Event() for _ in range(self.n_slots)] if (world > 1 and host) else []
-        self.slots = [torch.empty(layer_bytes, dtype=torch.uint8, device=self.device) for _ in range(self.n_slots)]
+        self.slots = [torch.empty(self.seg_bytes(j % S), dtype=torch.uint8, device=self.device)
+                      for j in range(self.n_slots)]
         # events are created eagerly through the C ABI (a lazily created torch
         # event has handle 0, and record/wait on it silently no-op)
         self.loaded = [native.Event() for _ in range(self.n_slots)]
@@ -403,14 +425,25 @@ class LayerStreamer:
             for u in metas.values():
                 if u.raw_bytes != layer_bytes:
                     raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
-            self.frames = {li: u.frame_range(rank, world) for li, u in metas.items()}
+            if S == 1:
+                self.frames = {li: u.frame_range(rank, world) for li, u in metas.items()}
+            else:  # a segment's frames decode to exactly its byte range
+                self.frames = {}
+                for li, u in metas.items():
+                    fb = 2 * u.frame_elems
+                    for sg, (lo, hi) in enumerate(self.segments):
+                        if lo % fb or (hi % fb and hi != layer_bytes):
+                            raise ValueError(f"segment [{lo}, {hi}) does not fall on XC4 frame boundaries "
+                                             f"({fb} B frames): encode with codec.Encoder(align_elems=…)")
+                        self.frames[(li, sg)] = (lo // fb, -(-hi // fb))
             self.ring_slot_bytes = (max(u.max_frame_bytes() for u in metas.values()) + 255) // 256 * 256
             self.ring = torch.empty(self.RING_SLOTS * self.ring_slot_bytes, dtype=torch.uint8, device=self.device)
             self.ring_events = [native.Event() for _ in range(2 * self.RING_SLOTS)]
             self.ring_cursor = Cursor(0)
             # decode kernels jump ahead of the verify/draft kernels: they gate the next layer
             self.decode_stream = torch.cuda.Stream(device=self.device, priority=-1)
-        self.k_use = 0      # global index of the next streamed use
+        self.k_use = 0      # global index of the next streamed use to release
+        self.k_acq = 0      # global index of the next streamed use to acquire (≥ k_use)
         self.k_issued = 0   # copies enqueued so far
         self.bytes_issued = 0      # bytes moved over this rank's host link
         self.raw_bytes_issued = 0  # layer bytes this rank's copies / shards delivered
@@ -426,13 +459,18 @@ class LayerStreamer:
         if disk is not None:
             disk.start([li for li in self.streamed if isinstance(host.get(li), DiskRef)])
 
+    def seg_bytes(self, sg: int) -> int:
+        lo, hi = self.segments[sg]
+        return hi - lo
+
     @property
     def window_bytes(self) -> int:
-        return self.n_slots * self.layer_bytes + (self.ring.numel() if self.ring is not None else 0)
+        return sum(t.numel() for t in self.slots) + (self.ring.numel() if self.ring is not None else 0)
 
     def _issue(self, k: int) -> None:
         slot = k % self.n_slots
-        layer = self.streamed[k % len(self.streamed)]
+        layer, sg = self.uses[k % len(self.uses)]
+        lo, hi = self.segments[sg]
         if layer in self.shards:  # f3: NVLink all-gather of the resident 1/N shards
             start = native.Event(timing=True).record(self.comm_stream) if self.trace else None
             if k >= self.n_slots:
@@ -459,9 +497,10 @@ class LayerStreamer:
             start = native.Event(timing=True).record(self.copy_stream)
         if self.coded:
             unit = src
-            f0, f1 = self.frames[layer]
+            f0, f1 = self.frames[layer] if len(self.segments) == 1 else self.frames[(layer, sg)]
             done = self.loaded[slot] if self.world == 1 else self.copied[slot]
-            native.xc4_stream(self.slots[slot].data_ptr(), unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
+            # frames decode to their unit offset from the pointer given: the slot's virtual unit base
+            native.xc4_stream(self.slots[slot].data_ptr() - lo, unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
                               self.ring_slot_bytes, self.ring_events, self.ring_cursor, self.copy_stream,
                               self.decode_stream, self.free[slot] if k >= self.n_slots else None, done)
             if dk is not None:
@@ -472,18 +511,18 @@ class LayerStreamer:
                     gather_layer(self.slots[slot], self.rank, self.world, self.group)
                 self.loaded[slot].record(self.comm_stream)
             self.bytes_issued += unit.frame_bytes(f0, f1)
-            self.raw_bytes_issued += self.hi - self.lo
+            self.raw_bytes_issued += (self.hi - self.lo) if len(self.segments) == 1 else hi - lo
             if self.trace:
                 # two resources (T7: one timeline per stream): the copy engine moving
                 # the frames, then the decoder (and, N > 1, the all-gather) finishing the slot
                 copied = native.Event(timing=True).record(self.copy_stream)
-                self.copy_marks.append((k, layer, start, copied, "IO_C2G", "ffn_load"))
+                self.copy_marks.append((k, layer, start, copied, "IO_C2G", "ffn_load_part" if sg else "ffn_load"))
                 end_stream = self.decode_stream if self.world == 1 else self.comm_stream
                 self.copy_marks.append((k, layer, copied, native.Event(timing=True).record(end_stream),
                                         "GPU_DECODE", "ffn_decode"))
             return
         if self.world == 1:
-            native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr(), self.layer_bytes, self.chunk,
+            native.stream_layer(self.slots[slot].data_ptr(), src.data_ptr() + lo, hi - lo, self.chunk,
                                 self.copy_stream, self.loaded[slot])
             if dk is not None:
                 self.disk.release(dk, self.copy_stream)
@@ -499,9 +538,10 @@ class LayerStreamer:
         if self.trace:
             end_stream = self.copy_stream if self.world == 1 else self.comm_stream
             self.copy_marks.append((k, layer, start, native.Event(timing=True).record(end_stream), "IO_C2G",
-                                    "ffn_load"))
-        self.bytes_issued += self.hi - self.lo
-        self.raw_bytes_issued += self.hi - self.lo
+                                    "ffn_load_part" if sg else "ffn_load"))
+        moved = (self.hi - self.lo) if len(self.segments) == 1 else hi - lo
+        self.bytes_issued += moved
+        self.raw_bytes_issued += moved
 
     def _ensure_issued(self, upto: int) -> None:
         while self.k_issued <= upto:
@@ -513,21 +553,31 @@ class LayerStreamer:
         if self.streamed:
             self._ensure_issued(self.k_use + self.n_slots - 1)
 
-    def acquire(self, layer: int, stream: torch.cuda.Stream) -> int:
+    def acquire(self, layer: int, stream: torch.cuda.Stream, seg: int = 0) -> int:
+        """Make ``stream`` wait for segment ``seg`` of ``layer`` and return the unit's
+        base address (virtual for seg > 0, see the class docstring).  Uses are
+        acquired and released in pass order; up to ``n_slots`` may be held at once."""
         if layer not in self.host and layer not in self.shards:
             return self.resident[layer].data_ptr()
-        k = self.k_use
-        assert self.streamed[k % len(self.streamed)] == layer, "layers must be consumed in pass order"
+        k = self.k_acq
+        if self.uses[k % len(self.uses)] != (layer, seg):
+            raise RuntimeError(f"acquire({layer}, seg {seg}) out of pass order: next is "
+                               f"{self.uses[k % len(self.uses)]}")
+        if k >= self.k_use + self.n_slots:
+            raise RuntimeError(f"{self.n_slots} window slots are all held: release before acquiring more")
         if self.trace and self.pass_tag is not None:
             self.use_tags[k] = self.pass_tag
-        self._ensure_issued(k + self.n_slots - 1)
+        self._ensure_issued(self.k_use + self.n_slots - 1)
         self.loaded[k % self.n_slots].wait(stream)
-        return self.slots[k % self.n_slots].data_ptr()
+        self.k_acq += 1
+        return self.slots[k % self.n_slots].data_ptr() - self.segments[seg][0]
 
-    def release(self, layer: int, stream: torch.cuda.Stream) -> None:
+    def release(self, layer: int, stream: torch.cuda.Stream, seg: int = 0) -> None:
         if layer not in self.host and layer not in self.shards:
             return
         k = self.k_use
+        if self.uses[k % len(self.uses)] != (layer, seg) or k >= self.k_acq:
+            raise RuntimeError(f"release({layer}, seg {seg}) out of order or never acquired")
         self.free[k % self.n_slots].record(stream)
         self.k_use += 1
         # keep the link busy: the copy that waits on this release goes out now

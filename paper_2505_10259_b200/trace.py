@@ -18,7 +18,9 @@ import json
 
 RESOURCES = ("GPU_TARGET", "GPU_DRAFT", "CPU", "IO_C2G", "IO_G2C", "IO_DISK", "GPU_DECODE")
 LABELS = ("attn_gpu", "ffn_load", "ffn_gpu", "draft_prefill", "draft_decode", "accept", "kv_offload",
-          "disk_prefetch", "barrier", "prefill", "ffn_decode", "lm_head", "verify")
+          "disk_prefetch", "barrier", "prefill", "ffn_decode", "lm_head", "verify",
+          # split window (streamer segments): the layer's second segment and the FFN part that reads it
+          "ffn_load_part", "ffn_gpu_part")
 
 
 @dataclasses.dataclass(frozen=True)

@@ -72,6 +72,18 @@ def unit_layout(arch: ModelArch, stream_attn: bool) -> tuple[int, int]:
     return a, a + ffn_bytes
 
 
+def unit_segments(arch: ModelArch, stream_attn: bool, split: bool) -> list[tuple[int, int]]:
+    """Byte ranges the streamer moves a unit in: the whole unit, or (split
+    window) [.. gate_up | down] — the layer's first GEMM reads only the first
+    range, its second GEMM only the second (streamer.py)."""
+    off, total = unit_layout(arch, stream_attn)
+    if not split:
+        return [(0, total)]
+    if stream_attn:
+        raise ValueError("the split window streams FFN-only units")
+    return [(0, off + 2 * ffn_offsets(arch)[0]), (off + 2 * ffn_offsets(arch)[0], total)]
+
+
 @dataclasses.dataclass
 class LayerWeights:
     attn_norm: torch.Tensor

@@ -383,6 +383,70 @@ def test_trace_causality_ffn_after_its_load(pair, codec):
     assert checked >= 4
 
 
+@pytest.mark.parametrize("codec", ["none", "xc4"])
+def test_split_window_tokens_identical(pair, codec):
+    """Split window: each streamed unit moves as [gate_up | down] into its own
+    slot (one unit of HBM instead of two).  Greedy generate with slot refill —
+    single-chunk verify passes (the gate_up slot is released before down waits)
+    and multi-chunk prefill passes (both segments held) — gives exactly the
+    tokens of the whole-unit window, raw and XC4-coded."""
+    tw, dw = pair
+    prompts = tiny.prompts(13, seed=41)
+    pol = Policy(6, 4, 4, 4)
+    whole = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 3}, codec=codec)
+    want = whole.generate(prompts, 10, pol)
+    w_bytes = whole.target.streamer.window_bytes
+    del whole
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 3}, codec=codec, split_window=True)
+    st = eng.target.streamer
+    assert len(st.segments) == 2 and st.segments[1][1] == st.layer_bytes
+    ring = st.ring.numel() if st.ring is not None else 0
+    assert st.window_bytes - ring == st.layer_bytes  # one unit of slots (was two)
+    assert w_bytes - ring == 2 * st.layer_bytes
+    got = eng.generate(prompts, 10, pol)
+    assert eng.last_session.refill
+    assert got == want
+    assert st.k_acq == st.k_use and st.k_use % 6 == 0  # every acquired segment released, whole passes
+
+
+def test_split_window_trace_causality(pair):
+    """The reference's causality invariant on a split-window trace: ffn_gpu (router
+    + gate_up) starts after the layer's attention and its first segment's load,
+    ffn_gpu_part (down) after the second segment's load; per-resource
+    exclusivity and dual-batch overlap hold as with whole units."""
+    from _trace_checks import assert_causality, assert_dual_batch_overlap, assert_resource_exclusive
+
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2}, codec="xc4", split_window=True)
+    res = eng.run_decoding(Policy(16, 8, 8, 4), Workload(16, 32, 12, 0.8), acceptance=Forced(0.8))
+    labels = collections.Counter(ev.label for ev in res.trace)
+    assert labels["ffn_load_part"] > 0 and labels["ffn_gpu_part"] > 0
+    assert labels["ffn_load_part"] >= labels["ffn_gpu_part"]
+    assert_resource_exclusive(res.trace)
+    assert_dual_batch_overlap(res.trace)
+    assert assert_causality(res.trace) >= 2 * labels["ffn_gpu_part"]
+
+
+def test_split_window_order_is_enforced(pair):
+    """Segments are acquired and released in pass order, at most n_slots held."""
+    tw, dw = pair
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={1, 2}, split_window=True)
+    st, stream = eng.target.streamer, eng.tgt_stream
+    with pytest.raises(RuntimeError):
+        st.acquire(1, stream, 1)  # segment 1 before segment 0
+    st.acquire(1, stream, 0)
+    with pytest.raises(RuntimeError):
+        st.release(1, stream, 1)  # never acquired
+    st.acquire(1, stream, 1)
+    with pytest.raises(RuntimeError):
+        st.acquire(2, stream, 0)  # both slots held
+    st.release(1, stream, 0)
+    st.release(1, stream, 1)
+    st.acquire(2, stream, 0)
+    st.release(2, stream, 0)
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("draft_kv,refill", [("cached", False), ("reprefill", False), ("cached", True)])
 def test_host_resident_kv_matches(pair, draft_kv, refill):
     """Target KV in pinned host DRAM (tiny-HBM budgets): each pass stages one

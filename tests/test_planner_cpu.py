@@ -136,3 +136,20 @@ def test_disk_tier_spill():
     host_units = len(p.stream_layers) - len(p.disk_layers)
     assert (host_units + 2) * p.host_bytes / len(p.stream_layers) <= 60e9 * 1.001
     assert p.t_disk_s > 0 and p.t_round_s >= p.t_disk_s
+
+
+def test_split_window_frees_one_unit_of_hbm_for_kv():
+    """A split window ([gate_up | down] segments, one slot each) holds one
+    unit instead of two: the fixed HBM drops by a unit and the planner spends
+    it on the batch."""
+    kw = dict(stream_ratio=0.7, ring_bytes=800 << 20, stream_attn_modes=(False,))
+    whole = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(178e9), int(193e9), 8, 0.8, 503, 16, RATES, **kw)
+    split = plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(178e9), int(193e9), 8, 0.8, 503, 16, RATES,
+                         split_window=True, **kw)
+    unit = ffn_offsets(MIXTRAL_8X22B)[2]
+    assert split.split_window and not whole.split_window
+    assert whole.hbm_bytes["fixed"] - split.hbm_bytes["fixed"] == unit
+    assert split.bs_decoding >= whole.bs_decoding and split.tokens_per_s >= whole.tokens_per_s
+    with pytest.raises(ValueError):
+        plan_offload(MIXTRAL_8X22B, MISTRAL_7B_V3, int(178e9), int(193e9), 8, 0.8, 503, 16, RATES,
+                     split_window=True, world=2)

@@ -90,3 +90,19 @@ def test_invariants_catch_violations():
     with pytest.raises(AssertionError, match="no draft"):
         assert_dual_batch_overlap(nodraft)
     assert_dual_batch_overlap(nodraft, allow_verify_only={3})
+
+
+def test_causality_split_window_parts():
+    """Split window: the down part (ffn_gpu_part) is checked against its own
+    segment's load (ffn_load_part); starting it before that load ends fails."""
+    evs = [SimEvent("IO_C2G", 0.0, 0.010, "ffn_load", 0, 0, 0),
+           SimEvent("IO_C2G", 0.010, 0.015, "ffn_load_part", 0, 0, 0),
+           SimEvent("GPU_TARGET", 0.0, 0.002, "attn_gpu", 0, 0, 0),
+           SimEvent("GPU_TARGET", 0.010, 0.012, "ffn_gpu", 0, 0, 0),
+           SimEvent("GPU_TARGET", 0.015, 0.016, "ffn_gpu_part", 0, 0, 0)]
+    assert assert_causality(evs) == 2
+    early = evs[:4] + [SimEvent("GPU_TARGET", 0.012, 0.016, "ffn_gpu_part", 0, 0, 0)]
+    with pytest.raises(AssertionError):
+        assert_causality(early)
+    with pytest.raises(AssertionError):  # a part with no segment load recorded
+        assert_causality([e for e in evs if e.label != "ffn_load_part"])

@@ -119,13 +119,42 @@ def _layer_fp32(eng, li, L, unit, streamed, x, pos, state, bs, T, routing=None):
     return h + y, lr
 
 
+class _SegUnit:
+    """A streamed unit held as several window slots (split window): element
+    slices map to the segment that holds them (a slice never spans two)."""
+
+    def __init__(self, parts, off=0):
+        self.parts, self.off = parts, off  # [(first element, bf16 view)]
+
+    def __getitem__(self, sl):
+        a = (sl.start or 0) + self.off
+        for lo, t in self.parts:
+            if lo <= a < lo + t.numel():
+                if sl.stop is None:
+                    return _SegUnit(self.parts, a) if a - lo else (
+                        t if len(self.parts) == 1 or lo == self.parts[-1][0] else _SegUnit(self.parts, a))
+                b = sl.stop + self.off
+                assert b <= lo + t.numel(), "slice spans two window segments"
+                return t[a - lo:b - lo]
+        raise IndexError(sl)
+
+
 def _unit(eng, li, L, stream):
     st = eng.target.streamer
     streamed = st is not None and li in st.streamed
     if streamed:
-        st.acquire(li, stream)  # the stream waits for the slot; k_use indexes it until release
-        return st.slots[st.k_use % st.n_slots].view(torch.bfloat16), True
+        parts = []
+        for sg, (lo, _) in enumerate(st.segments):
+            st.acquire(li, stream, sg)  # the stream waits for the slot; k_acq - 1 indexes it
+            parts.append((lo // 2, st.slots[(st.k_acq - 1) % st.n_slots].view(torch.bfloat16)))
+        return (parts[0][1] if len(parts) == 1 else _SegUnit(parts)), True
     return L.ffn, False
+
+
+def _release(eng, li, stream):
+    st = eng.target.streamer
+    for sg in range(len(st.segments)):
+        st.release(li, stream, sg)
 
 
 def verify_fp32(eng, state: SeqState, draft_tokens: torch.Tensor, stream) -> torch.Tensor:
@@ -142,7 +171,7 @@ def verify_fp32(eng, state: SeqState, draft_tokens: torch.Tensor, stream) -> tor
             unit, streamed = _unit(eng, li, L, stream)
             x, _ = _layer_fp32(eng, li, L, unit, streamed, x, pos, state, bs, T)
             if streamed:
-                st.release(li, stream)
+                _release(eng, li, stream)
         xf = _rms(x, w.final_norm, tm.arch.eps)
         return (xf @ w.lm_head.float().T).view(bs, T, -1)
 
@@ -201,7 +230,7 @@ def verify_teacher_forced(eng, state: SeqState, draft_tokens: torch.Tensor, stre
             x_in = xs[li].float()
             ref, lr = _layer_fp32(eng, li, L, unit, streamed, x_in, pos, state, bs, T, routing=sel)
             if streamed:
-                st.release(li, stream)
+                _release(eng, li, stream)
             out = xs[li + 1].float()
             d = (out - ref).abs()
             upd = ref - x_in
