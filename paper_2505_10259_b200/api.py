@@ -41,9 +41,9 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     (default: a temporary file) and staged through pinned DRAM each pass.
     ``arith="canonical"`` runs both models through the parity-mode kernels
     (fixed IEEE order, bit-identical to the CPU oracle; tiny shapes only).
-    ``split_window``: each streamed unit moves as [gate_up | down] into its
-    own slot, so the HBM window is one unit instead of ``n_slots`` units
-    (single GPU, FFN-only units; the link still runs a unit ahead)."""
+    ``split_window``: each streamed unit moves as [(attention +) gate_up | down]
+    into its own slot, so the HBM window is one unit instead of ``n_slots``
+    units (single GPU, host DRAM; the link still runs a unit ahead)."""
     if codec not in ("none", "xc4"):
         raise ValueError(f"unknown codec {codec!r}")
     dev = torch.device(device)
@@ -68,12 +68,11 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
     segments = W.unit_segments(target_arch, stream_attn, split_window)
     if split_window and (world > 1 or shard_layers or disk_layers):
         raise ValueError("split_window is single-GPU and host-DRAM only")
-    enc = (C.Encoder(dev, align_elems=segments[0][1] // 2 if split_window else 0)
-           if codec == "xc4" and stream_layers else None)
+    enc = C.Encoder(dev) if codec == "xc4" and stream_layers else None
     if target_weights is not None:
         store = host_store or HostStore()
         tw = W.from_logical(target_arch, target_weights, dev, stream_layers, stream_attn, encoder=enc,
-                            host_alloc=store.alloc)
+                            host_alloc=store.alloc, segments=segments)
     elif shared_store is not None:
         sink = shared_store.write_coded if enc is not None else shared_store.write_slice
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_sink=sink,
@@ -82,7 +81,7 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
         store = host_store or HostStore()
         tw = W.synthetic(target_arch, dev, seed=seed, stream_layers=stream_layers, host_alloc=store.alloc,
                          stream_attn=stream_attn, encoder=enc, shard_layers=shard_layers, shard=(rank, world),
-                         disk=disk, disk_layers=disk_layers)
+                         disk=disk, disk_layers=disk_layers, segments=segments)
     if enc is not None:
         enc.release()
         torch.cuda.empty_cache()  # hand the encoder's staging back before KV / workspaces are sized

@@ -26,24 +26,13 @@ MIN_FRAME_ELEMS = 4096
 SLICE_WORLD = 8             # frames split evenly over 1, 2, 4 or 8 ranks when the unit allows it
 
 
-def frame_elems_for(n_elems: int, world: int = SLICE_WORLD, align_elems: int = 0) -> int:
+def frame_elems_for(n_elems: int, world: int = SLICE_WORLD) -> int:
     """Largest frame (a multiple of 4096 weights, ≤ 32 Mi) that tiles the unit
     into a multiple of ``world`` whole frames — any divisor works, so awkward
     unit sizes (e.g. attention + FFN units, 2^22·597 weights) still get frames
     of tens of MB rather than a power of two small enough to divide them.
     Units that cannot split evenly fall back to world = 1, then to a partial
-    last frame (single rank only).  ``align_elems`` > 0: frames must also tile
-    [0, align_elems) exactly — a split window's segment boundary (streamer.py)."""
-    if align_elems:
-        for w in (world, 1):
-            if n_elems % w:
-                continue
-            share = n_elems // w
-            for k in range(max(1, -(-share // MAX_FRAME_ELEMS)), share // MIN_FRAME_ELEMS + 1):
-                fe = share // k
-                if share % k == 0 and fe % MIN_FRAME_ELEMS == 0 and align_elems % fe == 0:
-                    return fe
-        raise ValueError(f"no XC4 frame size tiles both {n_elems} and {align_elems} weights")
+    last frame (single rank only)."""
     for w in (world, 1):
         if n_elems % w:
             continue
@@ -106,13 +95,36 @@ class XC4Unit:
         return int(np.max(np.diff(self.frame_off)))
 
 
+@dataclasses.dataclass
+class XC4Parts:
+    """A streamed unit encoded as independent XC4 units, one per window segment
+    (split window, streamer.py): segment s decodes from its own frame 0 into
+    its own slot, so segment boundaries need not fall on frame boundaries."""
+
+    parts: list
+
+    @property
+    def nbytes(self) -> int:
+        return sum(u.nbytes for u in self.parts)
+
+    @property
+    def raw_bytes(self) -> int:
+        return sum(u.raw_bytes for u in self.parts)
+
+    @property
+    def ratio(self) -> float:
+        return self.nbytes / self.raw_bytes
+
+    def max_frame_bytes(self) -> int:
+        return max(u.max_frame_bytes() for u in self.parts)
+
+
 class Encoder:
     """Device-side XC4 encoder with grow-only scratch (setup time only)."""
 
-    def __init__(self, device, world: int = SLICE_WORLD, code_bits: int = 0, align_elems: int = 0):
+    def __init__(self, device, world: int = SLICE_WORLD, code_bits: int = 0):
         self.device = torch.device(device)
         self.world = world
-        self.align_elems = align_elems  # split window: frames also tile the segment boundary
         self.code_bits = code_bits  # 0 = per unit, the smaller of 3- and 4-bit codes
         self._scratch = None
         self._dst = None
@@ -132,7 +144,7 @@ class Encoder:
         if flat.dtype != torch.bfloat16:
             flat = flat.view(torch.bfloat16)
         n = flat.numel()
-        fe = frame_elems_for(n, self.world, self.align_elems)
+        fe = frame_elems_for(n, self.world)
         scratch = self._grow("_scratch", native.xc4_scratch_bytes(n, fe))
         nbytes, _ = native.xc4_encode(flat, fe, None, scratch, code_bits=self.code_bits)
         dst = self._grow("_dst", nbytes)
@@ -152,6 +164,15 @@ def encode_to_host(unit: torch.Tensor, encoder: Encoder, host_alloc=None) -> XC4
     buf = buf.view(torch.uint8)[: dev.numel()]
     buf.copy_(dev)
     return XC4Unit.parse(buf)
+
+
+def encode_segments_to_host(unit: torch.Tensor, encoder: Encoder, segments, host_alloc=None):
+    """One XC4Unit for the whole unit, or (``segments`` = byte ranges of a split
+    window) an XC4Parts with one independently encoded unit per range."""
+    if not segments or len(segments) == 1:
+        return encode_to_host(unit, encoder, host_alloc)
+    flat = unit.reshape(-1).view(torch.uint8)
+    return XC4Parts([encode_to_host(flat[lo:hi].view(torch.bfloat16), encoder, host_alloc) for lo, hi in segments])
 
 
 def decode_unit(u: XC4Unit, out: torch.Tensor) -> None:

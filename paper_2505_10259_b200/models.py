@@ -157,14 +157,16 @@ class CausalLM:
                 hook(li, "attn_start", stream)
             kc, vc = kv.layer(li, stream)
             base = None
-            split = self._split(li)  # [gate_up | down] in two window slots (streamer segments)
+            split = self._split(li)  # [.. gate_up | down] in two window slots (streamer segments)
             base_dn = None
             wqkv, wo = L.wqkv, L.wo
+            ffn_off = 0  # the FFN's byte offset inside the streamed unit
             if wqkv is None:  # attention weights stream with the layer: wait before QKV
                 unit = self._ffn_acquire(li, L, stream)
                 wqkv = _RawView(unit, (a.qkv_rows, H))
                 wo = _RawView(unit + a.qkv_rows * H * 2, (H, q_dim))
-                base = unit + (a.qkv_rows * H + H * q_dim) * 2
+                ffn_off = (a.qkv_rows * H + H * q_dim) * 2
+                base = unit + ffn_off
             for ci, c in enumerate(chunks):
                 T = c.T
                 x = xa[c.row0:c.row0 + T]
@@ -200,7 +202,7 @@ class CausalLM:
                         # one chunk: gate_up's slot goes back to the link before down waits for its own
                         if len(chunks) == 1:
                             self.streamer.release(li, stream, 0)
-                        base_dn = self.streamer.acquire(li, stream, 1)
+                        base_dn = self.streamer.acquire(li, stream, 1) + ffn_off
                         if hook:
                             hook(li, "ffn_part", stream)
                     else:

@@ -79,7 +79,7 @@ class OffloadPlan:
     disk_layers: tuple[int, ...] = ()   # f4: streamed layers kept on disk (subset of stream_layers)
     t_disk_s: float = 0.0
     kv_host: bool = False               # target KV in pinned host DRAM, one batch staged per layer
-    split_window: bool = False  # FFN units move as [gate_up | down] segments: n_slots / 2 units of window
+    split_window: bool = False  # units move as [.. gate_up | down] segments: n_slots / 2 units of window
 
     def as_dict(self) -> dict:
         d = dataclasses.asdict(self)
@@ -170,9 +170,9 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     moves the verified batch's KV host → GPU (the write-back uses the other
     link direction).
 
-    ``split_window`` (single GPU): FFN-only units stream as [gate_up | down]
+    ``split_window`` (single GPU): units stream as [(attention +) gate_up | down]
     segments, one slot each, so the window costs n_slots / 2 units of HBM
-    (streamer.py); units that carry the attention projections keep whole slots."""
+    (streamer.py)."""
     if split_window and (world > 1 or n_slots % 2):
         raise ValueError("split_window needs world == 1 and an even slot count")
     # commits per verification: E[k], or the caller's steady-state figure (clamped requests,
@@ -188,7 +188,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
         # unit = bytes of one streamed (or pinned) layer; with stream_attn the
         # attention projections travel with the FFN and leave the resident set
         layer_bytes = unit_layout(target, stream_attn)[1]
-        window_units = n_slots // 2 if (split_window and not stream_attn) else n_slots
+        window_units = n_slots // 2 if split_window else n_slots
         fixed = (resident_bytes(target, False) - (target.n_layer * attn_layer if stream_attn else 0)
                  + resident_bytes(draft, True) + window_units * layer_bytes
                  + (ring_bytes if stream_ratio < 1 else 0))
@@ -280,7 +280,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                         "shards": int(n_sh * layer_bytes / world)},
                        streamed * host_unit, S, t_stream, t_comp, t_round, bs * e_tok, tps, sa, stream_ratio,
                        kc if mode == "mixed" else 0, shard_l, world, t_nvl, disk_l,
-                       n_disk * host_unit / rates.disk_bytes_per_s, kv_host, split_window and not sa)
+                       n_disk * host_unit / rates.disk_bytes_per_s, kv_host, split_window)
 
 
 def roofline_tokens_per_s(committed_per_round: float, streamed_bytes: int, flops: float,

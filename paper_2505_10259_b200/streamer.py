@@ -25,7 +25,7 @@ import weakref
 import torch
 
 from . import native
-from .codec import Cursor, XC4Unit
+from .codec import Cursor, XC4Parts, XC4Unit
 from .errors import InsufficientTotalMemory
 
 
@@ -394,7 +394,7 @@ class LayerStreamer:
             raise ValueError("a layer is either host-streamed or HBM-sharded")
         # host values are raw pinned uint8 tensors, or XC4Unit (K9: encoded
         # frames cross the link and are decoded into the slot on the GPU)
-        kinds = {isinstance(v.meta if isinstance(v, DiskRef) else v, XC4Unit) for v in host.values()}
+        kinds = {isinstance(v.meta if isinstance(v, DiskRef) else v, (XC4Unit, XC4Parts)) for v in host.values()}
         self.coded = kinds == {True}
         if len(kinds) > 1:
             raise ValueError("streamed layers must be all raw or all XC4-encoded")
@@ -425,17 +425,14 @@ class LayerStreamer:
             for u in metas.values():
                 if u.raw_bytes != layer_bytes:
                     raise ValueError(f"XC4 unit decodes to {u.raw_bytes} B, slot holds {layer_bytes} B")
+                if isinstance(u, XC4Parts) != (S > 1) or (S > 1 and [p.raw_bytes for p in u.parts] != [
+                        self.seg_bytes(sg) for sg in range(S)]):
+                    raise ValueError("a split window streams XC4Parts encoded per segment "
+                                     "(codec.encode_segments_to_host), a whole window XC4Units")
             if S == 1:
                 self.frames = {li: u.frame_range(rank, world) for li, u in metas.items()}
-            else:  # a segment's frames decode to exactly its byte range
-                self.frames = {}
-                for li, u in metas.items():
-                    fb = 2 * u.frame_elems
-                    for sg, (lo, hi) in enumerate(self.segments):
-                        if lo % fb or (hi % fb and hi != layer_bytes):
-                            raise ValueError(f"segment [{lo}, {hi}) does not fall on XC4 frame boundaries "
-                                             f"({fb} B frames): encode with codec.Encoder(align_elems=…)")
-                        self.frames[(li, sg)] = (lo // fb, -(-hi // fb))
+            else:  # every segment is its own XC4 unit: all its frames, decoded from its own slot base
+                self.frames = {(li, sg): (0, p.n_frames) for li, u in metas.items() for sg, p in enumerate(u.parts)}
             self.ring_slot_bytes = (max(u.max_frame_bytes() for u in metas.values()) + 255) // 256 * 256
             self.ring = torch.empty(self.RING_SLOTS * self.ring_slot_bytes, dtype=torch.uint8, device=self.device)
             self.ring_events = [native.Event() for _ in range(2 * self.RING_SLOTS)]
@@ -496,11 +493,14 @@ class LayerStreamer:
         if self.trace:
             start = native.Event(timing=True).record(self.copy_stream)
         if self.coded:
-            unit = src
-            f0, f1 = self.frames[layer] if len(self.segments) == 1 else self.frames[(layer, sg)]
+            if len(self.segments) == 1:
+                unit = src
+                f0, f1 = self.frames[layer]
+            else:
+                unit = src.parts[sg]
+                f0, f1 = self.frames[(layer, sg)]
             done = self.loaded[slot] if self.world == 1 else self.copied[slot]
-            # frames decode to their unit offset from the pointer given: the slot's virtual unit base
-            native.xc4_stream(self.slots[slot].data_ptr() - lo, unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
+            native.xc4_stream(self.slots[slot].data_ptr(), unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
                               self.ring_slot_bytes, self.ring_events, self.ring_cursor, self.copy_stream,
                               self.decode_stream, self.free[slot] if k >= self.n_slots else None, done)
             if dk is not None:

@@ -74,14 +74,14 @@ def unit_layout(arch: ModelArch, stream_attn: bool) -> tuple[int, int]:
 
 def unit_segments(arch: ModelArch, stream_attn: bool, split: bool) -> list[tuple[int, int]]:
     """Byte ranges the streamer moves a unit in: the whole unit, or (split
-    window) [.. gate_up | down] — the layer's first GEMM reads only the first
-    range, its second GEMM only the second (streamer.py)."""
+    window) [attention projections (if streamed) + gate_up | down] — the
+    layer reads the first range up to its gate_up GEMM and the second only in
+    its down GEMM (streamer.py)."""
     off, total = unit_layout(arch, stream_attn)
     if not split:
         return [(0, total)]
-    if stream_attn:
-        raise ValueError("the split window streams FFN-only units")
-    return [(0, off + 2 * ffn_offsets(arch)[0]), (off + 2 * ffn_offsets(arch)[0], total)]
+    cut = off + 2 * ffn_offsets(arch)[0]  # [Wqkv | Wo |] gate_up  ‖  down
+    return [(0, cut), (cut, total)]
 
 
 @dataclasses.dataclass
@@ -114,12 +114,13 @@ class ModelWeights:
 
 
 def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = frozenset(),
-                 stream_attn: bool = False, encoder=None, host_alloc=None) -> ModelWeights:
+                 stream_attn: bool = False, encoder=None, host_alloc=None, segments=None) -> ModelWeights:
     """Build device weights from logical (HF-shaped) arrays — numpy or torch.
     With ``encoder`` (codec.Encoder) the streamed units are kept XC4-encoded.
     Streamed units go to ``host_alloc(nbytes)`` (e.g. HostStore.alloc: exact-size
     page-locked mmaps) — torch's pinned allocator would round each unit up to a
-    power of two and cache it (8 GiB per 5 GB 8x22B layer)."""
+    power of two and cache it (8 GiB per 5 GB 8x22B layer).  ``segments``
+    (split window): byte ranges encoded as independent XC4 units."""
     dev = torch.device(device)
     layers = []
     host = {}
@@ -132,7 +133,7 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
                 packed = torch.cat([wqkv.reshape(-1), wo.reshape(-1), packed])
                 wqkv = wo = None
             if encoder is not None:
-                host[li] = codec.encode_to_host(packed.to(dev), encoder, host_alloc)
+                host[li] = codec.encode_segments_to_host(packed.to(dev), encoder, segments, host_alloc)
             elif dev.type != "cuda":
                 host[li] = packed
             elif host_alloc is not None:
@@ -159,7 +160,7 @@ def from_logical(arch: ModelArch, W: dict, device, stream_layers: set[int] = fro
 def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = frozenset(),
               host_alloc=None, std: float = 0.02, host_sink=None, stream_attn: bool = False,
               encoder=None, shard_layers: set[int] = frozenset(), shard: tuple[int, int] = (0, 1),
-              disk=None, disk_layers: set[int] = frozenset()) -> ModelWeights:
+              disk=None, disk_layers: set[int] = frozenset(), segments=None) -> ModelWeights:
     """Random-init weights of the given shape (N(0, 0.02²), norms = 1).
 
     Generated on the GPU; streamed FFN layers are generated in HBM one at a
@@ -207,7 +208,7 @@ def synthetic(arch: ModelArch, device, seed: int = 0, stream_layers: set[int] = 
             if host_sink is not None:
                 host[li] = host_sink(li, encoder.encode(unit)[0])
             else:
-                host[li] = codec.encode_to_host(unit, encoder, host_alloc)
+                host[li] = codec.encode_segments_to_host(unit, encoder, segments, host_alloc)
         elif streamed and host_sink is not None:
             host[li] = host_sink(li, unit).view(torch.bfloat16)
         elif streamed:

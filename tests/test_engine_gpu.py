@@ -151,6 +151,21 @@ def test_streamed_attention_weights_match(pair):
     assert eng.generate(prompts, 10, pol) == ref
 
 
+@pytest.mark.parametrize("codec", ["none", "xc4"])
+def test_split_window_with_streamed_attention(pair, codec):
+    """H3 units under a split window: [Wqkv | Wo | gate_up] in one slot, down in
+    the other (XC4: one encoded unit per segment) — the resident result."""
+    tw, dw = pair
+    prompts = tiny.prompts(6, seed=17)
+    pol = Policy(6, 3, 3, 4)
+    ref = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=set()).generate(prompts, 10, pol)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 2, 3}, stream_attn=True, codec=codec,
+                       split_window=True)
+    st = eng.target.streamer
+    assert len(st.segments) == 2 and st.segments[0][1] > st.layer_bytes // 2  # attention rides in segment 0
+    assert eng.generate(prompts, 10, pol) == ref
+
+
 def test_draft_chunking_matches(pair):
     tw, dw = pair
     prompts = tiny.prompts(8, seed=3)
