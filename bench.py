@@ -566,7 +566,9 @@ def main():
     codec_k = None
     if st is not None and st.coded:
         try:
-            u = st.host[st.streamed[0]]
+            u0 = st.host[st.streamed[0]]
+            u = u0.parts[0] if hasattr(u0, "parts") else u0  # split window: the first segment's unit
+            frames_per_layer = sum(p.n_frames for p in u0.parts) if hasattr(u0, "parts") else u.n_frames
             nf = min(st.RING_SLOTS, u.n_frames)
             # frames [0, nf) copied contiguously into the staging ring; the decoder
             # addresses frame f at base + frame_off[f], so base = ring − frame_off[0]
@@ -589,8 +591,8 @@ def main():
             codec_k = {"kernel": "xc4_decode_kernel (K9)", "bound": "hbm", "achieved": algo / t_d / 1e9,
                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": algo / t_d / 1e9 / peaks["hbm_gbs"],
                        "ms_per_launch_group": t_d * 1e3, "frames": nf, "algorithmic_bytes": algo,
-                       "ms_per_layer_est": t_d * 1e3 * u.n_frames / nf, "ratio": u.ratio, "escapes": u.n_escapes,
-                       "frames_per_layer": u.n_frames,
+                       "ms_per_layer_est": t_d * 1e3 * frames_per_layer / nf, "ratio": u0.ratio,
+                       "escapes": u.n_escapes, "frames_per_layer": frames_per_layer,
                        "note": "algorithmic bytes = encoded frames read + decoded bf16 written"}
         except Exception as exc:
             codec_k = {"error": str(exc)}

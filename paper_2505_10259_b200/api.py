@@ -91,7 +91,8 @@ def build_engine(target_arch: ModelArch, draft_arch: ModelArch, target_weights: 
         dw = W.synthetic(draft_arch, dev, seed=seed + 1)
     _, ffn_bytes = W.unit_layout(target_arch, stream_attn)  # bytes of one streamed layer unit
     resident = {li: L.ffn for li, L in enumerate(tw.layers) if L.ffn is not None}
-    host = {li: t if isinstance(t, (C.XC4Unit, DiskRef)) else t.view(torch.uint8) for li, t in tw.host_ffn.items()}
+    host = {li: t if isinstance(t, (C.XC4Unit, C.XC4Parts, DiskRef)) else t.view(torch.uint8)
+            for li, t in tw.host_ffn.items()}
     streamer = LayerStreamer(ffn_bytes, resident, host, target_arch.n_layer, dev, n_slots=n_slots,
                              chunk_bytes=chunk_bytes, rank=rank, world=world, group=group,
                              shards=tw.shard_ffn, disk=disk, segments=segments) if (host or tw.shard_ffn) else None
