@@ -61,9 +61,9 @@ def parse():
                          "pool's 196 GiB boxes; lowered to MemAvailable − 12 GB only if the box has less)")
     ap.add_argument("--hbm-gb", type=float, default=0.0, help="HBM budget (0 = device; 8x7b config: 24 GiB cap)")
     ap.add_argument("--slots", type=int, default=2)
-    ap.add_argument("--window", choices=("split", "whole"), default="whole",
-                    help="split: streamed FFN units move as [gate_up | down] segments, one window slot each "
-                         "(one unit of HBM instead of --slots units; single GPU)")
+    ap.add_argument("--window", choices=("split", "whole"), default="split",
+                    help="split: streamed units move as [(attention +) gate_up | down] segments, one window slot "
+                         "each (one unit of HBM instead of --slots units; single GPU — N > 1 uses whole units)")
     ap.add_argument("--draft-kv", choices=("auto", "cached", "reprefill", "mixed"), default="auto",
                     help="draft KV policy (auto = planner)")
     ap.add_argument("--layers", type=int, default=0,
