@@ -604,6 +604,8 @@ def main():
         try:
             del s
             torch.cuda.empty_cache()
+            if plan.split_window:  # prefill passes hold both segments of a layer: double-buffer each
+                eng.set_window_slots(2 * args.slots)
             # Its own slot pool: with prefill inside every round the generate workload is
             # tensor-bound, not link-bound, so the draft keeps a KV row per slot (no
             # per-round context re-prefill) and HBM left after the engine's weights

@@ -284,6 +284,15 @@ class Engine:
         for arena in self._arenas.values():
             arena.reset()
 
+    def set_window_slots(self, n_slots: int) -> None:
+        """Resize the target's streamed-layer window between passes
+        (``LayerStreamer.resize``): e.g. widen a split window to two slots per
+        segment before a prefill-heavy ``generate()``, whose multi-chunk
+        passes hold a layer's segments together."""
+        if self.target.streamer is not None:
+            torch.cuda.synchronize(self.device)
+            self.target.streamer.resize(n_slots)
+
     def new_session(self, n_seq: int, bs_decoding: int, max_len: int, n_cand: int, mode: str = "greedy",
                     seed: int = 0, temperature: float = 1.0, forced_p: float | None = None,
                     bs_draft: int | None = None, draft_kv: str = "cached",

@@ -442,6 +442,7 @@ class LayerStreamer:
         self.k_use = 0      # global index of the next streamed use to release
         self.k_acq = 0      # global index of the next streamed use to acquire (≥ k_use)
         self.k_issued = 0   # copies enqueued so far
+        self.k_base = 0     # first use of the current slot map (resize): earlier uses left no free events
         self.bytes_issued = 0      # bytes moved over this rank's host link
         self.raw_bytes_issued = 0  # layer bytes this rank's copies / shards delivered
         self.nvlink_bytes_issued = 0  # bytes this rank receives in the all-gathers
@@ -470,7 +471,7 @@ class LayerStreamer:
         lo, hi = self.segments[sg]
         if layer in self.shards:  # f3: NVLink all-gather of the resident 1/N shards
             start = native.Event(timing=True).record(self.comm_stream) if self.trace else None
-            if k >= self.n_slots:
+            if k - self.n_slots >= self.k_base:
                 self.free[slot].wait(self.comm_stream)
             with torch.cuda.stream(self.comm_stream):
                 gather_shards(self.slots[slot], self.shards[layer], self.group)
@@ -481,7 +482,7 @@ class LayerStreamer:
                 self.copy_marks.append((k, layer, start, native.Event(timing=True).record(self.comm_stream),
                                         "IO_C2G", "ffn_load"))
             return
-        if k >= self.n_slots and not self.coded:  # coded: the decoder waits instead, the link runs ahead
+        if k - self.n_slots >= self.k_base and not self.coded:  # coded: the decoder waits, the link runs ahead
             self.free[slot].wait(self.copy_stream)
         src = self.host[layer]
         dk = None
@@ -502,7 +503,8 @@ class LayerStreamer:
             done = self.loaded[slot] if self.world == 1 else self.copied[slot]
             native.xc4_stream(self.slots[slot].data_ptr(), unit.data.data_ptr(), f0, f1, self.ring.data_ptr(),
                               self.ring_slot_bytes, self.ring_events, self.ring_cursor, self.copy_stream,
-                              self.decode_stream, self.free[slot] if k >= self.n_slots else None, done)
+                              self.decode_stream, self.free[slot] if k - self.n_slots >= self.k_base else None,
+                              done)
             if dk is not None:
                 self.disk.release(dk, self.copy_stream)
             if self.world > 1:
@@ -542,6 +544,30 @@ class LayerStreamer:
         moved = (self.hi - self.lo) if len(self.segments) == 1 else hi - lo
         self.bytes_issued += moved
         self.raw_bytes_issued += moved
+
+    def resize(self, n_slots: int) -> None:
+        """Change the window's slot count between passes (nothing held).  E.g. a
+        split window (one unit of HBM) for link-bound decode rounds, widened to
+        two slots per segment (two units) for prefill-heavy passes, whose
+        multi-chunk layers hold both segments at once and would otherwise stop
+        the link for the whole layer.  Synchronises the device; copies already
+        issued ahead are dropped and re-issued into the new slot map."""
+        S = len(self.segments)
+        if not self.streamed or n_slots == self.n_slots:
+            return
+        if n_slots < 2 or n_slots % S:
+            raise ValueError(f"{n_slots} slots cannot hold {S} segments per unit, double-buffered")
+        if self.k_acq != self.k_use:
+            raise RuntimeError("resize while window slots are held")
+        torch.cuda.synchronize(self.device)  # every issued copy / decode has landed; no slot is read
+        self.slots = [self.slots[j] if j < len(self.slots) else
+                      torch.empty(self.seg_bytes(j % S), dtype=torch.uint8, device=self.device)
+                      for j in range(n_slots)]
+        for evs in (self.loaded, self.free) + ((self.copied,) if self.copied else ()):
+            del evs[n_slots:]
+            evs.extend(native.Event() for _ in range(n_slots - len(evs)))
+        self.n_slots = n_slots
+        self.k_issued = self.k_base = self.k_use
 
     def _ensure_issued(self, upto: int) -> None:
         while self.k_issued <= upto:

@@ -425,6 +425,25 @@ def test_split_window_tokens_identical(pair, codec):
     assert st.k_acq == st.k_use and st.k_use % 6 == 0  # every acquired segment released, whole passes
 
 
+def test_split_window_resize_between_passes(pair):
+    """A split window widened to two slots per segment (Engine.set_window_slots)
+    between generate() calls, and narrowed back: the same tokens every time."""
+    tw, dw = pair
+    prompts = tiny.prompts(13, seed=43)
+    pol = Policy(6, 4, 4, 4)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 3}, codec="xc4", split_window=True)
+    st = eng.target.streamer
+    want = eng.generate(prompts, 10, pol)
+    eng.set_window_slots(4)
+    assert st.n_slots == 4 and len(st.slots) == 4 and st.window_bytes - st.ring.numel() == 2 * st.layer_bytes
+    assert eng.generate(prompts, 10, pol) == want
+    eng.set_window_slots(2)
+    assert st.n_slots == 2 and st.window_bytes - st.ring.numel() == st.layer_bytes
+    assert eng.generate(prompts, 10, pol) == want
+    with pytest.raises(ValueError):
+        eng.set_window_slots(3)
+
+
 def test_split_window_trace_causality(pair):
     """The reference's causality invariant on a split-window trace: ffn_gpu (router
     + gate_up) starts after the layer's attention and its first segment's load,
