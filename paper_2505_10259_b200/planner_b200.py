@@ -201,11 +201,11 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
             else:
                 kcs = [bs if mode == "cached" else 0]
             for kc in kcs:
-                # re-prefill scratch chunk: max_draft_chunk sequences or half of it (1.3 GB less
-                # activation scratch at Mistral-7B shapes — KV for more cached draft rows); with
-                # host-resident KV (tiny HBM budgets) also a quarter
+                # re-prefill scratch chunk: max_draft_chunk sequences; with host-resident
+                # KV (tiny HBM budgets) the largest of it, ½ and ¼ that fits (half-size chunks
+                # at full HBM were measured draft-bound: profiles/bench_r2.json r2mm)
                 chunks = [bs] if mode == "cached" else sorted(
-                    {min(bs, max_draft_chunk >> k) for k in range(3 if kv_host else 2)}, reverse=True)
+                    {min(bs, max_draft_chunk >> k) for k in range(3 if kv_host else 1)}, reverse=True)
                 for bs_draft in chunks:
                     draft_rows = 2 * kc + (bs_draft if kc < bs else 0)
                     tkv_bytes = PagedKVCache.bytes_needed(target, 2 * bs, max_len, page_size)
