@@ -47,6 +47,9 @@ class B200Rates:
     # effective).  Planned at 0.70: a 6 % margin under that
     tensor_efficiency: float = 0.70
     round_overhead_s: float = 0.004        # host enqueue + barrier per round
+    # a draft decode step is a pass over the draft's weights: K5c's whole-launch rate at decode shapes
+    # (O 14.8 µs, down 31.3 µs = 3.75 TB/s, profiles/kernels_r2.md) ≈ 0.57 of the HBM peak
+    decode_hbm_efficiency: float = 0.57
     # NVLink 5 all-gather bus bandwidth per GPU (B200_PROFILING.md: 770 GB/s measured peer copy
     # per direction, 725 GB/s 8-rank all-reduce bus bandwidth); planning value with margin
     nvlink_bytes_per_s: float = 650e9
@@ -233,7 +236,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
                 # the smaller chunks of host-KV plans pay the extra passes explicitly
                 if bs_draft < min(bs, max_draft_chunk) and kc < bs:
                     extra = -(-(bs - kc) // bs_draft) - -(-(bs - kc) // max_draft_chunk)
-                    t_base += n_cand * extra * draft_w / rates.hbm_bytes_per_s
+                    t_base += n_cand * extra * draft_w / (rates.hbm_bytes_per_s * rates.decode_hbm_efficiency)
                 p0 = min(L, int(free // layer_bytes), cap)
                 for n_sh in (range(0, L - p0 + 1) if (world > 1 and allow_shards) else (0,)):
                     room = free - n_sh * layer_bytes / world
