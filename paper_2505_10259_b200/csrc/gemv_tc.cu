@@ -168,18 +168,35 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer: this CTA's k-blocks of each of the cluster's tiles =====
+      // The weights never depend on the previous kernel: the first `stages` weight tiles are
+      // requested before griddep_wait(), so under programmatic dependent launch they stream
+      // while the kernel that produces X (and the residual) finishes; X loads follow the wait.
+      const uint32_t pre = (uint32_t)stages;
+      {
+        uint32_t it = 0;
+        for (int tile = cluster; tile < n_tiles && it < pre; tile += n_clusters)
+          for (int kb = kb_lo; kb < kb_hi && it < pre; ++kb, ++it) {
+            mbar_expect_tx(&full[it], stage_bytes);  // weights + tokens land on the same barrier
+            tma_load_2d(sW + (size_t)it * kWBytes, &tmW, &full[it], kb * kTmaBoxK, tile * kWRows);
+          }
+      }
+      griddep_wait();
       uint32_t it = 0;
       for (int tile = cluster; tile < n_tiles; tile += n_clusters) {
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
           const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          mbar_wait_guard(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], stage_bytes);
+          if (it >= pre) {
+            const uint32_t ph = (it / stages) & 1;
+            mbar_wait_guard(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], stage_bytes);
+            tma_load_2d(sW + (size_t)s * kWBytes, &tmW, &full[s], kb * kTmaBoxK, tile * kWRows);
+          }
           if (it == 0) gtrace(2);
-          tma_load_2d(sW + (size_t)s * kWBytes, &tmW, &full[s], kb * kTmaBoxK, tile * kWRows);
           tma_load_2d(sX + (size_t)s * xbytes, &tmX, &full[s], kb * kTmaBoxK, 0);
         }
       }
+    } else {
+      griddep_wait();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -211,6 +228,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
   } else {
     // ===== epilogue warps: TMEM partial → pushed to the row's owner CTA → owner reduces its rows =====
+    griddep_wait();  // the residual (aux) and C's previous readers belong to earlier kernels
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int tid = threadIdx.x - 64;  // 0..127
@@ -294,6 +312,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
 }
 
+// SO_NO_PDL=1 launches K5c with plain stream serialization (A/B measurement); read once
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SO_NO_PDL");
+    return !(v && v[0] && v[0] != '0');
+  }();
+  return on;
+}
+
 struct GemvPlan {
   int NT, stages, CS, clusters, n_tiles;
 };
@@ -373,13 +400,17 @@ int launch_gemv(const GemvPlan& p, const CUtensorMap& mw, const CUtensorMap& mx,
   cfg.blockDim = dim3(kGThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = p.CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the kernel may start while its predecessor finishes; it prefetches
+  // weights, then griddepcontrol.wait()s before touching anything the predecessor wrote
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mw, mx, M, N, K, p.NT, p.stages, C, ldc, aux);
   if (e != cudaSuccess) return (int)e;
   SO_CHECK_LAUNCH();

@@ -29,6 +29,9 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const __nv_bfloat
                                                                const __nv_bfloat16* __restrict__ w, int H,
                                                                float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[kNormThreads / 32];
+  // a programmatically launched successor (K5c) may be scheduled now: it prefetches its weights and
+  // waits (griddepcontrol.wait) for this grid to finish before reading the normalised rows
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.x;
   const int vec = H / 8;
   const int4* xr = reinterpret_cast<const int4*>(x + (size_t)t * H);

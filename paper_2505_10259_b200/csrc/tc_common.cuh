@@ -107,6 +107,15 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
+// programmatic dependent launch: a kernel launched with programmatic stream serialization may start
+// before its predecessor in the stream finishes; griddep_wait() returns once every prerequisite grid
+// has completed and its memory is visible (immediately for a normally launched kernel).
+// griddep_launch_dependents() lets such a successor be scheduled early (its own wait still guards it).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
