@@ -529,9 +529,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // one CTA per SM at most (persistent grid): a programmatically launched successor (K5c) may take
-  // each SM as this grid's CTAs retire, prefetching its weights under this grid's tail
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < CF::kStages; ++s) {

@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const __nv_bfloat
                                                                float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[kNormThreads / 32];
   // a programmatically launched successor (K5c) may be scheduled now: it prefetches its weights and
-  // waits (griddepcontrol.wait) for this grid to finish before reading the normalised rows
+  // waits (griddepcontrol.wait) for this grid to finish before reading the normalised rows.  Only
+  // short kernels release early — a successor's CTAs spin on SMs the concurrent stream could use
+  // (the persistent GEMM releasing early cost the verify stream 13 %: profiles/kernels_r2.md)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.x;
   const int vec = H / 8;

@@ -506,6 +506,44 @@ def test_gemv_back_to_back_shapes():
             _bf16_close(out, ref)
 
 
+def test_gemv_programmatic_launch_reads_the_fresh_rows():
+    """K5c is launched with programmatic stream serialization: it may start while
+    its predecessor runs (rmsnorm and the persistent GEMM release it early) and
+    prefetches weights, but must read X and the residual only after the
+    predecessor finished.  A chain that rewrites X right before every K5c call
+    (rmsnorm → K5c with residual; persistent GEMM → K5c) must see each fresh X:
+    the outputs equal the same calls synchronised one by one."""
+    g = torch.Generator(device=DEV).manual_seed(11)
+    H, N, M = 4096, 4096, 64
+    w = torch.ones(H, dtype=torch.bfloat16, device=DEV)
+    W = (torch.randn(N, H, device=DEV, generator=g) / math.sqrt(H)).to(torch.bfloat16)
+    Wbig = (torch.randn(H, 2 * H, device=DEV, generator=g) / math.sqrt(2 * H)).to(torch.bfloat16)
+    xs = [torch.randn(M, H, device=DEV, generator=g).to(torch.bfloat16) for _ in range(12)]
+    big = [torch.randn(256, 2 * H, device=DEV, generator=g).to(torch.bfloat16) for _ in range(12)]
+    xn = torch.empty(M, H, dtype=torch.bfloat16, device=DEV)
+    ybig = torch.empty(256, H, dtype=torch.bfloat16, device=DEV)
+    outs = [torch.empty(M, N, dtype=torch.bfloat16, device=DEV) for _ in xs]
+    outs2 = [torch.empty(M, N, dtype=torch.bfloat16, device=DEV) for _ in xs]
+    for i, x in enumerate(xs):  # back to back, no host sync
+        native.rmsnorm(x, w, xn, 1e-5)
+        native.gemm(xn, W, outs[i], native.EPI_BF16_RESID, x)        # K5c, residual = x
+        native.gemm(big[i], Wbig, ybig, variant=1)                    # persistent tcgen05 GEMM writes ybig
+        native.gemm(ybig[:M], W, outs2[i], native.EPI_BF16)            # K5c reads it at once
+    torch.cuda.synchronize()
+    for i, x in enumerate(xs):
+        native.rmsnorm(x, w, xn, 1e-5)
+        torch.cuda.synchronize()
+        ref = torch.empty_like(outs[i])
+        native.gemm(xn, W, ref, native.EPI_BF16_RESID, x)
+        native.gemm(big[i], Wbig, ybig, variant=1)
+        torch.cuda.synchronize()
+        ref2 = torch.empty_like(outs2[i])
+        native.gemm(ybig[:M], W, ref2, native.EPI_BF16)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], ref), i
+        assert torch.equal(outs2[i], ref2), i
+
+
 def test_gemv_is_the_auto_choice_for_decode_steps():
     """Auto (variant 0) routes M ≤ 128 dense GEMMs to the decode-step kernel and
     larger M to the tiled kernels: same results either way within bf16."""
