@@ -162,7 +162,11 @@ int so_gemm_bf16_ex(const void* A, const void* B, int M, int N, int K, void* C, 
  * so_gemv_workspace_bytes returns 256 for shapes K5c serves (fewer weight
  * tiles than SMs) and 0 otherwise; the kernel itself needs no scratch (the
  * workspace arguments are accepted and ignored).  so_gemm_bf16_v (variant 0
- * or 4) routes eligible shapes here. */
+ * or 4) routes eligible shapes here.  Launched with programmatic stream
+ * serialization (PDL): it may start while the previous kernel on the stream
+ * finishes, prefetching weight tiles, and reads X / aux only after
+ * griddepcontrol.wait — stream semantics are unchanged for callers
+ * (environment SO_NO_PDL=1 launches it plainly). */
 size_t so_gemv_workspace_bytes(int M, int N, int K);
 int so_gemv_bf16(const void* X, const void* W, int M, int N, int K, void* C, int ldc, int epilogue,
                  const void* aux, void* workspace, size_t ws_bytes, void* stream);
