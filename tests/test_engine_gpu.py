@@ -503,6 +503,23 @@ def test_host_resident_kv_matches(pair, draft_kv, refill):
         _oracle_groups(tw, dw, prompts, 12, 4, 4)
 
 
+@pytest.mark.parametrize("refill", [False, True])
+def test_host_resident_kv_with_split_window(pair, refill):
+    """configs[1]'s combination: target KV in host DRAM, attention streamed with
+    the layer, XC4 units through the split window — the tokens of the resident
+    engine, with and without slot refill."""
+    tw, dw = pair
+    prompts = tiny.prompts(13 if refill else 8, seed=43)
+    pol = Policy(8, 4, 4, 4)
+    ref = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers=set()).generate(
+        prompts, 12, pol, draft_kv="reprefill", refill=refill)
+    eng = build_engine(TINY_TARGET, TINY_DRAFT, tw, dw, stream_layers={0, 1, 2, 3}, stream_attn=True,
+                       codec="xc4", split_window=True)
+    got = eng.generate(prompts, 12, pol, draft_kv="reprefill", refill=refill, kv_host=True)
+    assert type(eng.last_session.tkv).__name__ == "HostPagedKVCache"
+    assert got == ref
+
+
 def test_host_kv_refill_at_scale_does_not_stall():
     """Host-resident KV + slot refill at the capped configs[1] shapes (8 layers of
     the 8x7B target, 576 prompts through 192 slots) finishes; an intermittent
