@@ -95,7 +95,7 @@ def _layer_fp32(eng, li, L, unit, streamed, x, pos, state, bs, T, routing=None):
         g = ffn[: 2 * a.inter * H].view(a.inter // SWIGLU_BLOCK, 2, SWIGLU_BLOCK, H)
         gate = hn @ g[:, 0].reshape(a.inter, H).float().T
         up = hn @ g[:, 1].reshape(a.inter, H).float().T
-        return h + (torch.nn.functional.silu(gate) * up) @ ffn[2 * a.inter * H:].view(H, a.inter).float().T, None
+        return h + (torch.nn.functional.silu(gate) * up) @ ffn[2 * a.inter * H:3 * a.inter * H].view(H, a.inter).float().T, None
     lr = hn @ L.router.float().T
     if routing is None:
         top = torch.topk(lr, 2, dim=-1).indices
@@ -128,12 +128,11 @@ class _SegUnit:
 
     def __getitem__(self, sl):
         a = (sl.start or 0) + self.off
+        if sl.stop is None:  # an open-ended view: re-based, still resolved per slice
+            return _SegUnit(self.parts, a)
+        b = sl.stop + self.off
         for lo, t in self.parts:
             if lo <= a < lo + t.numel():
-                if sl.stop is None:
-                    return _SegUnit(self.parts, a) if a - lo else (
-                        t if len(self.parts) == 1 or lo == self.parts[-1][0] else _SegUnit(self.parts, a))
-                b = sl.stop + self.off
                 assert b <= lo + t.numel(), "slice spans two window segments"
                 return t[a - lo:b - lo]
         raise IndexError(sl)
