@@ -65,6 +65,10 @@ def main():
         ("8x22B LM head (T 2232)", 2232, 32768, 6144, native.EPI_F32, 0),
         ("Mistral-7B re-prefill gate_up (64 seqs x 520)", 33280, 28672, 4096, native.EPI_SWIGLU, 0),
         ("Mistral-7B re-prefill down", 33280, 4096, 14336, native.EPI_BF16_RESID, 0),
+        ("Mistral-7B re-prefill O", 33280, 4096, 4096, native.EPI_BF16_RESID, 0),
+        ("Mistral-7B re-prefill QKV", 33280, 6144, 4096, native.EPI_BF16, 0),
+        ("Mistral-7B re-prefill down (32 seqs x 520)", 16640, 4096, 14336, native.EPI_BF16_RESID, 0),
+        ("Mistral-7B re-prefill gate_up (32 seqs x 520)", 16640, 28672, 4096, native.EPI_SWIGLU, 0),
         ("square 8192^3", 8192, 8192, 8192, native.EPI_BF16, 0),
         ("draft decode step QKV (64 seqs)", 64, 6144, 4096, native.EPI_BF16, 0),
         ("draft decode step O (64 seqs)", 64, 4096, 4096, native.EPI_BF16_RESID, 0),
