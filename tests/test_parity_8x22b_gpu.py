@@ -158,7 +158,7 @@ def _oracle_arch(a):
 
 
 def _layer_parity(arch, model_of, stream_layers, codec, n_seq=32, n_cand=8, ctx=503, seed=7, stream_attn=False,
-                  draft=None):
+                  draft=None, split_window=False):
     """Verify pass of n_seq sequences × (n_cand + 1) tokens over ctx positions of
     shared random KV, engine vs oracle.  Returns (got, want, router_gap, want_fp32):
     ``want`` mirrors the kernels' bf16 rounding points, ``want_fp32`` keeps fp32."""
@@ -176,7 +176,7 @@ def _layer_parity(arch, model_of, stream_layers, codec, n_seq=32, n_cand=8, ctx=
     kv_np.v[0, :, :ctx] = v_ctx.float().cpu().numpy()
     if arch.is_moe:
         eng = build_engine(arch, draft or MISTRAL_7B_V3_1L, W, None, stream_layers=stream_layers, codec=codec,
-                           trace=False, stream_attn=stream_attn)
+                           trace=False, stream_attn=stream_attn, split_window=split_window)
     else:
         eng = build_engine(MIXTRAL_1L_TINYFFN, arch, None, W, stream_layers=set(), trace=False)
     model = model_of(eng)
@@ -264,12 +264,16 @@ def _check_logits(got, want, exclude=None, want32=None):
     return float(d.max()), float(decisive.mean())
 
 
-def test_mixtral_8x22b_layer_and_lm_head_vs_oracle():
+@pytest.mark.parametrize("split", [False, True])
+def test_mixtral_8x22b_layer_and_lm_head_vs_oracle(split):
+    """``split``: the unit streams through the split window ([gate_up | down], one XC4 unit per
+    segment) — the same oracle bar."""
     a = dataclasses.replace(MIXTRAL_8X22B, n_layer=1)
-    got, want, gap, want32 = _layer_parity(a, lambda e: e.target, {0}, "xc4")
+    got, want, gap, want32 = _layer_parity(a, lambda e: e.target, {0}, "xc4", split_window=split)
     near = gap < 1e-3
     maxd, dec = _check_logits(got, want, exclude=near, want32=want32)
-    print(f"8x22B layer: max |Δlogit| {maxd:.4f}, decisive rows {dec:.2f}, near-tie routed tokens {near.sum()}")
+    print(f"8x22B layer (split {split}): max |Δlogit| {maxd:.4f}, decisive rows {dec:.2f}, "
+          f"near-tie routed tokens {near.sum()}")
 
 
 def test_mistral_7b_draft_layer_and_lm_head_vs_oracle():
@@ -281,12 +285,14 @@ def test_mistral_7b_draft_layer_and_lm_head_vs_oracle():
 
 def test_mixtral_8x7b_streamed_attention_layer_vs_oracle():
     """configs[1]'s layout (HBM capped at 24 GiB): the attention projections travel
-    inside the streamed XC4 unit with the FFN (H3), Mixtral-8x7B shapes."""
+    inside the streamed XC4 unit with the FFN (H3) through the split window
+    ([Wqkv | Wo | gate_up] | down), Mixtral-8x7B shapes."""
     from paper_2505_10259_b200 import MIXTRAL_8X7B, MISTRAL_7B
 
     a = dataclasses.replace(MIXTRAL_8X7B, n_layer=1)
     d = dataclasses.replace(MISTRAL_7B, n_layer=1)
-    got, want, gap, want32 = _layer_parity(a, lambda e: e.target, {0}, "xc4", n_seq=16, stream_attn=True, draft=d)
+    got, want, gap, want32 = _layer_parity(a, lambda e: e.target, {0}, "xc4", n_seq=16, stream_attn=True, draft=d,
+                                           split_window=True)
     near = gap < 1e-3
     maxd, dec = _check_logits(got, want, exclude=near, want32=want32)
     print(f"8x7B streamed-attention layer: max |Δlogit| {maxd:.4f}, decisive rows {dec:.2f}")
