@@ -124,9 +124,11 @@ def test_measured_trace_invariants_8x22b_shapes(split):
         assert_causality(back.trace)
 
 
-def test_hbm_contract_capped_plan():
+@pytest.mark.parametrize("split", [False, True])
+def test_hbm_contract_capped_plan(split):
     """a10: the measured allocator peak of a plan-built engine at the configs[1]
-    cap (24 GiB, 8x7B-shaped, 4 layers) stays within the plan's hbm_bytes."""
+    cap (24 GiB, 8x7B-shaped, 4 layers) stays within the plan's hbm_bytes —
+    with the whole window and with the split window the plan charges one unit for."""
     from paper_2505_10259_b200 import MIXTRAL_8X7B, MISTRAL_7B
     from paper_2505_10259_b200.planner_b200 import B200Rates, plan_offload
 
@@ -135,11 +137,13 @@ def test_hbm_contract_capped_plan():
     cap = 12 * 2**30
     n_cand, ctx, max_new = 4, 256, 20
     plan = plan_offload(t, d, cap, int(40e9), n_cand, 0.8, ctx, max_new, B200Rates(), bs_candidates=[32, 64],
-                        kv_host_modes=(False,), draft_kv_modes=("cached",))
+                        kv_host_modes=(False,), draft_kv_modes=("cached",), split_window=split)
+    assert plan.split_window == split
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     base = torch.cuda.memory_allocated()
-    eng = build_engine(t, d, stream_layers=set(plan.stream_layers), stream_attn=plan.stream_attn, trace=False)
+    eng = build_engine(t, d, stream_layers=set(plan.stream_layers), stream_attn=plan.stream_attn, trace=False,
+                       split_window=plan.split_window)
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()  # decoding peak: weights + window + KV + workspaces (not init scratch)
     S = 2 * plan.bs_decoding
