@@ -475,6 +475,8 @@ def main():
     if world > 1:
         dist.barrier()
     log("timed rounds done")
+    hbm_peak = int(torch.cuda.max_memory_allocated(device))  # allocator peak of setup + decode so far
+    hbm_reserved = int(torch.cuda.memory_reserved(device))
     clk = clocks.stop()
     dev_s = ev0.elapsed_time(ev1) * 1e-3
     committed = s.committed_decode - committed0
@@ -736,6 +738,10 @@ def main():
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(streamed / steps + meta_bytes),
                 "d2h_bytes_per_step": int(bs * (args.n_cand + 2) * 4)},
         "plan": plan.as_dict(),
+        "hbm": {"budget": int(hbm), "planned": int(sum(plan.hbm_bytes.values())), "peak_allocated": hbm_peak,
+                "reserved": hbm_reserved,
+                "note": "planned = the plan's hbm_bytes (weights, window, KV, workspaces); peak_allocated = "
+                        "torch.cuda.max_memory_allocated after the timed rounds"},
     }
     if gen is not None:
         line["e2e_generate"] = gen
