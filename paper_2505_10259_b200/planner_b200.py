@@ -184,7 +184,7 @@ def plan_offload(target: ModelArch, draft: ModelArch, hbm_budget: int, host_budg
     max_len = ctx_len + max_new + n_cand + 2
     draft_w = resident_bytes(draft, True)
     best = None
-    cands = bs_candidates or [b for b in range(8, 2049, 8)]
+    cands = bs_candidates or [b for b in range(8, 2049, 4)]  # 4-sequence steps: 1 GB of 8x22B KV per step
     attn_layer = attn_elems(target) * 2
     for stream_attn, mode, kv_host in [(sa, m, kh) for sa in stream_attn_modes for m in draft_kv_modes
                                         for kh in kv_host_modes]:
