@@ -567,6 +567,8 @@ class LayerStreamer:
             del evs[n_slots:]
             evs.extend(native.Event() for _ in range(n_slots - len(evs)))
         self.n_slots = n_slots
+        # the dropped uses are re-issued (and re-traced) under the new map
+        self.copy_marks = [m for m in self.copy_marks if m[0] < self.k_use]
         self.k_issued = self.k_base = self.k_use
 
     def _ensure_issued(self, upto: int) -> None:
